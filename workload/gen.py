@@ -1,0 +1,147 @@
+"""Seeded synthetic-input generator shared by the oracle tests and the CUDA path.
+
+It holds NONE of the method's arithmetic (no CNN, ZF, precoding, DFT, GMP or
+slicing).  It only draws the random inputs of the chain, with the recipe of
+SURVEY.md §8(c) readings A6, A7, A10, A14, A15 and §8(d):
+
+  stream 0  QAM indices, one substream per OFDM symbol n
+  stream 1  Rayleigh taps H_t, T x U x B
+  stream 2  per-antenna PA coefficient spread              (A15)
+  stream 3  CNN weights, stream 4 CNN biases               (A6)
+
+Every stream is ``numpy.random.Generator(PCG64(SeedSequence([seed, stream, index])))``
+so any symbol can be regenerated alone (any rank, any subset).
+
+The canonical arrays are float32 / complex64 (what the GPU consumes); the oracle
+upcasts them exactly to float64 / complex128.
+
+QAM symbol values (needed as the chain's input s) are the square M-QAM grid of
+SPEC.md:116 / SURVEY §8(c) step 1: level 2i-(m-1), unit average energy.  The
+oracle re-derives them independently from the indices (tests pin the two).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .configs import ChainConfig
+
+STREAM_SYMBOLS = 0
+STREAM_CHANNEL = 1
+STREAM_SPREAD = 2
+STREAM_CNN_W = 3
+STREAM_CNN_B = 4
+
+
+def rng(seed: int, stream: int, index: int = 0) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, stream, index])))
+
+
+# ----------------------------------------------------------------------------- symbols
+def qam_indices(cfg: ChainConfig, symbols) -> np.ndarray:
+    """uint16 [len(symbols)][U][N_d], i.i.d. uniform in [0, M_qam)."""
+    out = np.empty((len(symbols), cfg.U, cfg.N_d), dtype=np.uint16)
+    for i, n in enumerate(symbols):
+        out[i] = rng(cfg.seed, STREAM_SYMBOLS, int(n)).integers(
+            0, cfg.M_qam, size=(cfg.U, cfg.N_d), dtype=np.uint16)
+    return out
+
+
+def qam_symbols(idx: np.ndarray, M_qam: int) -> np.ndarray:
+    """complex64 points for indices: I = idx mod m, Q = idx div m (fixed map, A19)."""
+    m = int(round(np.sqrt(M_qam)))
+    scale = np.sqrt(3.0 / (2.0 * (M_qam - 1)))
+    i = (idx.astype(np.int64) % m) * 2 - (m - 1)
+    q = (idx.astype(np.int64) // m) * 2 - (m - 1)
+    return ((i + 1j * q) * scale).astype(np.complex64)
+
+
+# ----------------------------------------------------------------------------- channel
+def pdp(cfg: ChainConfig) -> np.ndarray:
+    """Power-delay profile p_t, sum 1: uniform 1/T or 3 dB/tap decay (BASELINE)."""
+    if cfg.pdp == "uniform":
+        p = np.full(cfg.T, 1.0 / cfg.T)
+    elif cfg.pdp == "exp3dB":
+        p = 10.0 ** (-0.3 * np.arange(cfg.T))
+        p = p / p.sum()
+    else:
+        raise ValueError(cfg.pdp)
+    return p
+
+
+def channel_taps(cfg: ChainConfig) -> np.ndarray:
+    """complex64 [T][U][B]; entries CN(0, p_t), i.i.d.."""
+    g = rng(cfg.seed, STREAM_CHANNEL)
+    z = g.standard_normal((cfg.T, cfg.U, cfg.B, 2))
+    h = (z[..., 0] + 1j * z[..., 1]) * np.sqrt(pdp(cfg) / 2.0)[:, None, None]
+    return h.astype(np.complex64)
+
+
+# ----------------------------------------------------------------------------- PA bank
+# Nominal a_{p,0} (BASELINE C1 gives p = 1, 3, 5; 7 and 9 invented, reading A14).
+NOMINAL_A0 = {1: 1.0 + 0.0j, 3: -0.08 + 0.02j, 5: 0.01 - 0.005j,
+              7: -1e-3 + 5e-4j, 9: 1e-4 - 5e-5j}
+
+
+def gmp_nominal(cfg: ChainConfig) -> np.ndarray:
+    """complex128 [n_coef] in the flattened order of SURVEY §8(b):
+    a[p][l] for p in orders, l = 0..L; then b[p][l][g] for p >= 3, l, g = 1..M;
+    then c[p][l][g] likewise.  Values per reading A14."""
+    a = []
+    for p in cfg.orders:
+        for l in range(cfg.L + 1):
+            a.append(NOMINAL_A0[p] * (1.0 if l == 0 else 0.05 * 0.5 ** (l - 1)))
+    bc = []
+    for p in cfg.orders[1:]:
+        for l in range(cfg.L + 1):
+            for g in range(1, cfg.M + 1):
+                bc.append(NOMINAL_A0[p] * 0.02 * 0.5 ** l * 0.5 ** (g - 1))
+    return np.array(a + bc + bc, dtype=np.complex128)
+
+
+def gmp_coefficients(cfg: ChainConfig) -> np.ndarray:
+    """complex64 [B][n_coef]: nominal * (1 + delta), delta ~ U[-spread, spread] real,
+    i.i.d. per (antenna, coefficient), frozen per seed (reading A15)."""
+    nom = gmp_nominal(cfg)
+    d = rng(cfg.seed, STREAM_SPREAD).uniform(-cfg.spread, cfg.spread, size=(cfg.B, nom.size))
+    return (nom[None, :] * (1.0 + d)).astype(np.complex64)
+
+
+def gmp_identity(cfg: ChainConfig) -> np.ndarray:
+    """a_{1,0} = 1, all else 0 on every antenna: the linear PA of PAPER.md:94."""
+    c = np.zeros((cfg.B, cfg.n_coef), dtype=np.complex64)
+    c[:, 0] = 1.0
+    return c
+
+
+# ----------------------------------------------------------------------------- CNN
+def cnn_params(cfg: ChainConfig) -> np.ndarray:
+    """float32 flat parameter vector: per layer W[co][ci][3][3] then b[co].
+    All entries N(0, w_std^2) (reading A6)."""
+    gw = rng(cfg.seed, STREAM_CNN_W)
+    gb = rng(cfg.seed, STREAM_CNN_B)
+    parts = []
+    for ci, co in zip(cfg.chans[:-1], cfg.chans[1:]):
+        parts.append(gw.normal(0.0, cfg.w_std, size=co * ci * 9))
+        parts.append(gb.normal(0.0, cfg.w_std, size=co))
+    return np.concatenate(parts).astype(np.float32)
+
+
+def cnn_zero(cfg: ChainConfig) -> np.ndarray:
+    return np.zeros(cfg.n_params, dtype=np.float32)
+
+
+# ----------------------------------------------------------------------------- bundle
+def make_inputs(cfg: ChainConfig, symbols=None, *, zero_cnn=False, linear_pa=False):
+    """All inputs of one run (or of a subset of its symbols)."""
+    if symbols is None:
+        symbols = range(cfg.n_sym)
+    symbols = list(symbols)
+    idx = qam_indices(cfg, symbols)
+    return {
+        "symbols": np.array(symbols, dtype=np.int64),
+        "idx": idx,
+        "s": qam_symbols(idx, cfg.M_qam),
+        "h_taps": channel_taps(cfg),
+        "coef": gmp_identity(cfg) if linear_pa else gmp_coefficients(cfg),
+        "params": cnn_zero(cfg) if zero_cnn else cnn_params(cfg),
+    }
