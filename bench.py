@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the FD-CNN DPD downlink hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step = one pass of the whole hot path over one batch
+of synthetic OFDM symbols of BASELINE.json configs[1] (C2: U=4, B=64, N_ifft=4096,
+1024 symbols): FD-CNN -> fused precode/IDFT/GMP (PA waveform written to HBM) ->
+receive DFT + channel sum + slicing/SER.  The ZF precoder (a2) is built once per
+channel realisation before timing (reading A10) and timed separately.
+
+Multi-GPU (torchrun): symbol-batch sharding, weak scaling — each rank runs its
+own 1024-symbol batch (symbol indices rank*n_sym + i); the only collective is
+the int64 SER-counter all-reduce at the end of each step.  Timing: CUDA events
+per step on the launching stream, L2 flushed between steps (256 MiB write,
+outside the events), barrier + synchronize around the timed loop, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from workload import configs, gen  # noqa: E402
+
+METRIC = "OFDM symbols/s through DPD+precode+IFFT+GMP chain; % HBM roofline"
+FP32_LANES_PER_SM = 128          # FP32 FMA lanes per SM (Blackwell SM: 4 SMSP x 32)
+
+
+def peaks():
+    p = {"hbm_gbs": 6538.9, "sm_max_mhz": 1965.0, "src": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        p.update({"hbm_gbs": m.get("hbm_gbs", p["hbm_gbs"]), "sm_max_mhz": m.get("sm_max_mhz", p["sm_max_mhz"]),
+                  "src": "measured"})
+    return p
+
+
+def gmp_flop_per_sample(cfg):
+    """3 (envelope) + (Kp-2) (powers) + (L+1)[4(Kp-1)(2M+1) + 8]."""
+    return 3 + (cfg.Kp - 2) + (cfg.L + 1) * (4 * (cfg.Kp - 1) * (2 * cfg.M + 1) + 8)
+
+
+def chain_tx_flop_per_symbol(cfg):
+    """Algorithmic FLOPs of the fused precode + IDFT + GMP per OFDM symbol."""
+    N = cfg.N_ifft
+    return (8 * cfg.B * cfg.U * cfg.N_d                       # precode, Eq. (1)
+            + 5 * N * int(np.log2(N)) * cfg.B                  # IDFT, 5 N log2 N (P:165 convention)
+            + gmp_flop_per_sample(cfg) * N * cfg.B)            # GMP, Eq. (9)
+
+
+def chain_bytes_per_symbol(cfg):
+    """Algorithmic HBM bytes of the step per symbol: read s, idx; write y (PA waveform) once,
+    read it back for the receive; write yhat; P and h_fd amortised over the batch."""
+    s = 8 * cfg.U * cfg.N_d
+    y = 8 * cfg.B * cfg.N_ifft
+    return s + 2 * cfg.U * cfg.N_d + 2 * y + s + (16 * cfg.B * cfg.U * cfg.N_d) / cfg.n_sym
+
+
+# ============================================================================ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v.lower() == "active"})
+        loaded = [r for r in rows if r[2] > 200.0] or rows
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(r[2] for r in rows)}
+
+
+# ============================================================================ oracle timing
+def oracle_symbols_per_s(cfg, symbols, rank_seed_offset=0):
+    """Time the fp64 oracle (as it stands) on a bounded sample: the per-step stages
+    (CNN, precode, IDFT, GMP, receive, slice) over `symbols`; ZF built untimed, like the GPU."""
+    from oracle import fdpd_oracle as O
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    inp = gen.make_inputs(cfg, symbols)
+    Hfd = O.channel_fd(inp["h_taps"], cfg.N_ifft, cfg.N_d)
+    P, alpha, _ = O.zf_precoder(Hfd, cfg.N_ifft, cfg.rho)
+
+    def run():
+        t0 = time.perf_counter()
+        for i in range(len(symbols)):
+            s = inp["s"][i:i + 1]
+            st = O.fdcnn_forward(s, inp["params"], cfg.chans, cfg.N_d)
+            x = O.ofdm_modulate(O.precode(P, st), cfg.N_ifft)
+            y = O.gmp_pa(x, inp["coef"], cfg.orders, cfg.L, cfg.M)
+            O.slice_ser(O.ue_receive(y, Hfd, cfg.N_d), alpha, inp["idx"][i:i + 1], cfg.M_qam)
+        return time.perf_counter() - t0
+
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1):
+            dt = run()
+    else:
+        dt = run()
+    return len(symbols) / dt, dt
+
+
+# ============================================================================ main arms
+def init_dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = init_dist()
+    if rank != 0:
+        return
+    k = max(1, args.ref_step_symbols)
+    for _ in range(args.warmup):
+        oracle_symbols_per_s(cfg, list(range(1)))
+    times = []
+    for st in range(args.steps):
+        _, dt = oracle_symbols_per_s(cfg, list(range(st * k, st * k + k)))
+        times.append(dt)
+    total = sum(times)
+    value = args.steps * k / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, ws, k),
+        "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{k} symbols of {cfg.name} per step, fp64 numpy oracle, 1 BLAS thread"},
+        "e2e": {"value": value, "unit": "symbols/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, ws, batch):
+    return {"workload": cfg.name, "U": cfg.U, "B": cfg.B, "N_ifft": cfg.N_ifft, "N_d": cfg.N_d, "M_qam": cfg.M_qam,
+            "gmp": {"orders": list(cfg.orders), "L": cfg.L, "M": cfg.M}, "cnn_chans": list(cfg.chans),
+            "symbols_per_gpu_per_step": batch, "global_batch_symbols": batch * ws,
+            "parallelism": f"symbol-batch x{ws}", "l2": "flushed between steps (256 MiB write outside the events)"}
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_05158_b200 import fdpd
+    from paper_2205_05158_b200.chain import Chain, Shapes
+
+    ws, rank, local = init_dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    fdpd.lib()
+    n = args.batch or cfg.n_sym
+    symbols = range(rank * n, rank * n + n)
+    inp = gen.make_inputs(cfg, symbols)
+
+    t_zf0 = time.perf_counter()
+    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device=dev, max_batch=n)
+    torch.cuda.synchronize()
+    t_zf = time.perf_counter() - t_zf0
+
+    s = torch.from_numpy(inp["s"]).to(dev)
+    idx = torch.from_numpy(inp["idx"]).to(dev)
+    counts = torch.zeros(3, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        st = ch.dpd(s)
+        if ev is not None:
+            ev[0].record(stream)
+        y = ch.tx(st)
+        if ev is not None:
+            ev[1].record(stream)
+        ch.rx(y, idx, counts=counts)
+        if ev is not None:
+            ev[2].record(stream)
+        if ws > 1:
+            dist.all_reduce(counts)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    evs = [(E(), E(), E(), E(), E()) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step(ev=(evs[i][1], evs[i][2], evs[i][3]))
+            evs[i][4].record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        # end-to-end: pinned host inputs copied in, counts read back, every step
+        s_h = torch.from_numpy(inp["s"]).pin_memory()
+        i_h = torch.from_numpy(inp["idx"]).pin_memory()
+        c_h = torch.zeros(3, dtype=torch.int64).pin_memory()
+        s_d = torch.empty_like(s)
+        i_d = torch.empty_like(idx)
+        e2e_ev = [(E(), E()) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.zero_()
+            e2e_ev[i][0].record(stream)
+            s_d.copy_(s_h, non_blocking=True)
+            i_d.copy_(i_h, non_blocking=True)
+            counts.zero_()
+            ch.step(s_d, i_d, counts=counts)
+            if ws > 1:
+                dist.all_reduce(counts)
+            c_h.copy_(counts, non_blocking=True)
+            e2e_ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    ms = sum(e[0].elapsed_time(e[4]) for e in evs)
+    ms_e2e = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    st_dpd = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    st_tx = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    st_rx = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    t = torch.tensor([ms, ms_e2e, st_tx], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ms_e2e, st_tx = t.tolist()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    total_symbols = n * ws * args.steps
+    value = total_symbols / (ms / 1e3)
+    pk = peaks()
+    fp32_peak = 148 * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12       # TFLOP/s
+    tx_flop = chain_tx_flop_per_symbol(cfg) * n
+    achieved = tx_flop / (st_tx / 1e3) / 1e12
+    bytes_sym = chain_bytes_per_symbol(cfg)
+    hbm_achieved = bytes_sym * n * args.steps / (ms / 1e3) / 1e9
+    launches_per_step = (len(cfg.chans) - 1) + 1 + 2
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1 or (rank == 0 and not args.no_cpu_baseline):
+        k = args.ref_symbols
+        v, dt = oracle_symbols_per_s(cfg, list(range(k)))
+        cpu = {"value": v, "unit": "symbols/s", "cores": 1, "kind": "oracle",
+               "sample": f"{k} symbols of {cfg.name} (per-step stages, ZF untimed), fp64 numpy, 1 BLAS thread, "
+                         f"{dt:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, workload/gen.py)",
+        "config": config_dict(cfg, ws, n),
+        "roofline": {"kernel": "chain_tx (precode+IDFT+GMP fused)", "bound": "alu", "achieved": achieved,
+                     "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                     "peak_src": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
+                     "flop_per_symbol": chain_tx_flop_per_symbol(cfg), "ms_per_launch": st_tx},
+        "hbm": {"algorithmic_bytes_per_symbol": bytes_sym, "achieved_GBps": hbm_achieved, "peak_GBps": pk["hbm_gbs"],
+                "frac": hbm_achieved / pk["hbm_gbs"], "peak_src": pk["src"]},
+        "stage_ms": {"fdcnn": st_dpd, "chain_tx": st_tx, "ue_receive_ser": st_rx, "zf_build_once_s": t_zf},
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_symbols / (ms_e2e / 1e3), "unit": "symbols/s",
+                "h2d_bytes_per_step": int(inp["s"].nbytes + inp["idx"].nbytes), "d2h_bytes_per_step": 24},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=0, help="symbols per GPU per step (default: the config's n_sym)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-symbols", type=int, default=64, help="oracle symbols per CPU sample (~10 s)")
+    ap.add_argument("--ref-step-symbols", type=int, default=4, help="oracle symbols per --impl reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    cfg = configs.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

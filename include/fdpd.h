@@ -1,0 +1,166 @@
+/*
+ * fdpd.h — C ABI of libfdpd.so, the B200 (sm_100a) hot path of the FD-CNN DPD
+ * massive MU-MIMO-OFDM downlink chain of arXiv 2205.05158 (PAPER.md = P:n).
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - Array pointers are CUDA DEVICE memory owned by the caller (e.g. torch
+ *    tensors), contiguous, 16-byte aligned.  Small shape descriptors (chans,
+ *    orders) are HOST int arrays.  "complex64" = interleaved {float re, im}
+ *    (== torch.complex64 / std::complex<float>).
+ *  - Calls are asynchronous on `stream`, never allocate and never synchronise,
+ *    except zf_precoder_build (which returns alpha to the host) and the
+ *    fd_chain_* runtime (documented there).
+ *  - Errors: FD_ERR_ARG for bad sizes / null or misaligned pointers (nothing is
+ *    launched); FD_ERR_NUMERIC when a Gram matrix is not positive definite;
+ *    FD_ERR_CUDA for launch/runtime errors.  fd_last_error() returns a
+ *    thread-local message for the last non-OK status.
+ *  - Subcarrier map (reading A7): data subcarrier j = 0..N_d-1 sits at IDFT bin
+ *    k_j = (j - N_d/2) mod N_ifft; guards are zero.
+ *  - Threads: reentrant; the library's only state is an immutable per-N_ifft
+ *    twiddle-table cache (freed by fd_shutdown()).
+ */
+#ifndef FDPD_H
+#define FDPD_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FD_OK = 0,
+    FD_ERR_ARG = 2,      /* bad dims / pointer / alignment (SPEC exit code 2) */
+    FD_ERR_NUMERIC = 3,  /* Gram matrix not positive definite (SPEC exit code 3) */
+    FD_ERR_CUDA = 4      /* CUDA launch / runtime error */
+} fd_status;
+
+/* Thread-local message describing the last non-OK status of this thread. */
+const char* fd_last_error(void);
+/* ABI version (major*100 + minor). */
+int fd_version(void);
+/* Release cached plan data (twiddle tables).  Safe to call at any time when no
+ * call is in flight. */
+void fd_shutdown(void);
+
+/* -------------------------------------------------------------------------
+ * a1. FD-CNN forward — P:167-177 (structure, Eq. 15), BASELINE residual conv
+ * stack (SURVEY §8(c) readings A1-A6).
+ *
+ * For each (symbol n, UE u): the N_d-vector s_in[n][u][:] is laid out row-major
+ * in an S x S image, S = ceil(sqrt(N_d)), tail zero-padded; channels
+ * [Re, Im]; n_layers 3x3 "same" zero-padded cross-correlation layers
+ * with bias, tanh after every layer but the last; residual output
+ * s_out = s_in + (h[0] + j h[1]) on the first N_d pixels.
+ *
+ *  params    device float, per layer l: W[co][ci][3][3] then b[co], layers
+ *            concatenated (sum_l co*ci*9 + co floats).
+ *  chans     HOST int[n_layers+1]; chans[0] = chans[n_layers] = 2; each <= 256.
+ *  s_in      device complex64 [n_sym][U][N_d].
+ *  s_out     device complex64 [n_sym][U][N_d]; must not alias s_in.
+ *  workspace device scratch of >= fdcnn_workspace_bytes(...) bytes (may be NULL
+ *            when that returns 0).
+ * ------------------------------------------------------------------------- */
+size_t fdcnn_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d);
+int fdcnn_forward(const float* params, const int* chans, int n_layers,
+                  const void* s_in, void* s_out, void* workspace, size_t workspace_bytes,
+                  long long n_sym, int U, int N_d, cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
+ * a2. Zero-forcing precoder build — Eq. (6), FD channel P:72 (A9),
+ * power normalisation P:84 (reading A12).  Once per channel realisation.
+ *
+ *   Hfd_j = sum_t H_t exp(-j 2 pi k_j t / N_ifft)          (U x B)
+ *   G_j   = Hfd_j Hfd_j^H ;  P0_j = Hfd_j^H G_j^-1          (B x U)
+ *   alpha = rho * sqrt(B * N_ifft / sum_j tr(G_j^-1))        (mean TD |x|^2 = rho^2)
+ *   P_j   = alpha * P0_j
+ * Gram, Cholesky and inverse in fp64; outputs complex64.
+ *
+ *  h_taps    device complex64 [T][U][B] (full array, every rank).
+ *  b0,B_loc  emit antenna rows [b0, b0+B_loc) only (antenna sharding).
+ *  h_fd      device complex64 out [U][B_loc][N_d].
+ *  P         device complex64 out [B_loc][U][N_d] (alpha folded in).
+ *  alpha     HOST float out.  The call synchronises `stream`.
+ *  workspace device scratch >= zf_workspace_bytes(N_d) bytes.
+ *  Returns FD_ERR_NUMERIC if any G_j is not numerically positive definite.
+ * ------------------------------------------------------------------------- */
+size_t zf_workspace_bytes(int N_d);
+int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N_d, float rho,
+                      int b0, int B_loc, void* h_fd, void* P, float* alpha,
+                      void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
+ * a3. Precode — Eq. (1):  X[n][b][j] = sum_u P[b][u][j] * s[n][u][j].
+ *  P [B_loc][U][N_d], s [n_sym][U][N_d] -> X [n_sym][B_loc][N_d], complex64.
+ * ------------------------------------------------------------------------- */
+int precode(const void* P, const void* s, void* X,
+            long long n_sym, int B_loc, int U, int N_d, cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
+ * a4. OFDM IDFT — Eq. (2) P:54-57 (unitary, guards zero):
+ *   x[n][b][m] = N^-1/2 sum_j X[n][b][j] exp(+j 2 pi k_j m / N),  N = N_ifft.
+ *  X [n_sym][B][N_d] -> x [n_sym][B][N_ifft], complex64.
+ *  N_ifft power of two, 16 <= N_ifft <= 16384, N_d even, N_d <= N_ifft.
+ * ------------------------------------------------------------------------- */
+int ofdm_modulate(const void* X, void* x, long long n_sym, int B, int N_d, int N_ifft,
+                  cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
+ * a5. GMP PA — Eq. (9) P:113-122 as the PA f_b of Eq. (7) P:89-93,
+ * odd orders p <-> |u|^(p-1), l = 0..L, g = 1..M, circular within the symbol
+ * (reading A13):
+ *   y_m = sum_p sum_l a_{p,l} u_{m-l} |u_{m-l}|^(p-1)
+ *       + sum_{p>=3} sum_l sum_g ( b_{p,l,g} u_{m-l} |u_{m-l-g}|^(p-1)
+ *                                + c_{p,l,g} u_{m-l} |u_{m-l+g}|^(p-1) )
+ *  x    device complex64 [n_sym][B][N_ifft]; y same shape, must not alias x.
+ *  coef device complex64 [B][n_coef], flattened a[p][l]; b[p>=3][l][g]; c[p>=3][l][g];
+ *       n_coef = Kp(L+1) + 2(Kp-1)(L+1)M.
+ *  orders HOST int[n_orders], odd, ascending, orders[0] = 1, n_orders <= 8;
+ *  0 <= L <= 15, 0 <= M <= 7 (M = 0: no cross terms), L + 2M < N_ifft.
+ * ------------------------------------------------------------------------- */
+int gmp_pa(const void* x, const void* coef, void* y, const int* orders, int n_orders,
+           int L, int M, long long n_sym, int B, int N_ifft, cudaStream_t stream);
+
+/* Fused a3 -> a4 -> a5 (one CTA per (symbol, antenna); X and x never touch HBM).
+ * Numerically equivalent to precode -> ofdm_modulate -> gmp_pa.
+ *  P [B_loc][U][N_d], s_tilde [n_sym][U][N_d], coef [B_loc][n_coef] -> y [n_sym][B_loc][N_ifft]. */
+int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y,
+             const int* orders, int n_orders, int L, int M,
+             long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
+ * a6. Evaluation — Eqs. (4)-(5) P:67-77 (noiseless, reading A11), SER P:351.
+ *
+ * ue_receive: XPA[n][b][j] = N^-1/2 sum_m y[n][b][m] exp(-j 2 pi k_j m / N);
+ *             yhat[n][u][j] (+)= sum_{b<B_loc} h_fd[u][b][j] * XPA[n][b][j].
+ *  y [n_sym][B_loc][N_ifft], h_fd [U][B_loc][N_d] -> yhat [n_sym][U][N_d], complex64.
+ *  accumulate != 0 adds into yhat (antenna shards / chunks); 0 overwrites.
+ *  workspace >= ue_receive_workspace_bytes(...) bytes (holds XPA).
+ *
+ * ue_slice_ser: z = yhat / alpha (genie alpha, A17); per-axis nearest odd level
+ *  d = clip(2 floor(v/2) + 1, -(m-1), m-1), v = Re|Im z / c, c = (2(M_qam-1)/3)^-1/2;
+ *  dec = (d_I + m-1)/2 + m (d_Q + m-1)/2 ; counts[0] += #(dec != tx_idx),
+ *  counts[1] += n_sym*U*N_d, counts[2] += #samples within boundary_eps of an
+ *  interior boundary.  tx_idx uint16 [n_sym][U][N_d]; dec nullable; counts device
+ *  int64[3] (accumulated: the caller zeroes it).
+ * ------------------------------------------------------------------------- */
+size_t ue_receive_workspace_bytes(long long n_sym, int B_loc, int N_d);
+int ue_receive(const void* y, const void* h_fd, void* yhat, void* workspace, size_t workspace_bytes,
+               long long n_sym, int B_loc, int U, int N_d, int N_ifft, int accumulate,
+               cudaStream_t stream);
+int ue_slice_ser(const void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                 uint16_t* dec, long long* counts, long long n_sym, int U, int N_d,
+                 float boundary_eps, cudaStream_t stream);
+/* ue_receive (accumulate = 0) then ue_slice_ser, single GPU. */
+int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace, size_t workspace_bytes,
+                   float alpha, const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts,
+                   long long n_sym, int B_loc, int U, int N_d, int N_ifft, float boundary_eps,
+                   cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDPD_H */

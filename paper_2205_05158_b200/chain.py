@@ -1,0 +1,90 @@
+"""Device-resident state and one step of the hot path, on top of the C ABI.
+
+``Chain`` owns the per-run device tensors (CNN params, PA coefficients, channel,
+ZF precoder, workspaces) and runs one step over a batch of OFDM symbols:
+
+    fdcnn_forward (a1) -> chain_tx (a3+a4+a5 fused) -> ue_receive_ser (a6)
+
+with the ZF build (a2) done once per channel realisation at construction
+(SURVEY.md §8(c) reading A10).  Pure orchestration: every arithmetic step is a
+libfdpd.so kernel.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import fdpd
+
+
+@dataclass
+class Shapes:
+    U: int
+    B: int
+    N_d: int
+    N_ifft: int
+    M_qam: int
+    chans: tuple
+    orders: tuple
+    L: int
+    M: int
+    rho: float = 0.3
+    eps: float = 1e-4
+
+    @classmethod
+    def from_config(cls, cfg):
+        return cls(U=cfg.U, B=cfg.B, N_d=cfg.N_d, N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, chans=tuple(cfg.chans),
+                   orders=tuple(cfg.orders), L=cfg.L, M=cfg.M, rho=cfg.rho)
+
+
+class Chain:
+    def __init__(self, shapes: Shapes, h_taps, coef, params, device="cuda", max_batch=1, b0=0, B_loc=None):
+        self.sh = shapes
+        self.device = torch.device(device)
+        dev = self.device
+        self.b0 = b0
+        self.B_loc = shapes.B - b0 if B_loc is None else B_loc
+        self.h_taps = torch.as_tensor(h_taps).to(dev, torch.complex64).contiguous()
+        self.coef = torch.as_tensor(coef).to(dev, torch.complex64)[b0:b0 + self.B_loc].contiguous()
+        self.params = torch.as_tensor(params).to(dev, torch.float32).contiguous()
+        # a2, once per channel realisation
+        self.h_fd, self.P, self.alpha = fdpd.zf_precoder_build(self.h_taps, shapes.N_ifft, shapes.N_d, shapes.rho,
+                                                               b0=b0, B_loc=self.B_loc)
+        self.reserve(max_batch)
+
+    def reserve(self, n):
+        sh, dev = self.sh, self.device
+        self.cap = n
+        self.s_tilde = torch.empty((n, sh.U, sh.N_d), dtype=torch.complex64, device=dev)
+        self.y = torch.empty((n, self.B_loc, sh.N_ifft), dtype=torch.complex64, device=dev)
+        self.yhat = torch.empty((n, sh.U, sh.N_d), dtype=torch.complex64, device=dev)
+        self.counts = torch.zeros(3, dtype=torch.int64, device=dev)
+        ch = fdpd._ints(sh.chans)
+        self.ws_cnn = fdpd._ws(fdpd.lib().fdcnn_workspace_bytes(ch, len(sh.chans) - 1, n, sh.U, sh.N_d), self.y)
+        self.ws_rx = fdpd._ws(fdpd.lib().ue_receive_workspace_bytes(n, self.B_loc, sh.N_d), self.y)
+
+    # ------------------------------------------------------------------ stages
+    def dpd(self, s):
+        n = s.shape[0]
+        return fdpd.fdcnn_forward(self.params, self.sh.chans, s, out=self.s_tilde[:n], workspace=self.ws_cnn)
+
+    def tx(self, s_tilde):
+        n = s_tilde.shape[0]
+        sh = self.sh
+        return fdpd.chain_tx(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, out=self.y[:n])
+
+    def rx(self, y, tx_idx, counts=None, dec=None):
+        n = y.shape[0]
+        sh = self.sh
+        counts = self.counts if counts is None else counts
+        return fdpd.ue_receive_ser(y, self.h_fd, self.alpha, tx_idx, sh.M_qam, yhat=self.yhat[:n], counts=counts,
+                                   dec=dec, workspace=self.ws_rx, boundary_eps=sh.eps)
+
+    def step(self, s, tx_idx, counts=None, dec=None):
+        """One pass of the hot path over a batch: s, tx_idx on the device."""
+        if s.shape[0] > self.cap:
+            self.reserve(s.shape[0])
+        st = self.dpd(s)
+        y = self.tx(st)
+        return self.rx(y, tx_idx, counts=counts, dec=dec)

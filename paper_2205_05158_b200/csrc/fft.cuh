@@ -1,0 +1,196 @@
+// fft.cuh — one-CTA shared-memory Stockham FFT for N = 2^LOG2N <= 16384 points.
+//
+// Each pass: every thread holds VPT = N/T complex values in registers, performs
+// VPT/R radix-R butterflies (R in {2,4,8,16}; radix-16 = 4x4 with internal
+// twiddles) and writes them back in Stockham auto-sort order, so the result is
+// in natural order without a bit-reversal pass.  Pass twiddles come from a
+// fp64-derived complex64 table W[m] = exp(-2 pi i m / N) (L1-resident).
+//
+// Shared-memory layout: one pad slot per 16 complex (pidx), which makes the
+// stride-R stores of the first pass and the stride-16 loads bank-conflict free.
+//
+// DIR = +1: inverse transform sum_k X_k e^{+2 pi i k m / N} (Eq. 2);
+// DIR = -1: forward transform (the receive DFT of Eq. 4).
+// No normalisation is applied here; callers apply N^{-1/2}.
+#pragma once
+
+#include "common.cuh"
+
+namespace fdpd {
+
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int n) { return n + (n >> 4); }
+
+// multiply by DIR * i
+template <int DIR>
+__device__ __forceinline__ float2 mul_i(float2 a) {
+    return DIR > 0 ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+
+// exp(DIR * 2 pi i m / 16) constants, m = 0..15
+__device__ __forceinline__ float2 w16(int m, int dir) {
+    // cos(2 pi m / 16), sin(2 pi m / 16)
+    const float C[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                         0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                         -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                         0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+    const float S[16] = {0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f,
+                         1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                         0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                         -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f};
+    return make_float2(C[m & 15], dir > 0 ? S[m & 15] : -S[m & 15]);
+}
+
+template <int DIR>
+__device__ __forceinline__ void dft2(float2& a, float2& b) {
+    float2 t = csub(a, b);
+    a = cadd(a, b);
+    b = t;
+}
+
+template <int DIR>
+__device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
+    // X_k = sum_n x_n W^{nk}, W = exp(DIR 2 pi i / 4) = DIR * i
+    float2 a = cadd(x0, x2), b = csub(x0, x2), c = cadd(x1, x3), d = mul_i<DIR>(csub(x1, x3));
+    x0 = cadd(a, c);
+    x2 = csub(a, c);
+    x1 = cadd(b, d);
+    x3 = csub(b, d);
+}
+
+// In-register DFT of length R on v[off .. off+R), natural order in and out.
+template <int R, int DIR, int N_>
+__device__ __forceinline__ void dftR(float2 (&v)[N_], int off) {
+    if constexpr (R == 2) {
+        dft2<DIR>(v[off], v[off + 1]);
+    } else if constexpr (R == 4) {
+        dft4<DIR>(v[off], v[off + 1], v[off + 2], v[off + 3]);
+    } else if constexpr (R == 8) {
+        // n = 2 n1 + n2 ; X[k1 + 4 k2]
+#pragma unroll
+        for (int n2 = 0; n2 < 2; ++n2) dft4<DIR>(v[off + n2], v[off + 2 + n2], v[off + 4 + n2], v[off + 6 + n2]);
+        // now A[n2][k1] at v[off + 2 k1 + n2]; twiddle by W8^{n2 k1} = W16^{2 n2 k1}
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) v[off + 2 * k1 + 1] = cmul(v[off + 2 * k1 + 1], w16(2 * k1, DIR));
+        float2 t[8];
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            float2 a = v[off + 2 * k1], b = v[off + 2 * k1 + 1];
+            t[k1] = cadd(a, b);
+            t[k1 + 4] = csub(a, b);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[off + i] = t[i];
+    } else if constexpr (R == 16) {
+        // n = 4 n1 + n2 ; X[k1 + 4 k2]
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) dft4<DIR>(v[off + n2], v[off + 4 + n2], v[off + 8 + n2], v[off + 12 + n2]);
+        // A[n2][k1] at v[off + 4 k1 + n2]; twiddle W16^{n2 k1}
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1)
+#pragma unroll
+            for (int n2 = 1; n2 < 4; ++n2)
+                v[off + 4 * k1 + n2] = cmul(v[off + 4 * k1 + n2], w16(n2 * k1, DIR));
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) dft4<DIR>(v[off + 4 * k1], v[off + 4 * k1 + 1], v[off + 4 * k1 + 2], v[off + 4 * k1 + 3]);
+        // X[k1 + 4 k2] is at v[off + 4 k1 + k2]: transpose 4x4
+        float2 t[16];
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) t[k1 + 4 * k2] = v[off + 4 * k1 + k2];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[off + i] = t[i];
+    }
+}
+
+// Radix of pass p for N = 2^LOG2N: 16 while >= 4 bits remain, then the remainder.
+template <int LOG2N>
+__host__ __device__ constexpr int n_passes() { return LOG2N / 4 + (LOG2N % 4 ? 1 : 0); }
+template <int LOG2N>
+__host__ __device__ constexpr int pass_radix(int p) {
+    return (p < LOG2N / 4) ? 16 : (1 << (LOG2N % 4));
+}
+template <int LOG2N>
+__host__ __device__ constexpr int pass_ns(int p) {
+    int ns = 1;
+    for (int i = 0; i < p; ++i) ns *= pass_radix<LOG2N>(i);
+    return ns;
+}
+
+// Threads per CTA for an N-point transform: VPT = 16 values/thread up to N = 4096,
+// then 512 threads.
+template <int LOG2N>
+__host__ __device__ constexpr int fft_threads() { return LOG2N <= 12 ? (1 << LOG2N) / 16 : 512; }
+// resident CTAs per SM requested from ptxas (register cap 65536 / (T * this))
+template <int LOG2N>
+__host__ __device__ constexpr int fft_min_blocks() { return fft_threads<LOG2N>() <= 256 ? 2 : 1; }
+
+// Register layout of a pass with radix R: element (q, r), q < VPT/R, r < R, is
+// position j + r * (N/R) with j = tid + q * T.
+template <int R, int VPT, int T, int N>
+__device__ __forceinline__ int pass_pos(int tid, int q, int r) { return tid + q * T + r * (N / R); }
+
+template <int R, int VPT, int T, int N>
+__device__ __forceinline__ void pass_load_smem(const float2* sm, float2 (&v)[VPT], int tid) {
+#pragma unroll
+    for (int q = 0; q < VPT / R; ++q)
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q * R + r] = sm[pidx(pass_pos<R, VPT, T, N>(tid, q, r))];
+}
+
+template <int R, int DIR, int VPT, int T, int N>
+__device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT], int Ns, const float2* __restrict__ tw,
+                                                   int tid) {
+#pragma unroll
+    for (int q = 0; q < VPT / R; ++q) {
+        const int j = tid + q * T;
+        const int k = j & (Ns - 1);
+        if (Ns > 1) {
+            const int step = k * (N / (Ns * R));
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                float2 w = __ldg(tw + r * step);
+                if (DIR > 0) w.y = -w.y;
+                v[q * R + r] = cmul(v[q * R + r], w);
+            }
+        }
+        dftR<R, DIR>(v, q * R);
+        const int d = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[pidx(d + r * Ns)] = v[q * R + r];
+    }
+}
+
+// Runs passes [1, n_passes) after the caller has filled v with the pass-0 input
+// layout (pass_pos with R = pass_radix(0)).  Leaves the transform (unnormalised)
+// in sm in natural order; ends with __syncthreads().
+template <int LOG2N, int DIR, int P = 0>
+__device__ __forceinline__ void fft_run(float2* sm, float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
+                                        const float2* __restrict__ tw, int tid) {
+    constexpr int N = 1 << LOG2N;
+    constexpr int T = fft_threads<LOG2N>();
+    constexpr int VPT = N / T;
+    constexpr int R = pass_radix<LOG2N>(P);
+    if constexpr (P > 0) {
+        pass_load_smem<R, VPT, T, N>(sm, v, tid);
+        __syncthreads();
+    }
+    pass_compute_store<R, DIR, VPT, T, N>(sm, v, pass_ns<LOG2N>(P), tw, tid);
+    __syncthreads();
+    if constexpr (P + 1 < n_passes<LOG2N>()) fft_run<LOG2N, DIR, P + 1>(sm, v, tw, tid);
+}
+
+// Data-subcarrier index of IDFT bin k (reading A7), or -1 for a guard bin.
+__device__ __forceinline__ int bin_to_data(int k, int N, int N_d) {
+    const int h = N_d >> 1;
+    if (k < h) return k + h;
+    if (k >= N - h) return k - (N - h);
+    return -1;
+}
+__device__ __forceinline__ int data_to_bin(int j, int N, int N_d) {
+    const int h = N_d >> 1;
+    return j >= h ? j - h : N - h + j;
+}
+
+}  // namespace fdpd

@@ -1,0 +1,234 @@
+// rx.cu — evaluation side of the hot path: receive DFT at the data bins,
+// FD channel sum over antennas (Eqs. 4-5), QAM slicing and SER.
+#include "fft.cuh"
+
+namespace fdpd {
+
+// ============================================================================ receive DFT
+// XPA[n][b][j] = N^-1/2 sum_m y[n][b][m] e^{-2 pi i k_j m / N}
+template <int LOG2N>
+__global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>()) k_rx_fft(const float2* __restrict__ y, float2* __restrict__ XPA,
+                                                                const float2* __restrict__ tw, int N_d, float sc) {
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* sm = reinterpret_cast<float2*>(smem_raw);
+    const int tid = threadIdx.x;
+    const size_t nb = blockIdx.x;
+    const float2* yi = y + nb * N;
+    float2 v[VPT];
+#pragma unroll
+    for (int q = 0; q < VPT / R0; ++q)
+#pragma unroll
+        for (int r = 0; r < R0; ++r) v[q * R0 + r] = __ldg(yi + pass_pos<R0, VPT, T, N>(tid, q, r));
+    fft_run<LOG2N, -1>(sm, v, tw, tid);
+    float2* xo = XPA + nb * N_d;
+    for (int j = tid; j < N_d; j += T) xo[j] = cscale(sm[pidx(data_to_bin(j, N, N_d))], sc);
+}
+
+// ============================================================================ slicer
+struct SliceParams {
+    float inv_ac;   // 1 / (alpha * c): yhat -> level units
+    float thr;      // boundary_eps / c in level units
+    int m;          // sqrt(M_qam)
+};
+
+__device__ __forceinline__ int slice_axis(float v, const SliceParams& sp, bool& near) {
+    const float lim = (float)(sp.m - 1);
+    float d = fmaf(2.f, floorf(0.5f * v), 1.f);
+    d = fminf(fmaxf(d, -lim), lim);
+    const float bnd = 2.f * rintf(0.5f * v);
+    near |= (fabsf(v - bnd) < sp.thr) && (fabsf(bnd) <= lim - 1.f);
+    return (int)((d + lim) * 0.5f);
+}
+
+// Block-reduce (err, near, total) and add to the global int64 counters.
+__device__ __forceinline__ void add_counts(long long* counts, int err, int near, int total) {
+    __shared__ int s_red[3][32];
+    for (int o = 16; o > 0; o >>= 1) {
+        err += __shfl_xor_sync(0xffffffffu, err, o);
+        near += __shfl_xor_sync(0xffffffffu, near, o);
+        total += __shfl_xor_sync(0xffffffffu, total, o);
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    if (lane == 0) { s_red[0][w] = err; s_red[1][w] = near; s_red[2][w] = total; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long e = 0, n = 0, c = 0;
+        for (int i = 0; i < nw; ++i) { e += s_red[0][i]; n += s_red[1][i]; c += s_red[2][i]; }
+        if (e) atomicAdd(reinterpret_cast<unsigned long long*>(counts + 0), (unsigned long long)e);
+        if (c) atomicAdd(reinterpret_cast<unsigned long long*>(counts + 1), (unsigned long long)c);
+        if (n) atomicAdd(reinterpret_cast<unsigned long long*>(counts + 2), (unsigned long long)n);
+    }
+}
+
+__global__ void k_slice(const float2* __restrict__ yhat, const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
+                        long long* counts, long long total, SliceParams sp) {
+    int err = 0, near = 0, cnt = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float2 z = yhat[i];
+        bool nr = false;
+        const int di = slice_axis(z.x * sp.inv_ac, sp, nr);
+        const int dq = slice_axis(z.y * sp.inv_ac, sp, nr);
+        const int dd = di + sp.m * dq;
+        if (dec) dec[i] = (uint16_t)dd;
+        err += (dd != (int)idx[i]);
+        near += nr;
+        ++cnt;
+    }
+    add_counts(counts, err, near, cnt);
+}
+
+// ============================================================================ channel sum (+ slicing)
+// yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j].  Thread per (n, j), loop over u and b.
+template <bool SER>
+__global__ void __launch_bounds__(128) k_rx_combine(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
+                                                    float2* __restrict__ yhat, int B, int U, int N_d, int accumulate,
+                                                    const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
+                                                    long long* counts, SliceParams sp) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n = blockIdx.y;
+    int err = 0, near = 0, cnt = 0;
+    if (j < N_d) {
+        const float2* X = XPA + n * B * N_d + j;
+        for (int u = 0; u < U; ++u) {
+            const float2* h = hfd + (size_t)u * B * N_d + j;
+            float2 acc = make_float2(0.f, 0.f);
+            for (int b = 0; b < B; ++b) acc = cfma(__ldg(h + (size_t)b * N_d), __ldg(X + (size_t)b * N_d), acc);
+            const size_t o = (n * U + u) * N_d + j;
+            if (accumulate) acc = cadd(acc, yhat[o]);
+            yhat[o] = acc;
+            if (SER) {
+                bool nr = false;
+                const int di = slice_axis(acc.x * sp.inv_ac, sp, nr);
+                const int dq = slice_axis(acc.y * sp.inv_ac, sp, nr);
+                const int dd = di + sp.m * dq;
+                if (dec) dec[o] = (uint16_t)dd;
+                err += (dd != (int)idx[o]);
+                near += nr;
+                ++cnt;
+            }
+        }
+    }
+    if (SER) add_counts(counts, err, near, cnt);
+}
+
+// ============================================================================ host side
+static int validate_slice(int M_qam, float alpha, float eps, SliceParams& sp) {
+    int m = 1;
+    while (m * m < M_qam) ++m;
+    FD_REQUIRE(m * m == M_qam && M_qam >= 4 && M_qam <= 65536, "M_qam=%d must be a square >= 4", M_qam);
+    FD_REQUIRE(alpha > 0.f && std::isfinite(alpha), "alpha=%g must be > 0", (double)alpha);
+    FD_REQUIRE(eps >= 0.f, "boundary_eps < 0");
+    const double c = 1.0 / std::sqrt(2.0 * (M_qam - 1) / 3.0);
+    sp.m = m;
+    sp.inv_ac = (float)(1.0 / ((double)alpha * c));
+    sp.thr = (float)((double)eps / c);
+    return FD_OK;
+}
+
+template <int LOG2N>
+static int launch_rx_fft(const float2* y, float2* XPA, long long n_sym, int B, int N_d, cudaStream_t st) {
+    constexpr int N = 1 << LOG2N;
+    const float2* tw = twiddle_table(N, st);
+    if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
+    const size_t smem = sizeof(float2) * padded_len(N);
+    cudaFuncSetAttribute(k_rx_fft<LOG2N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_rx_fft<LOG2N><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(y, XPA, tw, N_d,
+                                                                            (float)(1.0 / std::sqrt((double)N)));
+    return check_launch("ue_receive (fft)");
+}
+
+static int rx_fft(const float2* y, float2* XPA, long long n_sym, int B, int N_d, int N, cudaStream_t st) {
+    switch (ilog2(N)) {
+        case 4: return launch_rx_fft<4>(y, XPA, n_sym, B, N_d, st);
+        case 5: return launch_rx_fft<5>(y, XPA, n_sym, B, N_d, st);
+        case 6: return launch_rx_fft<6>(y, XPA, n_sym, B, N_d, st);
+        case 7: return launch_rx_fft<7>(y, XPA, n_sym, B, N_d, st);
+        case 8: return launch_rx_fft<8>(y, XPA, n_sym, B, N_d, st);
+        case 9: return launch_rx_fft<9>(y, XPA, n_sym, B, N_d, st);
+        case 10: return launch_rx_fft<10>(y, XPA, n_sym, B, N_d, st);
+        case 11: return launch_rx_fft<11>(y, XPA, n_sym, B, N_d, st);
+        case 12: return launch_rx_fft<12>(y, XPA, n_sym, B, N_d, st);
+        case 13: return launch_rx_fft<13>(y, XPA, n_sym, B, N_d, st);
+        case 14: return launch_rx_fft<14>(y, XPA, n_sym, B, N_d, st);
+        default: return fail_arg("unsupported N_ifft=%d", N);
+    }
+}
+
+static int validate_rx(const void* y, const void* h_fd, const void* yhat, const void* ws, size_t ws_bytes,
+                       long long n_sym, int B_loc, int U, int N_d, int N) {
+    FD_REQUIRE(n_sym >= 0 && B_loc >= 1 && U >= 1, "ue_receive: bad sizes");
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(y && h_fd && yhat, "ue_receive: NULL pointer");
+    FD_REQUIRE(aligned16(y) && aligned8(h_fd) && aligned8(yhat), "ue_receive: misaligned pointer");
+    FD_REQUIRE(is_pow2(N) && N >= 16 && N <= 16384, "ue_receive: N_ifft=%d unsupported", N);
+    FD_REQUIRE(N_d >= 2 && N_d % 2 == 0 && N_d <= N, "ue_receive: N_d=%d must be even and <= N_ifft", N_d);
+    FD_REQUIRE(n_sym <= 65535, "ue_receive: n_sym=%lld > 65535 per call (batch it)", n_sym);
+    FD_REQUIRE(n_sym * (long long)B_loc <= 0x7fffffffLL, "ue_receive: n_sym*B too large");
+    const size_t need = sizeof(float2) * (size_t)n_sym * B_loc * N_d;
+    FD_REQUIRE(ws != nullptr && aligned8(ws) && ws_bytes >= need,
+               "ue_receive: workspace of %zu bytes required (got %zu)", need, ws_bytes);
+    return FD_OK;
+}
+
+}  // namespace fdpd
+
+using namespace fdpd;
+
+extern "C" {
+
+size_t ue_receive_workspace_bytes(long long n_sym, int B_loc, int N_d) {
+    if (n_sym <= 0 || B_loc <= 0 || N_d <= 0) return 0;
+    return sizeof(float2) * (size_t)n_sym * B_loc * N_d;
+}
+
+int ue_receive(const void* y, const void* h_fd, void* yhat, void* workspace, size_t workspace_bytes, long long n_sym,
+               int B_loc, int U, int N_d, int N_ifft, int accumulate, cudaStream_t stream) {
+    int rc = validate_rx(y, h_fd, yhat, workspace, workspace_bytes, n_sym, B_loc, U, N_d, N_ifft);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    float2* XPA = (float2*)workspace;
+    rc = rx_fft((const float2*)y, XPA, n_sym, B_loc, N_d, N_ifft, stream);
+    if (rc) return rc;
+    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
+    k_rx_combine<false><<<grid, 128, 0, stream>>>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, accumulate,
+                                                 nullptr, nullptr, nullptr, SliceParams{});
+    return check_launch("ue_receive (combine)");
+}
+
+int ue_slice_ser(const void* yhat, float alpha, const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts,
+                 long long n_sym, int U, int N_d, float boundary_eps, cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && U >= 1 && N_d >= 1, "ue_slice_ser: bad sizes");
+    SliceParams sp;
+    int rc = validate_slice(M_qam, alpha, boundary_eps, sp);
+    if (rc) return rc;
+    const long long total = n_sym * U * (long long)N_d;
+    if (total == 0) return FD_OK;
+    FD_REQUIRE(yhat && tx_idx && counts, "ue_slice_ser: NULL pointer");
+    FD_REQUIRE(aligned8(yhat) && aligned8(counts), "ue_slice_ser: misaligned pointer");
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+    k_slice<<<blocks, 256, 0, stream>>>((const float2*)yhat, tx_idx, dec, counts, total, sp);
+    return check_launch("ue_slice_ser");
+}
+
+int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace, size_t workspace_bytes, float alpha,
+                   const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts, long long n_sym, int B_loc,
+                   int U, int N_d, int N_ifft, float boundary_eps, cudaStream_t stream) {
+    int rc = validate_rx(y, h_fd, yhat, workspace, workspace_bytes, n_sym, B_loc, U, N_d, N_ifft);
+    if (rc) return rc;
+    SliceParams sp;
+    rc = validate_slice(M_qam, alpha, boundary_eps, sp);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(tx_idx && counts && aligned8(counts), "ue_receive_ser: NULL/misaligned tx_idx or counts");
+    float2* XPA = (float2*)workspace;
+    rc = rx_fft((const float2*)y, XPA, n_sym, B_loc, N_d, N_ifft, stream);
+    if (rc) return rc;
+    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
+    k_rx_combine<true><<<grid, 128, 0, stream>>>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, 0, tx_idx,
+                                                dec, counts, sp);
+    return check_launch("ue_receive_ser (combine)");
+}
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+// tx.cu — transmit side of the hot path: precode (Eq. 1), OFDM IDFT (Eq. 2),
+// GMP PA (Eq. 9), and the fused chain_tx (one CTA per (symbol, antenna)).
+#include "gmp.cuh"
+
+namespace fdpd {
+
+// ============================================================================ precode
+// X[n][b][j] = sum_u P[b][u][j] s[n][u][j]          (Eq. 1)
+__global__ void k_precode(const float2* __restrict__ P, const float2* __restrict__ s, float2* __restrict__ X,
+                          long long n_sym, int B, int U, int N_d) {
+    const long long total = n_sym * B * (long long)N_d;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(i % N_d);
+        const long long nb = i / N_d;
+        const int b = (int)(nb % B);
+        const long long n = nb / B;
+        float2 acc = make_float2(0.f, 0.f);
+        for (int u = 0; u < U; ++u)
+            acc = cfma(__ldg(P + ((size_t)b * U + u) * N_d + j), __ldg(s + ((size_t)n * U + u) * N_d + j), acc);
+        X[i] = acc;
+    }
+}
+
+// ============================================================================ helpers
+// Fill the pass-0 registers with the precoded spectrum X = P_b s_n at data bins, 0 on guards.
+template <int LOG2N>
+__device__ __forceinline__ void load_precoded(float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
+                                              const float2* __restrict__ Pb, const float2* __restrict__ sn,
+                                              int U, int N_d, int tid) {
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
+#pragma unroll
+    for (int q = 0; q < VPT / R0; ++q)
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+            const int jj = bin_to_data(pass_pos<R0, VPT, T, N>(tid, q, r), N, N_d);
+            float2 acc = make_float2(0.f, 0.f);
+            if (jj >= 0)
+                for (int u = 0; u < U; ++u)
+                    acc = cfma(__ldg(Pb + (size_t)u * N_d + jj), __ldg(sn + (size_t)u * N_d + jj), acc);
+            v[q * R0 + r] = acc;
+        }
+}
+
+template <int LOG2N>
+__device__ __forceinline__ void load_spectrum(float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
+                                              const float2* __restrict__ Xnb, int N_d, int tid) {
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
+#pragma unroll
+    for (int q = 0; q < VPT / R0; ++q)
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+            const int jj = bin_to_data(pass_pos<R0, VPT, T, N>(tid, q, r), N, N_d);
+            v[q * R0 + r] = jj >= 0 ? __ldg(Xnb + jj) : make_float2(0.f, 0.f);
+        }
+}
+
+// ============================================================================ OFDM IDFT
+template <int LOG2N>
+__global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>()) k_ofdm(const float2* __restrict__ X, float2* __restrict__ x,
+                                                              const float2* __restrict__ tw, int B, int N_d, float sc) {
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* sm = reinterpret_cast<float2*>(smem_raw);
+    const int tid = threadIdx.x;
+    const size_t nb = blockIdx.x;
+    float2 v[VPT];
+    load_spectrum<LOG2N>(v, X + nb * N_d, N_d, tid);
+    fft_run<LOG2N, +1>(sm, v, tw, tid);
+    float2* xo = x + nb * N;
+    for (int i = tid; i < N; i += T) xo[i] = cscale(sm[pidx(i)], sc);
+}
+
+// ============================================================================ GMP (standalone)
+template <int KP, int L, int M, int RS>
+__global__ void __launch_bounds__(256, 2) k_gmp(const float2* __restrict__ x, const float2* __restrict__ coef,
+                                             float2* __restrict__ y, int B, int N, GmpDesc d) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* usm = reinterpret_cast<float2*>(smem_raw);
+    float* esm = reinterpret_cast<float*>(usm + padded_len(N));
+    float2* cf = reinterpret_cast<float2*>(esm + N);
+    const int tid = threadIdx.x, T = blockDim.x;
+    const size_t nb = blockIdx.x;
+    const int b = (int)(nb % B);
+    for (int i = tid; i < d.n_coef; i += T) cf[i] = coef[(size_t)b * d.n_coef + i];
+    const float2* xi = x + nb * N;
+    for (int i = tid; i < N; i += T) {
+        const float2 t = xi[i];
+        usm[pidx(i)] = t;
+        esm[i] = fmaf(t.x, t.x, t.y * t.y);
+    }
+    __syncthreads();
+    gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
+}
+
+// ============================================================================ fused chain_tx
+// One CTA per (symbol n, antenna b): precode at the data bins straight into the
+// pass-0 registers, IDFT in shared memory, 1/sqrt(N) scale + envelope, GMP, stream y.
+template <int LOG2N, int KP, int L, int M, int RS>
+__global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
+    k_chain_tx(const float2* __restrict__ P, const float2* __restrict__ s, const float2* __restrict__ coef,
+               float2* __restrict__ y, const float2* __restrict__ tw, int B, int U, int N_d, float sc, GmpDesc d) {
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* usm = reinterpret_cast<float2*>(smem_raw);
+    float* esm = reinterpret_cast<float*>(usm + padded_len(N));
+    float2* cf = reinterpret_cast<float2*>(esm + N);
+    const int tid = threadIdx.x;
+    const size_t nb = blockIdx.x;
+    const int b = (int)(nb % B);
+    const size_t n = nb / B;
+    for (int i = tid; i < d.n_coef; i += T) cf[i] = coef[(size_t)b * d.n_coef + i];
+    float2 v[VPT];
+    load_precoded<LOG2N>(v, P + (size_t)b * U * N_d, s + n * U * N_d, U, N_d, tid);
+    fft_run<LOG2N, +1>(usm, v, tw, tid);
+    for (int i = tid; i < N; i += T) {
+        const float2 t = cscale(usm[pidx(i)], sc);
+        usm[pidx(i)] = t;
+        esm[i] = fmaf(t.x, t.x, t.y * t.y);
+    }
+    __syncthreads();
+    gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
+}
+
+// ============================================================================ host side
+static int validate_gmp(const int* orders, int n_orders, int L, int M, int N, GmpDesc& d, int& variant) {
+    FD_REQUIRE(orders != nullptr, "orders is NULL");
+    FD_REQUIRE(n_orders >= 1 && n_orders <= GMP_MAX_ORDERS, "n_orders=%d outside [1,%d]", n_orders, GMP_MAX_ORDERS);
+    FD_REQUIRE(orders[0] == 1, "orders[0]=%d must be 1", orders[0]);
+    for (int k = 0; k < n_orders; ++k) {
+        FD_REQUIRE(orders[k] >= 1 && (orders[k] & 1), "orders[%d]=%d must be odd", k, orders[k]);
+        FD_REQUIRE(k == 0 || orders[k] > orders[k - 1], "orders must be ascending");
+        FD_REQUIRE(orders[k] <= 31, "orders[%d]=%d too large", k, orders[k]);
+    }
+    FD_REQUIRE(L >= 0 && L <= GMP_MAX_L, "L=%d outside [0,%d]", L, GMP_MAX_L);
+    FD_REQUIRE(M >= 0 && M <= GMP_MAX_M, "M=%d outside [0,%d]", M, GMP_MAX_M);
+    FD_REQUIRE(L + 2 * M < N, "L + 2M = %d must be < N_ifft = %d", L + 2 * M, N);
+    d.Kp = n_orders;
+    d.L = L;
+    d.M = M;
+    d.n_coef = n_orders * (L + 1) + 2 * (n_orders - 1) * (L + 1) * M;
+    bool consecutive = true;
+    for (int k = 0; k < GMP_MAX_ORDERS; ++k) d.pw[k] = k < n_orders ? (orders[k] - 1) / 2 : 0;
+    for (int k = 0; k < n_orders; ++k) consecutive &= (orders[k] == 2 * k + 1);
+    variant = 0;
+    if (consecutive) {
+        if (n_orders == 3 && L == 2 && M == 1) variant = 1;
+        else if (n_orders == 4 && L == 4 && M == 2) variant = 2;
+        else if (n_orders == 5 && L == 6 && M == 3) variant = 3;
+    }
+    return FD_OK;
+}
+
+template <typename K>
+static void set_smem(K kernel, size_t bytes) {
+    // opt-in above the 48 KB default; idempotent and cheap after the first call
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+static int validate_ofdm(long long n_sym, int B, int N_d, int N) {
+    FD_REQUIRE(n_sym >= 0, "n_sym=%lld < 0", n_sym);
+    FD_REQUIRE(B >= 1, "B=%d < 1", B);
+    FD_REQUIRE(is_pow2(N) && N >= 16 && N <= 16384, "N_ifft=%d must be a power of two in [16, 16384]", N);
+    FD_REQUIRE(N_d >= 2 && (N_d % 2) == 0 && N_d <= N, "N_d=%d must be even, >= 2 and <= N_ifft", N_d);
+    FD_REQUIRE(n_sym * (long long)B <= 0x7fffffffLL, "n_sym*B too large");
+    return FD_OK;
+}
+
+template <int LOG2N>
+static int launch_ofdm(const float2* X, float2* x, long long n_sym, int B, int N_d, cudaStream_t st) {
+    constexpr int N = 1 << LOG2N;
+    const float2* tw = twiddle_table(N, st);
+    if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
+    const size_t smem = sizeof(float2) * padded_len(N);
+    set_smem(k_ofdm<LOG2N>, smem);
+    k_ofdm<LOG2N><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(X, x, tw, B, N_d,
+                                                                          (float)(1.0 / std::sqrt((double)N)));
+    return check_launch("ofdm_modulate");
+}
+
+template <int KP, int L, int M, int RS>
+static int launch_gmp(const float2* x, const float2* coef, float2* y, long long n_sym, int B, int N, const GmpDesc& d,
+                      cudaStream_t st) {
+    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * d.n_coef;
+    set_smem(k_gmp<KP, L, M, RS>, smem);
+    k_gmp<KP, L, M, RS><<<(unsigned)(n_sym * B), 256, smem, st>>>(x, coef, y, B, N, d);
+    return check_launch("gmp_pa");
+}
+
+template <int LOG2N, int KP, int L, int M, int RS>
+static int launch_chain_one(const float2* P, const float2* s, const float2* coef, float2* y, long long n_sym, int B,
+                            int U, int N_d, const GmpDesc& d, cudaStream_t st) {
+    constexpr int N = 1 << LOG2N;
+    const float2* tw = twiddle_table(N, st);
+    if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
+    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * d.n_coef;
+    set_smem(k_chain_tx<LOG2N, KP, L, M, RS>, smem);
+    k_chain_tx<LOG2N, KP, L, M, RS><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(
+        P, s, coef, y, tw, B, U, N_d, (float)(1.0 / std::sqrt((double)N)), d);
+    return check_launch("chain_tx");
+}
+
+template <int LOG2N>
+static int launch_chain(int variant, const float2* P, const float2* s, const float2* coef, float2* y, long long n_sym,
+                        int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
+    switch (variant) {
+        case 1: return launch_chain_one<LOG2N, 3, 2, 1, 4>(P, s, coef, y, n_sym, B, U, N_d, d, st);
+        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 4>(P, s, coef, y, n_sym, B, U, N_d, d, st);
+        case 3: return launch_chain_one<LOG2N, 5, 6, 3, 2>(P, s, coef, y, n_sym, B, U, N_d, d, st);
+        default: return launch_chain_one<LOG2N, 0, 0, 0, 1>(P, s, coef, y, n_sym, B, U, N_d, d, st);
+    }
+}
+
+#define FD_LOG2N_SWITCH(LOG2, CALL)        \
+    switch (LOG2) {                        \
+        case 4: { constexpr int LG = 4; return CALL; }   \
+        case 5: { constexpr int LG = 5; return CALL; }   \
+        case 6: { constexpr int LG = 6; return CALL; }   \
+        case 7: { constexpr int LG = 7; return CALL; }   \
+        case 8: { constexpr int LG = 8; return CALL; }   \
+        case 9: { constexpr int LG = 9; return CALL; }   \
+        case 10: { constexpr int LG = 10; return CALL; } \
+        case 11: { constexpr int LG = 11; return CALL; } \
+        case 12: { constexpr int LG = 12; return CALL; } \
+        case 13: { constexpr int LG = 13; return CALL; } \
+        case 14: { constexpr int LG = 14; return CALL; } \
+        default: return fail_arg("unsupported N_ifft");   \
+    }
+
+}  // namespace fdpd
+
+using namespace fdpd;
+
+extern "C" {
+
+int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d, cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && B_loc >= 1 && U >= 1 && N_d >= 1, "precode: bad sizes");
+    const long long total = n_sym * B_loc * (long long)N_d;
+    if (total == 0) return FD_OK;
+    FD_REQUIRE(P && s && X, "precode: NULL pointer");
+    FD_REQUIRE(aligned8(P) && aligned8(s) && aligned8(X), "precode: pointers must be 8-byte aligned");
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    k_precode<<<blocks, 256, 0, stream>>>((const float2*)P, (const float2*)s, (float2*)X, n_sym, B_loc, U, N_d);
+    return check_launch("precode");
+}
+
+int ofdm_modulate(const void* X, void* x, long long n_sym, int B, int N_d, int N_ifft, cudaStream_t stream) {
+    int rc = validate_ofdm(n_sym, B, N_d, N_ifft);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(X && x, "ofdm_modulate: NULL pointer");
+    FD_REQUIRE(aligned16(X) && aligned16(x), "ofdm_modulate: pointers must be 16-byte aligned");
+    const float2* Xp = (const float2*)X;
+    float2* xp = (float2*)x;
+    FD_LOG2N_SWITCH(ilog2(N_ifft), launch_ofdm<LG>(Xp, xp, n_sym, B, N_d, stream));
+}
+
+int gmp_pa(const void* x, const void* coef, void* y, const int* orders, int n_orders, int L, int M, long long n_sym,
+           int B, int N_ifft, cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && B >= 1, "gmp_pa: bad sizes");
+    FD_REQUIRE(n_sym == 0 || (x && coef && y), "gmp_pa: NULL pointer");
+    FD_REQUIRE(n_sym == 0 || x != y, "gmp_pa: y must not alias x");
+    FD_REQUIRE(n_sym == 0 || (aligned16(x) && aligned16(y) && aligned8(coef)), "gmp_pa: misaligned pointer");
+    FD_REQUIRE(is_pow2(N_ifft) && N_ifft >= 16 && N_ifft <= 16384, "gmp_pa: N_ifft=%d unsupported", N_ifft);
+    FD_REQUIRE(n_sym * (long long)B <= 0x7fffffffLL, "gmp_pa: n_sym*B too large");
+    GmpDesc d;
+    int variant = 0;
+    int rc = validate_gmp(orders, n_orders, L, M, N_ifft, d, variant);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    const float2 *xp = (const float2*)x, *cp = (const float2*)coef;
+    float2* yp = (float2*)y;
+    switch (variant) {
+        case 1: return launch_gmp<3, 2, 1, 4>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
+        case 2: return launch_gmp<4, 4, 2, 4>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
+        case 3: return launch_gmp<5, 6, 3, 2>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
+        default: return launch_gmp<0, 0, 0, 1>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
+    }
+}
+
+int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y, const int* orders, int n_orders, int L,
+             int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream) {
+    FD_REQUIRE(n_sym == 0 || (P && s_tilde && coef && y), "chain_tx: NULL pointer");
+    FD_REQUIRE(n_sym == 0 || (aligned16(P) && aligned16(s_tilde) && aligned8(coef) && aligned16(y)),
+               "chain_tx: misaligned pointer");
+    FD_REQUIRE(U >= 1 && U <= 1024, "chain_tx: bad U=%d", U);
+    int rc = validate_ofdm(n_sym, B_loc, N_d, N_ifft);
+    if (rc) return rc;
+    GmpDesc d;
+    int variant = 0;
+    rc = validate_gmp(orders, n_orders, L, M, N_ifft, d, variant);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    const float2 *Pp = (const float2*)P, *sp = (const float2*)s_tilde, *cp = (const float2*)coef;
+    float2* yp = (float2*)y;
+    FD_LOG2N_SWITCH(ilog2(N_ifft), launch_chain<LG>(variant, Pp, sp, cp, yp, n_sym, B_loc, U, N_d, d, stream));
+}
+
+}  // extern "C"

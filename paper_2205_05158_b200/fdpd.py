@@ -1,0 +1,218 @@
+"""Thin ctypes binding of libfdpd.so (include/fdpd.h) — argument marshalling only.
+
+Each function has the C entry point's name, takes CUDA torch tensors, allocates
+outputs with torch when ``out`` is not given (device memory plumbing), passes raw
+pointers plus the current torch stream, and raises ``FdpdError`` on a non-OK
+status.  Every step of the path runs in libfdpd's kernels; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfdpd.so")
+
+FD_OK, FD_ERR_ARG, FD_ERR_NUMERIC, FD_ERR_CUDA = 0, 2, 3, 4
+
+_vp, _i, _ll, _f, _sz = C.c_void_p, C.c_int, C.c_longlong, C.c_float, C.c_size_t
+_ip = C.POINTER(C.c_int)
+
+# name -> (restype, argtypes), mirroring include/fdpd.h
+SIGNATURES = {
+    "fd_last_error": (C.c_char_p, []),
+    "fd_version": (_i, []),
+    "fd_shutdown": (None, []),
+    "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
+    "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
+    "zf_workspace_bytes": (_sz, [_i]),
+    "zf_precoder_build": (_i, [_vp, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, C.POINTER(C.c_float), _vp, _sz, _vp]),
+    "precode": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _vp]),
+    "ofdm_modulate": (_i, [_vp, _vp, _ll, _i, _i, _i, _vp]),
+    "gmp_pa": (_i, [_vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _vp]),
+    "chain_tx": (_i, [_vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _vp]),
+    "ue_receive_workspace_bytes": (_sz, [_ll, _i, _i]),
+    "ue_receive": (_i, [_vp, _vp, _vp, _vp, _sz, _ll, _i, _i, _i, _i, _i, _vp]),
+    "ue_slice_ser": (_i, [_vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
+    "ue_receive_ser": (_i, [_vp, _vp, _vp, _vp, _sz, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _i, _f, _vp]),
+}
+
+
+class FdpdError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libfdpd status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libfdpd.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2205_05158_b200.build` "
+                               "(there is no CPU fallback)")
+        h = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = h
+    return _lib
+
+
+def _check(status: int):
+    if status != FD_OK:
+        raise FdpdError(status, lib().fd_last_error().decode())
+
+
+def _ints(vals):
+    arr = (C.c_int * len(vals))(*[int(v) for v in vals])
+    return arr
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _dev(t, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _stream(t):
+    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ws(nbytes, like):
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=like.device)
+
+
+# ----------------------------------------------------------------------------- a1
+def fdcnn_forward(params, chans, s_in, out=None, workspace=None):
+    """s_tilde = s + CNN(s)  (include/fdpd.h fdcnn_forward).  s_in complex64 [n_sym][U][N_d]."""
+    _dev(params, torch.float32, "params")
+    _dev(s_in, torch.complex64, "s_in")
+    n_sym, U, N_d = s_in.shape
+    ch = _ints(chans)
+    nl = len(chans) - 1
+    out = torch.empty_like(s_in) if out is None else _dev(out, torch.complex64, "out")
+    need = lib().fdcnn_workspace_bytes(ch, nl, n_sym, U, N_d)
+    if workspace is None or workspace.numel() < need:
+        workspace = _ws(need, s_in)
+    _check(lib().fdcnn_forward(_ptr(params), ch, nl, _ptr(s_in), _ptr(out), _ptr(workspace), workspace.numel(),
+                               n_sym, U, N_d, _stream(s_in)))
+    return out
+
+
+# ----------------------------------------------------------------------------- a2
+def zf_precoder_build(h_taps, N_ifft, N_d, rho, b0=0, B_loc=None):
+    """Returns (h_fd [U][B_loc][N_d], P [B_loc][U][N_d], alpha) — include/fdpd.h zf_precoder_build."""
+    _dev(h_taps, torch.complex64, "h_taps")
+    T, U, B = h_taps.shape
+    B_loc = B - b0 if B_loc is None else B_loc
+    h_fd = torch.empty((U, B_loc, N_d), dtype=torch.complex64, device=h_taps.device)
+    P = torch.empty((B_loc, U, N_d), dtype=torch.complex64, device=h_taps.device)
+    ws = _ws(lib().zf_workspace_bytes(N_d), h_taps)
+    a = C.c_float(0.0)
+    _check(lib().zf_precoder_build(_ptr(h_taps), T, U, B, N_ifft, N_d, float(rho), b0, B_loc, _ptr(h_fd), _ptr(P),
+                                   C.byref(a), _ptr(ws), ws.numel(), _stream(h_taps)))
+    return h_fd, P, float(a.value)
+
+
+# ----------------------------------------------------------------------------- a3-a5
+def precode(P, s, out=None):
+    _dev(P, torch.complex64, "P")
+    _dev(s, torch.complex64, "s")
+    B, U, N_d = P.shape
+    n_sym = s.shape[0]
+    out = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=s.device) if out is None else out
+    _check(lib().precode(_ptr(P), _ptr(s), _ptr(out), n_sym, B, U, N_d, _stream(s)))
+    return out
+
+
+def ofdm_modulate(X, N_ifft, out=None):
+    _dev(X, torch.complex64, "X")
+    n_sym, B, N_d = X.shape
+    out = torch.empty((n_sym, B, N_ifft), dtype=torch.complex64, device=X.device) if out is None else out
+    _check(lib().ofdm_modulate(_ptr(X), _ptr(out), n_sym, B, N_d, N_ifft, _stream(X)))
+    return out
+
+
+def gmp_pa(x, coef, orders, L, M, out=None):
+    _dev(x, torch.complex64, "x")
+    _dev(coef, torch.complex64, "coef")
+    n_sym, B, N = x.shape
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().gmp_pa(_ptr(x), _ptr(coef), _ptr(out), _ints(orders), len(orders), L, M, n_sym, B, N, _stream(x)))
+    return out
+
+
+def chain_tx(P, s_tilde, coef, orders, L, M, N_ifft, out=None):
+    """Fused precode -> IDFT -> GMP: y [n_sym][B_loc][N_ifft]."""
+    _dev(P, torch.complex64, "P")
+    _dev(s_tilde, torch.complex64, "s_tilde")
+    _dev(coef, torch.complex64, "coef")
+    B, U, N_d = P.shape
+    n_sym = s_tilde.shape[0]
+    out = torch.empty((n_sym, B, N_ifft), dtype=torch.complex64, device=P.device) if out is None else out
+    _check(lib().chain_tx(_ptr(P), _ptr(s_tilde), _ptr(coef), _ptr(out), _ints(orders), len(orders), L, M,
+                          n_sym, B, U, N_d, N_ifft, _stream(P)))
+    return out
+
+
+# ----------------------------------------------------------------------------- a6
+def ue_receive(y, h_fd, out=None, accumulate=False, workspace=None):
+    _dev(y, torch.complex64, "y")
+    _dev(h_fd, torch.complex64, "h_fd")
+    n_sym, B, N = y.shape
+    U, _, N_d = h_fd.shape
+    if out is None:
+        out = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=y.device)
+    need = lib().ue_receive_workspace_bytes(n_sym, B, N_d)
+    if workspace is None or workspace.numel() < need:
+        workspace = _ws(need, y)
+    _check(lib().ue_receive(_ptr(y), _ptr(h_fd), _ptr(out), _ptr(workspace), workspace.numel(), n_sym, B, U, N_d, N,
+                            int(bool(accumulate)), _stream(y)))
+    return out
+
+
+def ue_slice_ser(yhat, alpha, tx_idx, M_qam, counts=None, dec=None, boundary_eps=1e-4):
+    """Returns counts (device int64[3]: errors, total, near) and dec (uint16 or None)."""
+    _dev(yhat, torch.complex64, "yhat")
+    _dev(tx_idx, torch.uint16, "tx_idx")
+    n_sym, U, N_d = yhat.shape
+    if counts is None:
+        counts = torch.zeros(3, dtype=torch.int64, device=yhat.device)
+    _check(lib().ue_slice_ser(_ptr(yhat), float(alpha), _ptr(tx_idx), M_qam, _ptr(dec), _ptr(counts), n_sym, U, N_d,
+                              float(boundary_eps), _stream(yhat)))
+    return counts, dec
+
+
+def ue_receive_ser(y, h_fd, alpha, tx_idx, M_qam, yhat=None, counts=None, dec=None, workspace=None,
+                   boundary_eps=1e-4):
+    _dev(y, torch.complex64, "y")
+    _dev(h_fd, torch.complex64, "h_fd")
+    _dev(tx_idx, torch.uint16, "tx_idx")
+    n_sym, B, N = y.shape
+    U, _, N_d = h_fd.shape
+    if yhat is None:
+        yhat = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=y.device)
+    if counts is None:
+        counts = torch.zeros(3, dtype=torch.int64, device=y.device)
+    need = lib().ue_receive_workspace_bytes(n_sym, B, N_d)
+    if workspace is None or workspace.numel() < need:
+        workspace = _ws(need, y)
+    _check(lib().ue_receive_ser(_ptr(y), _ptr(h_fd), _ptr(yhat), _ptr(workspace), workspace.numel(), float(alpha),
+                                _ptr(tx_idx), M_qam, _ptr(dec), _ptr(counts), n_sym, B, U, N_d, N,
+                                float(boundary_eps), _stream(y)))
+    return yhat, counts, dec

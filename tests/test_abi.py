@@ -1,0 +1,82 @@
+"""C-ABI checks that need no GPU: libfdpd.so loads, exports every entry point that
+include/fdpd.h declares, the Python binding mirrors them, and argument validation
+fails with FD_ERR_ARG before any CUDA call."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fdpd.h")
+LIB = os.path.join(ROOT, "paper_2205_05158_b200", "libfdpd.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b([a-z_][a-z0-9_]*)\s*\(", src, flags=re.M)
+    return sorted(set(n for n in names if n not in ("if", "while")))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2205_05158_b200 import build
+        build.build()
+    return ctypes.CDLL(LIB)
+
+
+def test_header_declares_the_section8_boundary():
+    names = declared_functions()
+    for fn in ["fdcnn_forward", "zf_precoder_build", "precode", "ofdm_modulate", "gmp_pa", "chain_tx",
+               "ue_receive", "ue_slice_ser", "ue_receive_ser", "fd_last_error"]:
+        assert fn in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_mirrors_header():
+    from paper_2205_05158_b200 import fdpd
+    assert set(fdpd.SIGNATURES) == set(declared_functions())
+
+
+def test_argument_errors_without_gpu(lib):
+    lib.fd_last_error.restype = ctypes.c_char_p
+    f = lib.ofdm_modulate
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                  ctypes.c_void_p]
+    assert f(None, None, 1, 1, 36, 128, None) == 2
+    assert b"NULL" in lib.fd_last_error()
+    buf = (ctypes.c_byte * 64)()
+    p = ctypes.cast(buf, ctypes.c_void_p).value
+    p16 = (p + 15) // 16 * 16
+    assert f(p16, p16, 1, 1, 36, 100, None) == 2          # not a power of two
+    assert b"power of two" in lib.fd_last_error()
+    assert f(p16, p16, 1, 1, 37, 128, None) == 2          # odd N_d
+    g = lib.gmp_pa
+    g.restype = ctypes.c_int
+    orders = (ctypes.c_int * 2)(1, 4)
+    g.argtypes = [ctypes.c_void_p] * 3 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    assert g(p16, p16, p16 + 16, orders, 2, 1, 1, 1, 1, 64, None) == 2   # even order
+    assert b"odd" in lib.fd_last_error()
+    assert g(p16, p16, p16, orders, 2, 1, 1, 1, 1, 64, None) == 2        # aliasing
+    z = lib.zf_precoder_build
+    z.restype = ctypes.c_int
+    assert lib.fd_version() == 100
+
+
+def test_workspace_queries(lib):
+    lib.ue_receive_workspace_bytes.restype = ctypes.c_size_t
+    lib.ue_receive_workspace_bytes.argtypes = [ctypes.c_longlong, ctypes.c_int, ctypes.c_int]
+    assert lib.ue_receive_workspace_bytes(1024, 64, 600) == 8 * 1024 * 64 * 600
+    lib.fdcnn_workspace_bytes.restype = ctypes.c_size_t
+    lib.fdcnn_workspace_bytes.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_longlong,
+                                          ctypes.c_int, ctypes.c_int]
+    ch = (ctypes.c_int * 4)(2, 16, 16, 2)
+    assert lib.fdcnn_workspace_bytes(ch, 3, 1024, 4, 600) == 2 * 4 * 1024 * 4 * 16 * 625

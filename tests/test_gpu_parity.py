@@ -1,0 +1,275 @@
+"""GPU parity: every stage of the CUDA path (through the C ABI) against the fp64
+oracle on the same seeded inputs.  Bar (north star): relative L2 <= 2e-5 per stage
+output; symbol decisions identical except where the oracle's sample lies within
+1e-4 of a slicing boundary; integer counts exact under that rule."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fdpd_oracle as O
+from workload import configs, gen
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2205_05158_b200 import fdpd
+    fdpd.lib()
+    return fdpd
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.complex128)
+    b = np.asarray(b, dtype=np.complex128)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def dev(x, dtype=torch.complex64):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def crandn(rng, *shape, scale=1.0):
+    return (scale * (rng.standard_normal(shape) + 1j * rng.standard_normal(shape))).astype(np.complex64)
+
+
+# ============================================================================ a4 / FFT
+@pytest.mark.parametrize("N,Nd", [(16, 8), (32, 20), (64, 64), (128, 36), (256, 100), (512, 300), (1024, 600),
+                                  (2048, 1200), (4096, 600), (8192, 1200), (16384, 3300)])
+def test_ofdm_modulate(F, N, Nd):
+    rng = np.random.default_rng(N)
+    X = crandn(rng, 3, 5, Nd)
+    got = host(F.ofdm_modulate(dev(X), N))
+    assert rel(got, O.ofdm_modulate(X, N)) < 2e-6
+
+
+def test_ofdm_vs_brute_force_small(F):
+    rng = np.random.default_rng(0)
+    N, Nd = 64, 36
+    X = crandn(rng, 1, 2, Nd)
+    full = np.zeros((1, 2, N), complex)
+    full[..., O.data_bins(Nd, N)] = X
+    n = np.arange(N)
+    brute = full @ (np.exp(2j * np.pi * np.outer(n, n) / N) / np.sqrt(N)).T
+    assert rel(host(F.ofdm_modulate(dev(X), N)), brute) < 2e-6
+
+
+# ============================================================================ a5 / GMP
+GMP_CASES = [((1, 3, 5), 2, 1), ((1, 3, 5, 7), 4, 2), ((1, 3, 5, 7, 9), 6, 3),   # specialised
+             ((1, 5, 9), 3, 0), ((1, 3), 1, 1), ((1,), 0, 0), ((1, 3, 5, 7, 9, 11), 2, 2)]  # generic
+
+
+@pytest.mark.parametrize("orders,L,M", GMP_CASES)
+@pytest.mark.parametrize("N", [128, 4096])
+def test_gmp_pa(F, orders, L, M, N):
+    rng = np.random.default_rng(L * 10 + M)
+    Kp = len(orders)
+    ncoef = Kp * (L + 1) + 2 * (Kp - 1) * (L + 1) * M
+    x = crandn(rng, 2, 3, N, scale=0.3 / np.sqrt(2))
+    coef = crandn(rng, 3, ncoef, scale=0.1)
+    coef[:, 0] = 1.0
+    got = host(F.gmp_pa(dev(x), dev(coef), orders, L, M))
+    assert rel(got, O.gmp_pa(x, coef, orders, L, M)) < TOL
+
+
+def test_gmp_golden_3sample_wrap(F):
+    # N must be >= 16 on the GPU: embed the hand-expanded case of tests/golden/gmp_3sample.txt
+    # is impossible (N = 3); instead check the GPU on the oracle at the smallest N with full wrap.
+    rng = np.random.default_rng(3)
+    x = crandn(rng, 1, 1, 16)
+    coef = crandn(rng, 1, 8)
+    got = host(F.gmp_pa(dev(x), dev(coef), (1, 3), 1, 1))
+    assert rel(got, O.gmp_pa(x, coef, (1, 3), 1, 1)) < TOL
+
+
+# ============================================================================ a1 / CNN
+@pytest.mark.parametrize("name,nsym", [("C1", 4), ("C2", 6), ("C3", 2), ("C4", 1), ("C5", 1)])
+def test_fdcnn_forward(F, name, nsym):
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg, range(nsym))
+    got = host(F.fdcnn_forward(dev(inp["params"], torch.float32), cfg.chans, dev(inp["s"])))
+    want = O.fdcnn_forward(inp["s"], inp["params"], cfg.chans, cfg.N_d)
+    assert rel(got, want) < TOL
+    assert rel(got - inp["s"], want - inp["s"]) < 1e-4       # the residual itself
+
+
+def test_fdcnn_zero_weights_identity(F):
+    cfg = configs.C2
+    inp = gen.make_inputs(cfg, range(3), zero_cnn=True)
+    got = host(F.fdcnn_forward(dev(inp["params"], torch.float32), cfg.chans, dev(inp["s"])))
+    assert np.array_equal(got, inp["s"])
+
+
+# ============================================================================ a2 / ZF
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
+def test_zf_precoder_build(F, name):
+    cfg = configs.get(name)
+    h = gen.channel_taps(cfg)
+    h_fd, P, alpha = F.zf_precoder_build(dev(h), cfg.N_ifft, cfg.N_d, cfg.rho)
+    Hfd = O.channel_fd(h, cfg.N_ifft, cfg.N_d)
+    Po, ao, _ = O.zf_precoder(Hfd, cfg.N_ifft, cfg.rho)
+    assert rel(host(h_fd), Hfd.transpose(1, 2, 0)) < TOL
+    assert rel(host(P), Po.transpose(1, 2, 0)) < TOL
+    assert abs(alpha / ao - 1) < 1e-6
+
+
+def test_zf_antenna_rows(F):
+    cfg = configs.C2
+    h = gen.channel_taps(cfg)
+    _, Pfull, a = F.zf_precoder_build(dev(h), cfg.N_ifft, cfg.N_d, cfg.rho)
+    _, Pl, al = F.zf_precoder_build(dev(h), cfg.N_ifft, cfg.N_d, cfg.rho, b0=16, B_loc=16)
+    assert al == a and torch.equal(Pl, Pfull[16:32])
+
+
+# ============================================================================ a3 / precode, fused tx
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_precode(F, name):
+    cfg = configs.get(name)
+    rng = np.random.default_rng(1)
+    P = crandn(rng, cfg.B, cfg.U, cfg.N_d)
+    s = crandn(rng, 3, cfg.U, cfg.N_d)
+    got = host(F.precode(dev(P), dev(s)))
+    assert rel(got, O.precode(P.transpose(2, 0, 1), s)) < TOL
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_chain_tx_vs_oracle_and_unfused(F, name):
+    cfg = configs.get(name)
+    nsym = 2
+    inp = gen.make_inputs(cfg, range(nsym))
+    h_fd, P, alpha = F.zf_precoder_build(dev(inp["h_taps"]), cfg.N_ifft, cfg.N_d, cfg.rho)
+    s = dev(inp["s"])
+    coef = dev(inp["coef"])
+    y = F.chain_tx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+    y2 = F.gmp_pa(F.ofdm_modulate(F.precode(P, s), cfg.N_ifft), coef, cfg.orders, cfg.L, cfg.M)
+    assert rel(host(y), host(y2)) < 2e-6
+    Po = host(P).transpose(2, 0, 1)
+    want = O.gmp_pa(O.ofdm_modulate(O.precode(Po, inp["s"]), cfg.N_ifft), inp["coef"], cfg.orders, cfg.L, cfg.M)
+    assert rel(host(y), want) < TOL
+
+
+# ============================================================================ a6 / receive + SER
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_ue_receive(F, name):
+    cfg = configs.get(name)
+    rng = np.random.default_rng(2)
+    y = crandn(rng, 3, cfg.B, cfg.N_ifft, scale=0.2)
+    hfd = crandn(rng, cfg.U, cfg.B, cfg.N_d)
+    got = host(F.ue_receive(dev(y), dev(hfd)))
+    assert rel(got, O.ue_receive(y, hfd.transpose(2, 0, 1), cfg.N_d)) < TOL
+    acc = F.ue_receive(dev(y), dev(hfd))
+    F.ue_receive(dev(y), dev(hfd), out=acc, accumulate=True)
+    assert rel(host(acc), 2 * got) < 1e-6
+
+
+@pytest.mark.parametrize("M", [16, 64, 256])
+def test_slicer_decisions(F, M):
+    rng = np.random.default_rng(M)
+    n, U, Nd = 4, 3, 500
+    idx = rng.integers(0, M, (n, U, Nd)).astype(np.uint16)
+    alpha = 0.8
+    yhat = (alpha * (O.qam_points(idx, M) + 0.3 * crandn(rng, n, U, Nd) / np.sqrt(M))).astype(np.complex64)
+    dec_o, cnt_o = O.slice_ser(yhat, alpha, idx, M)
+    _, near = _near_mask(yhat, alpha, M)
+    dec = torch.zeros((n, U, Nd), dtype=torch.uint16, device="cuda")
+    counts, _ = F.ue_slice_ser(dev(yhat), alpha, dev(idx, torch.uint16), M, dec=dec)
+    dg = host(dec)
+    assert np.array_equal(dg[~near], dec_o[~near])
+    c = host(counts)
+    assert c[1] == n * U * Nd
+    assert abs(int(c[0]) - int(cnt_o[0])) <= int(near.sum())
+
+
+def _near_mask(yhat, alpha, M):
+    m = int(round(np.sqrt(M)))
+    cst = 1.0 / np.sqrt(2.0 * (M - 1) / 3.0)
+    z = np.asarray(yhat, np.complex128) / alpha
+    near = np.zeros(z.shape, bool)
+    for v in (z.real / cst, z.imag / cst):
+        bnd = 2.0 * np.round(v / 2.0)
+        near |= (np.abs(v - bnd) < 1e-4 / cst) & (np.abs(bnd) <= m - 2)
+    return z, near
+
+
+# ============================================================================ end to end
+def _gpu_chain(F, cfg, inp):
+    from paper_2205_05158_b200.chain import Chain, Shapes
+    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], max_batch=len(inp["symbols"]))
+    s = dev(inp["s"])
+    idx = dev(inp["idx"], torch.uint16)
+    dec = torch.zeros(idx.shape, dtype=torch.uint16, device="cuda")
+    yhat, counts, _ = ch.step(s, idx, dec=dec)
+    torch.cuda.synchronize()
+    return ch, host(ch.s_tilde[:s.shape[0]]), host(ch.y[:s.shape[0]]), host(yhat), host(counts), host(dec)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_end_to_end(F, name):
+    """C1: all 4 symbols.  C2: the full 1024-symbol batch in one call (the bench's
+    launch configuration); symbols 0, 517, 1023 compared with the oracle."""
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg)
+    ch, st, y, yhat, counts, dec = _gpu_chain(F, cfg, inp)
+    pick = list(range(cfg.n_sym)) if cfg.n_sym <= 4 else [0, 517, cfg.n_sym - 1]
+    sub = gen.make_inputs(cfg, pick)
+    o = O.run_config(cfg, sub)
+    assert abs(ch.alpha / o["alpha"] - 1) < 1e-6
+    assert rel(st[pick], o["s_tilde"]) < TOL
+    assert rel(y[pick], o["y"]) < TOL
+    assert rel(yhat[pick], o["yhat"]) < TOL
+    _, near = _near_mask(o["yhat"], o["alpha"], cfg.M_qam)
+    assert np.array_equal(dec[pick][~near], o["dec"][~near])
+    assert counts[1] == cfg.n_sym * cfg.U * cfg.N_d
+    if cfg.n_sym <= 4:
+        assert abs(int(counts[0]) - int(o["counts"][0])) <= int(near.sum())
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_invariant_zero_cnn_linear_pa(F, name):
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg, range(8 if name == "C2" else 4), zero_cnn=True, linear_pa=True)
+    ch, st, y, yhat, counts, dec = _gpu_chain(F, cfg, inp)
+    z = yhat / ch.alpha
+    assert rel(z, inp["s"]) < TOL
+    assert counts[0] == 0 and np.array_equal(dec, inp["idx"])
+
+
+# ============================================================================ edge cases / errors
+def test_empty_batch_is_noop(F):
+    cfg = configs.C1
+    x = torch.zeros((0, cfg.B, cfg.N_ifft), dtype=torch.complex64, device="cuda")
+    X = torch.zeros((0, cfg.B, cfg.N_d), dtype=torch.complex64, device="cuda")
+    assert F.ofdm_modulate(X, cfg.N_ifft).shape == (0, cfg.B, cfg.N_ifft)
+    coef = torch.zeros((cfg.B, cfg.n_coef), dtype=torch.complex64, device="cuda")
+    assert F.gmp_pa(x, coef, cfg.orders, cfg.L, cfg.M).shape == x.shape
+
+
+def test_ragged_full_band(F):
+    # N_d == N_ifft (no guards), odd symbol count
+    rng = np.random.default_rng(9)
+    X = crandn(rng, 3, 7, 64)
+    assert rel(host(F.ofdm_modulate(dev(X), 64)), O.ofdm_modulate(X, 64)) < 2e-6
+
+
+def test_argument_errors(F):
+    X = torch.zeros((1, 2, 36), dtype=torch.complex64, device="cuda")
+    with pytest.raises(F.FdpdError) as e:
+        F.ofdm_modulate(X, 100)             # not a power of two
+    assert e.value.status == F.FD_ERR_ARG
+    with pytest.raises(F.FdpdError):
+        F.ofdm_modulate(X, 32)              # N_d > N_ifft
+    x = torch.zeros((1, 2, 64), dtype=torch.complex64, device="cuda")
+    coef = torch.zeros((2, 4), dtype=torch.complex64, device="cuda")
+    with pytest.raises(F.FdpdError):
+        F.gmp_pa(x, coef, (1, 2), 1, 1)     # even order
+    with pytest.raises(F.FdpdError):
+        F.gmp_pa(x, coef, (1, 3), 1, 1, out=x)   # aliasing
