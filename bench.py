@@ -60,12 +60,13 @@ def chain_tx_flop_per_symbol(cfg):
             + gmp_flop_per_sample(cfg) * N * cfg.B)            # GMP, Eq. (9)
 
 
-def chain_bytes_per_symbol(cfg):
-    """Algorithmic HBM bytes of the step per symbol: read s, idx; write y (PA waveform) once,
-    read it back for the receive; write yhat; P and h_fd amortised over the batch."""
+def chain_bytes_per_symbol(cfg, fused=True):
+    """Algorithmic HBM bytes of the step per symbol: read s and idx, write the PA waveform y
+    once (plus read it back when the receive is not fused), write yhat; P and h_fd amortised
+    over the batch."""
     s = 8 * cfg.U * cfg.N_d
     y = 8 * cfg.B * cfg.N_ifft
-    return s + 2 * cfg.U * cfg.N_d + 2 * y + s + (16 * cfg.B * cfg.U * cfg.N_d) / cfg.n_sym
+    return s + 2 * cfg.U * cfg.N_d + (1 if fused else 2) * y + s + (16 * cfg.B * cfg.U * cfg.N_d) / cfg.n_sym
 
 
 # ============================================================================ clocks
@@ -218,10 +219,16 @@ def run_ours(args, cfg):
         st = ch.dpd(s)
         if ev is not None:
             ev[0].record(stream)
-        y = ch.tx(st)
+        if args.unfused:
+            y = ch.tx(st)
+        else:
+            _, XPA = ch.txrx(st)
         if ev is not None:
             ev[1].record(stream)
-        ch.rx(y, idx, counts=counts)
+        if args.unfused:
+            ch.rx(y, idx, counts=counts)
+        else:
+            ch.combine(XPA, idx, counts=counts)
         if ev is not None:
             ev[2].record(stream)
         if ws > 1:
@@ -261,7 +268,7 @@ def run_ours(args, cfg):
             s_d.copy_(s_h, non_blocking=True)
             i_d.copy_(i_h, non_blocking=True)
             counts.zero_()
-            ch.step(s_d, i_d, counts=counts)
+            ch.step(s_d, i_d, counts=counts, fused=not args.unfused)
             if ws > 1:
                 dist.all_reduce(counts)
             c_h.copy_(counts, non_blocking=True)
@@ -286,9 +293,12 @@ def run_ours(args, cfg):
     fp32_peak = 148 * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12       # TFLOP/s
     tx_flop = chain_tx_flop_per_symbol(cfg) * n
     achieved = tx_flop / (st_tx / 1e3) / 1e12
-    bytes_sym = chain_bytes_per_symbol(cfg)
+    bytes_sym = chain_bytes_per_symbol(cfg, fused=not args.unfused)
     hbm_achieved = bytes_sym * n * args.steps / (ms / 1e3) / 1e9
-    launches_per_step = (len(cfg.chans) - 1) + 1 + 2
+    launches_per_step = (len(cfg.chans) - 1) + 1 + (2 if args.unfused else 1)
+    if not args.unfused:                       # chain_txrx also runs the receive FFT
+        tx_flop += 5 * cfg.N_ifft * int(np.log2(cfg.N_ifft)) * cfg.B * n
+        achieved = tx_flop / (st_tx / 1e3) / 1e12
     cpu = None
     if not args.no_cpu_baseline and ws == 1 or (rank == 0 and not args.no_cpu_baseline):
         k = args.ref_symbols
@@ -301,13 +311,15 @@ def run_ours(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, workload/gen.py)",
         "config": config_dict(cfg, ws, n),
-        "roofline": {"kernel": "chain_tx (precode+IDFT+GMP fused)", "bound": "alu", "achieved": achieved,
+        "roofline": {"kernel": ("chain_tx (precode+IDFT+GMP)" if args.unfused else
+                                "chain_txrx (precode+IDFT+GMP+receive DFT)"), "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
                      "peak_src": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
-                     "flop_per_symbol": chain_tx_flop_per_symbol(cfg), "ms_per_launch": st_tx},
+                     "flop_per_symbol": tx_flop / n, "ms_per_launch": st_tx},
         "hbm": {"algorithmic_bytes_per_symbol": bytes_sym, "achieved_GBps": hbm_achieved, "peak_GBps": pk["hbm_gbs"],
                 "frac": hbm_achieved / pk["hbm_gbs"], "peak_src": pk["src"]},
-        "stage_ms": {"fdcnn": st_dpd, "chain_tx": st_tx, "ue_receive_ser": st_rx, "zf_build_once_s": t_zf},
+        "stage_ms": {"fdcnn": st_dpd, ("chain_tx" if args.unfused else "chain_txrx"): st_tx,
+                     ("ue_receive_ser" if args.unfused else "ue_combine_ser"): st_rx, "zf_build_once_s": t_zf},
         "cpu_baseline": cpu,
         "e2e": {"value": total_symbols / (ms_e2e / 1e3), "unit": "symbols/s",
                 "h2d_bytes_per_step": int(inp["s"].nbytes + inp["idx"].nbytes), "d2h_bytes_per_step": 24},
@@ -330,6 +342,7 @@ def main():
     ap.add_argument("--ref-symbols", type=int, default=64, help="oracle symbols per CPU sample (~10 s)")
     ap.add_argument("--ref-step-symbols", type=int, default=4, help="oracle symbols per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="chain_tx + ue_receive_ser instead of chain_txrx")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -131,6 +131,16 @@ int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y,
              const int* orders, int n_orders, int L, int M,
              long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream);
 
+/* Fused a3 -> a4 -> a5 -> receive DFT (first half of a6): as chain_tx, and the PA
+ * output of each (symbol, antenna) is also transformed in the same CTA:
+ *   XPA[n][b][j] = N^-1/2 sum_m y[n][b][m] exp(-j 2 pi k_j m / N)      (Eq. 4, A9)
+ *  XPA device complex64 out [n_sym][B_loc][N_d]; y (required) is written exactly as
+ *  chain_tx writes it (the receive DFT re-reads this CTA's y through L2).  Feed XPA to
+ *  ue_combine(_ser). */
+int chain_txrx(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA,
+               const int* orders, int n_orders, int L, int M,
+               long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream);
+
 /* -------------------------------------------------------------------------
  * a6. Evaluation — Eqs. (4)-(5) P:67-77 (noiseless, reading A11), SER P:351.
  *
@@ -154,6 +164,14 @@ int ue_receive(const void* y, const void* h_fd, void* yhat, void* workspace, siz
 int ue_slice_ser(const void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
                  uint16_t* dec, long long* counts, long long n_sym, int U, int N_d,
                  float boundary_eps, cudaStream_t stream);
+/* Second half of ue_receive on an XPA produced by chain_txrx (or ue_receive's FFT):
+ *   yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j];  n_sym <= 65535 per call. */
+int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, int B_loc, int U, int N_d,
+               int accumulate, cudaStream_t stream);
+/* ue_combine (accumulate = 0) fused with ue_slice_ser. */
+int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                   uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d,
+                   float boundary_eps, cudaStream_t stream);
 /* ue_receive (accumulate = 0) then ue_slice_ser, single GPU. */
 int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace, size_t workspace_bytes,
                    float alpha, const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts,

@@ -75,16 +75,35 @@ class Chain:
         return fdpd.chain_tx(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, out=self.y[:n])
 
     def rx(self, y, tx_idx, counts=None, dec=None):
+        """Unfused evaluation from the stored waveform: receive FFT + channel sum + SER."""
         n = y.shape[0]
         sh = self.sh
         counts = self.counts if counts is None else counts
         return fdpd.ue_receive_ser(y, self.h_fd, self.alpha, tx_idx, sh.M_qam, yhat=self.yhat[:n], counts=counts,
                                    dec=dec, workspace=self.ws_rx, boundary_eps=sh.eps)
 
-    def step(self, s, tx_idx, counts=None, dec=None):
-        """One pass of the hot path over a batch: s, tx_idx on the device."""
+    def txrx(self, s_tilde):
+        """Fused precode -> IDFT -> GMP (waveform stored) -> receive DFT at the data bins."""
+        n = s_tilde.shape[0]
+        sh = self.sh
+        XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
+        return fdpd.chain_txrx(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, y=self.y[:n], XPA=XPA)
+
+    def combine(self, XPA, tx_idx, counts=None, dec=None):
+        n = XPA.shape[0]
+        sh = self.sh
+        counts = self.counts if counts is None else counts
+        return fdpd.ue_combine_ser(XPA, self.h_fd, self.alpha, tx_idx, sh.M_qam, yhat=self.yhat[:n], counts=counts,
+                                   dec=dec, boundary_eps=sh.eps)
+
+    def step(self, s, tx_idx, counts=None, dec=None, fused=True):
+        """One pass of the hot path over a batch (s, tx_idx on the device):
+        fdcnn_forward -> chain_txrx -> ue_combine_ser   (fused=True, 3 libfdpd calls)
+        fdcnn_forward -> chain_tx -> ue_receive_ser     (fused=False)."""
         if s.shape[0] > self.cap:
             self.reserve(s.shape[0])
         st = self.dpd(s)
-        y = self.tx(st)
-        return self.rx(y, tx_idx, counts=counts, dec=dec)
+        if not fused:
+            return self.rx(self.tx(st), tx_idx, counts=counts, dec=dec)
+        _, XPA = self.txrx(st)
+        return self.combine(XPA, tx_idx, counts=counts, dec=dec)

@@ -45,6 +45,31 @@ __device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
     return acc;
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// sm_100 packed FP32: one FFMA2 instruction does two fp32 FMAs (same rounding as fmaf).
+__device__ __forceinline__ unsigned long long f2_pack(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+// (a.x*b.x + c.x, a.y*b.y + c.y)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+    return f2_unpack(d);
+}
+// complex coefficient times real feature, accumulated: acc += a * w
+__device__ __forceinline__ float2 cfma_real(float2 a, float w, float2 acc) { return ffma2(a, make_float2(w, w), acc); }
+// acc += a * b (complex), as two FFMA2: (a.x, a.x)*(b.x, b.y) + (-a.y, a.y)*(b.y, b.x)
+__device__ __forceinline__ float2 cfma2(float2 a, float2 b, float2 acc) {
+    acc = ffma2(make_float2(a.x, a.x), b, acc);
+    return ffma2(make_float2(-a.y, a.y), make_float2(b.y, b.x), acc);
+}
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
 // ---------------------------------------------------------------- twiddles

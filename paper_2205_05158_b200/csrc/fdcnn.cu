@@ -198,6 +198,180 @@ static int fdcnn_validate(const int* chans, int n_layers, long long n_sym, int U
     return FD_OK;
 }
 
+// ============================================================================ fused whole-network kernel
+// When two activation buffers of the widest layer fit in shared memory (C1, C2), a
+// persistent CTA keeps one image's activations on chip through every layer: the
+// weights of all layers are staged once per CTA (transposed W[ci][tap][co], co
+// padded to 4), activations ping-pong between two zero-haloed smem buffers, and
+// only the complex symbols are read / the residual written to HBM.  Pairs of output
+// channels accumulate with packed FP32 (FFMA2).
+constexpr int FUSED_THREADS = 256;
+constexpr int FUSED_MAX_LAYERS = 8;
+
+struct FusedDesc {
+    int n_layers, S, N_d, buflen;
+    int chans[FUSED_MAX_LAYERS + 1];
+    int woff[FUSED_MAX_LAYERS];   // layer weights (transposed) in smem, floats from wsm
+    int boff[FUSED_MAX_LAYERS];   // layer biases in smem
+    int poff[FUSED_MAX_LAYERS];   // layer offset in the global parameter vector
+    int wtotal;
+};
+
+__host__ __device__ inline int round4(int v) { return (v + 3) & ~3; }
+
+template <int PX>
+__device__ __forceinline__ void fused_layer(const float* __restrict__ in, int Cin, float* __restrict__ out, int Cout,
+                                            const float* __restrict__ Wt, const float* __restrict__ bias, int S,
+                                            bool last, const float2* __restrict__ s_img, float2* __restrict__ o_img,
+                                            int N_d) {
+    const int SP = S + 2;
+    const int co4 = round4(Cout);
+    const int n_cob = co4 / 4;
+    const int pxb = (S + PX - 1) / PX;
+    const int n_items = S * pxb * n_cob;
+    for (int item = threadIdx.x; item < n_items; item += FUSED_THREADS) {
+        const int cob = item % n_cob;
+        const int rest = item / n_cob;
+        const int xb = rest % pxb;
+        const int y = rest / pxb;
+        const int x0 = xb * PX;
+        float2 acc[PX][2];
+#pragma unroll
+        for (int p = 0; p < PX; ++p) acc[p][0] = acc[p][1] = make_float2(0.f, 0.f);
+        const float* wp = Wt + cob * 4;
+        for (int ci = 0; ci < Cin; ++ci) {
+            const float* ip = in + (ci * SP + y) * SP + x0;
+            float iv[3][PX + 2];
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < PX + 2; ++dx) iv[dy][dx] = ip[dy * SP + dx];
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+                const float4 w = *reinterpret_cast<const float4*>(wp + (ci * 9 + tap) * co4);
+                const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
+                const int dy = tap / 3, dx = tap % 3;
+#pragma unroll
+                for (int p = 0; p < PX; ++p) {
+                    const float xv = iv[dy][p + dx];
+                    acc[p][0] = ffma2(w01, make_float2(xv, xv), acc[p][0]);
+                    acc[p][1] = ffma2(w23, make_float2(xv, xv), acc[p][1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+            const int x = x0 + p;
+            if (x >= S) continue;
+            if (!last) {
+                float* o = out + ((cob * 4) * SP + y + 1) * SP + x + 1;
+                const int cs = SP * SP;
+                const float* bb = bias + cob * 4;
+                if (cob * 4 + 0 < Cout) o[0] = tanhf(acc[p][0].x + bb[0]);
+                if (cob * 4 + 1 < Cout) o[cs] = tanhf(acc[p][0].y + bb[1]);
+                if (cob * 4 + 2 < Cout) o[2 * cs] = tanhf(acc[p][1].x + bb[2]);
+                if (cob * 4 + 3 < Cout) o[3 * cs] = tanhf(acc[p][1].y + bb[3]);
+            } else {
+                const int k = y * S + x;          // Cout == 2: the residual on the first N_d pixels
+                if (k < N_d) {
+                    const float2 z = s_img[k];
+                    o_img[k] = make_float2(z.x + (acc[p][0].x + bias[0]), z.y + (acc[p][0].y + bias[1]));
+                }
+            }
+        }
+    }
+}
+
+template <int PX>
+__global__ void __launch_bounds__(FUSED_THREADS, 2) k_cnn_fused(const float* __restrict__ params,
+                                                             const float2* __restrict__ s_in,
+                                                             float2* __restrict__ s_out, long long n_img, FusedDesc fd) {
+    extern __shared__ __align__(16) float fsm[];
+    float* bufA = fsm;
+    float* bufB = fsm + fd.buflen;
+    float* wsm = fsm + 2 * fd.buflen;
+    const int S = fd.S, SP = S + 2;
+    // stage all layers' weights (transposed, co padded to 4) and biases
+    for (int l = 0; l < fd.n_layers; ++l) {
+        const int ci_n = fd.chans[l], co_n = fd.chans[l + 1], co4 = round4(co_n);
+        const float* W = params + fd.poff[l];
+        for (int i = threadIdx.x; i < ci_n * 9 * co4; i += FUSED_THREADS) {
+            const int co = i % co4, rest = i / co4, tap = rest % 9, c = rest / 9;
+            wsm[fd.woff[l] + i] = co < co_n ? W[(co * ci_n + c) * 9 + tap] : 0.f;
+        }
+        for (int i = threadIdx.x; i < co4; i += FUSED_THREADS)
+            wsm[fd.boff[l] + i] = i < co_n ? W[co_n * ci_n * 9 + i] : 0.f;
+    }
+    for (int i = threadIdx.x; i < 2 * fd.buflen; i += FUSED_THREADS) fsm[i] = 0.f;   // zero halos (never written)
+    __syncthreads();
+    for (long long img = blockIdx.x; img < n_img; img += gridDim.x) {
+        const float2* s_img = s_in + img * fd.N_d;
+        for (int i = threadIdx.x; i < S * S; i += FUSED_THREADS) {
+            const float2 z = i < fd.N_d ? s_img[i] : make_float2(0.f, 0.f);
+            const int r = i / S, c = i % S;
+            bufA[(0 * SP + r + 1) * SP + c + 1] = z.x;
+            bufA[(1 * SP + r + 1) * SP + c + 1] = z.y;
+        }
+        __syncthreads();
+        for (int l = 0; l < fd.n_layers; ++l) {
+            const float* in = (l & 1) ? bufB : bufA;
+            float* out = (l & 1) ? bufA : bufB;
+            fused_layer<PX>(in, fd.chans[l], out, fd.chans[l + 1], wsm + fd.woff[l], wsm + fd.boff[l], S,
+                            l == fd.n_layers - 1, s_img, s_out + img * fd.N_d, fd.N_d);
+            __syncthreads();
+        }
+    }
+}
+
+// Returns the dynamic smem bytes of the fused kernel (0 if it does not apply).
+static size_t fused_plan(const int* chans, int n_layers, int S, int N_d, FusedDesc& fd) {
+    if (n_layers > FUSED_MAX_LAYERS) return 0;
+    int cmax = 0;
+    for (int l = 0; l <= n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
+    fd.n_layers = n_layers;
+    fd.S = S;
+    fd.N_d = N_d;
+    fd.buflen = round4(cmax * (S + 2) * (S + 2) + 16);   // slack for the over-read of the last px block
+    int w = 0, p = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        const int ci = chans[l], co = chans[l + 1];
+        fd.chans[l] = ci;
+        fd.woff[l] = w;
+        w += ci * 9 * round4(co);
+        fd.boff[l] = w;
+        w += round4(co);
+        fd.poff[l] = p;
+        p += co * ci * 9 + co;
+    }
+    fd.chans[n_layers] = chans[n_layers];
+    fd.wtotal = w;
+    const size_t bytes = sizeof(float) * (2 * (size_t)fd.buflen + w);
+    return bytes <= 200 * 1024 ? bytes : 0;
+}
+
+static int pick_px(int S) {
+    int best = 4, waste = 1 << 30;
+    for (int px = 6; px >= 4; --px) {
+        const int w = ((S + px - 1) / px) * px - S;
+        if (w < waste) { waste = w; best = px; }
+    }
+    return best;
+}
+
+template <int PX>
+static int launch_fused(const float* params, const float2* s_in, float2* s_out, long long n_img, const FusedDesc& fd,
+                        size_t smem, cudaStream_t st) {
+    cudaFuncSetAttribute(k_cnn_fused<PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cnn_fused<PX>, FUSED_THREADS, smem);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long grid = std::min<long long>(n_img, (long long)nsm * std::max(per_sm, 1));
+    k_cnn_fused<PX><<<(unsigned)grid, FUSED_THREADS, smem, st>>>(params, s_in, s_out, n_img, fd);
+    return check_launch("fdcnn_forward (fused)");
+}
+
 }  // namespace fdpd
 
 using namespace fdpd;
@@ -206,6 +380,12 @@ extern "C" {
 
 size_t fdcnn_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d) {
     if (!chans || n_layers < 2 || n_sym <= 0 || U <= 0 || N_d <= 0) return 0;
+    {
+        int S = 1;
+        while (S * S < N_d) ++S;
+        FusedDesc fd;
+        if (fused_plan(chans, n_layers, S, N_d, fd)) return 0;   // fused path needs no workspace
+    }
     int cmax = 0;
     for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
     int S = 1;
@@ -230,6 +410,17 @@ int fdcnn_forward(const float* params, const int* chans, int n_layers, const voi
     const long long n_img = n_sym * U;
     const float2* sin2 = (const float2*)s_in;
     float2* sout2 = (float2*)s_out;
+    {
+        FusedDesc fd;
+        const size_t smem = fused_plan(chans, n_layers, S, N_d, fd);
+        if (smem) {
+            switch (pick_px(S)) {
+                case 6: return launch_fused<6>(params, sin2, sout2, n_img, fd, smem, stream);
+                case 5: return launch_fused<5>(params, sin2, sout2, n_img, fd, smem, stream);
+                default: return launch_fused<4>(params, sin2, sout2, n_img, fd, smem, stream);
+            }
+        }
+    }
     float* buf[2] = {(float*)workspace, nullptr};
     if (n_layers > 2) {
         int cmax = 0;

@@ -147,13 +147,23 @@ __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT],
         const int j = tid + q * T;
         const int k = j & (Ns - 1);
         if (Ns > 1) {
+            // W^{r*step}, r = 1..R-1: load the power-of-two exponents from the fp64-derived
+            // table (log2 R scattered loads instead of R-1) and build the rest with at most
+            // three complex products (~3 ulp), e.g. W^7 = (W^1 W^2) W^4.
             const int step = k * (N / (Ns * R));
+            float2 wp[R];
+            wp[0] = make_float2(1.f, 0.f);
 #pragma unroll
-            for (int r = 1; r < R; ++r) {
-                float2 w = __ldg(tw + r * step);
+            for (int p = 1; p < R; p <<= 1) {
+                float2 w = __ldg(tw + p * step);
                 if (DIR > 0) w.y = -w.y;
-                v[q * R + r] = cmul(v[q * R + r], w);
+                wp[p] = w;
             }
+#pragma unroll
+            for (int r = 3; r < R; ++r)
+                if (r & (r - 1)) wp[r] = cmul(wp[r & (r - 1)], wp[r & -r]);   // r = (r without lowest bit) + lowest bit
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], wp[r]);
         }
         dftR<R, DIR>(v, q * R);
         const int d = (j - k) * R + k;

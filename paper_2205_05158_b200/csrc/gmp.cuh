@@ -24,15 +24,56 @@ struct GmpDesc {
     int pw[GMP_MAX_ORDERS];   // (p - 1) / 2 per order
 };
 
-// Specialised path: orders = {1, 3, ..., 2 KP - 1}.
+// Shared-memory coefficient layout of the specialised path, per memory tap l
+// (STRIDE complex, 16-byte aligned rows): a_{0..KP-1,l} padded to an even count,
+// then (b_{k,l,g}, c_{k,l,g}) pairs for k = 1..KP-1, g = 1..M, so one 128-bit
+// broadcast load yields two coefficients.
+template <int KP, int M>
+struct CoefRow {
+    static constexpr int KPE = (KP + 1) & ~1;
+    static constexpr int STRIDE = KPE + 2 * (KP - 1) * M;
+};
+
+// Number of complex slots the coefficient staging needs (>= n_coef for any layout).
+__host__ __device__ inline int coef_smem_elems(int Kp, int L, int M) {
+    return (L + 1) * (((Kp + 1) & ~1) + 2 * (Kp - 1) * M);
+}
+
+// Stage antenna b's coefficients (global, SURVEY §8(b) order) into shared memory:
+// the paired layout for the specialised path (KP > 0), a plain copy otherwise.
+template <int KP, int L, int M>
+__device__ __forceinline__ void stage_coefs(const float2* __restrict__ cg, float2* __restrict__ cs, const GmpDesc& d,
+                                            int tid, int T) {
+    if constexpr (KP > 0) {
+        using Row = CoefRow<KP, M>;
+        constexpr int NA = KP * (L + 1);
+        constexpr int NB = (KP - 1) * (L + 1) * M;
+        for (int i = tid; i < (L + 1) * Row::STRIDE; i += T) {
+            const int l = i / Row::STRIDE, o = i % Row::STRIDE;
+            int src = -1;
+            if (o < Row::KPE) {
+                if (o < KP) src = o * (L + 1) + l;
+            } else {
+                const int o2 = o - Row::KPE, pr = o2 >> 1;
+                const int k = pr / M + 1, g = pr % M + 1;
+                src = NA + ((k - 1) * (L + 1) + l) * M + (g - 1) + ((o2 & 1) ? NB : 0);
+            }
+            cs[i] = src >= 0 ? cg[src] : make_float2(0.f, 0.f);
+        }
+    } else {
+        for (int i = tid; i < d.n_coef; i += T) cs[i] = cg[i];
+    }
+}
+
+// Specialised path: orders = {1, 3, ..., 2 KP - 1}; coefficients in the CoefRow layout.
+// G accumulations are packed FP32 (FFMA2: complex coefficient x real feature).
 template <int KP, int L, int M, int RS>
 __device__ __forceinline__ void gmp_group(const float2* __restrict__ usm, const float* __restrict__ esm,
                                           const float2* __restrict__ cf, int N, const int (&m)[RS],
                                           float2 (&out)[RS]) {
+    using Row = CoefRow<KP, M>;
     constexpr int W = 2 * M + 1;
     constexpr int NP = KP > 1 ? KP - 1 : 1;
-    constexpr int NA = KP * (L + 1);
-    constexpr int NB = (KP - 1) * (L + 1) * M;
     const int mask = N - 1;
     float w[RS][W][NP];
 #pragma unroll
@@ -61,37 +102,34 @@ __device__ __forceinline__ void gmp_group(const float2* __restrict__ usm, const 
                 for (int k = 1; k < NP; ++k) w[r][0][k] = w[r][0][k - 1] * e;
             }
         }
+        const float4* row = reinterpret_cast<const float4*>(cf + l * Row::STRIDE);
         float2 G[RS];
-        const float2 a1 = cf[l];
 #pragma unroll
-        for (int r = 0; r < RS; ++r) G[r] = a1;
-#pragma unroll
-        for (int k = 1; k < KP; ++k) {
-            const float2 a = cf[k * (L + 1) + l];
+        for (int kk = 0; kk < Row::KPE / 2; ++kk) {
+            const float4 q = row[kk];
+            const float2 a0 = make_float2(q.x, q.y), a1 = make_float2(q.z, q.w);
 #pragma unroll
             for (int r = 0; r < RS; ++r) {
-                G[r].x = fmaf(a.x, w[r][M][k - 1], G[r].x);
-                G[r].y = fmaf(a.y, w[r][M][k - 1], G[r].y);
+                G[r] = (kk == 0) ? a0 : cfma_real(a0, w[r][M][2 * kk - 1], G[r]);
+                if (2 * kk + 1 < KP) G[r] = cfma_real(a1, w[r][M][2 * kk], G[r]);
             }
         }
 #pragma unroll
         for (int k = 1; k < KP; ++k)
 #pragma unroll
             for (int g = 1; g <= M; ++g) {
-                const float2 bb = cf[NA + ((k - 1) * (L + 1) + l) * M + (g - 1)];
-                const float2 cc = cf[NA + NB + ((k - 1) * (L + 1) + l) * M + (g - 1)];
+                const float4 q = row[Row::KPE / 2 + (k - 1) * M + (g - 1)];
+                const float2 bb = make_float2(q.x, q.y), cc = make_float2(q.z, q.w);
 #pragma unroll
                 for (int r = 0; r < RS; ++r) {
-                    G[r].x = fmaf(bb.x, w[r][M - g][k - 1], G[r].x);
-                    G[r].y = fmaf(bb.y, w[r][M - g][k - 1], G[r].y);
-                    G[r].x = fmaf(cc.x, w[r][M + g][k - 1], G[r].x);
-                    G[r].y = fmaf(cc.y, w[r][M + g][k - 1], G[r].y);
+                    G[r] = cfma_real(bb, w[r][M - g][k - 1], G[r]);
+                    G[r] = cfma_real(cc, w[r][M + g][k - 1], G[r]);
                 }
             }
 #pragma unroll
         for (int r = 0; r < RS; ++r) {
             const float2 ul = usm[pidx((m[r] - l) & mask)];
-            out[r] = cfma(ul, G[r], out[r]);
+            out[r] = cfma2(ul, G[r], out[r]);
         }
     }
 }
@@ -159,6 +197,173 @@ __device__ __forceinline__ void gmp_symbol(const float2* __restrict__ usm, const
         }
     } else {
         for (int m = tid; m < N; m += T) y[m] = gmp_sample_generic(usm, esm, cf, N, m, d);
+    }
+}
+
+// Same as gmp_symbol for a CTA of T = fft_threads threads, but also leaves this
+// thread's outputs in `v` in the pass-0 register layout of the N-point FFT
+// (fft.cuh pass_pos): the samples a thread evaluates, {tid + T j : j < N/T}, are
+// exactly its pass-0 FFT inputs, so the receive DFT starts without a shared-memory
+// round trip.  y may be NULL (waveform not stored).
+template <int LOG2N, int KP, int L, int M, int RS>
+__device__ __forceinline__ void gmp_symbol_to_fft(const float2* __restrict__ usm, const float* __restrict__ esm,
+                                                  const float2* __restrict__ cf, const GmpDesc& d,
+                                                  float2* __restrict__ y, int tid,
+                                                  float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()]) {
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
+    constexpr int QN = VPT / R0;      // pass-0 butterflies per thread
+    // register slot of sample tid + T*j in the pass-0 layout: j = q + QN * r'
+    auto slot = [](int j) { return (j % QN) * R0 + (j / QN); };
+    if constexpr (KP > 0) {
+        static_assert(VPT % RS == 0, "RS must divide N/T");
+        constexpr int G = VPT / RS;   // sample groups per thread; group k: j = k + G r
+#pragma unroll 1
+        for (int k = 0; k < G; ++k) {
+            asm volatile("" ::: "memory");
+            int m[RS];
+            float2 out[RS];
+#pragma unroll
+            for (int r = 0; r < RS; ++r) m[r] = tid + T * (k + G * r);
+            gmp_group<KP, L, M, RS>(usm, esm, cf, N, m, out);
+#pragma unroll
+            for (int r = 0; r < RS; ++r) {
+                if (y) y[m[r]] = out[r];
+                // k is a runtime loop index: select the slot with a compile-time switch over k
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk)
+                    if (kk == k) v[slot(kk + G * r)] = out[r];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int m = tid + T * j;
+            const float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
+            if (y) y[m] = o;
+            v[slot(j)] = o;
+        }
+    }
+}
+
+}  // namespace fdpd
+
+namespace fdpd {
+
+// =============================================================================
+// Run-based specialised GMP (used by the fused kernels).
+//
+// Each thread evaluates runs of R contiguous samples [R rho, R rho + R).  The
+// envelope window e[R rho - L - M, R rho + R - 1 + M] and the input window
+// u[R rho - L, R rho + R - 1] are loaded once per run with 128-bit shared-memory
+// loads into registers (compile-time indexed), so each e/u value is read once per
+// run instead of once per (sample, tap).  u and e live in XOR-swizzled layouts
+// (16-byte chunk x -> x ^ ((x >> 3) & (chunks_per_run - 1))), which makes both the
+// per-run 128-bit window loads and the contiguous 8-byte relayout stores
+// bank-conflict free.  Coefficient rows (CoefRow layout) are broadcast-loaded once
+// per (run, tap) and feed R samples.
+// =============================================================================
+template <int R>
+struct RunLayout {
+    static constexpr int CPR_U = R / 2;   // 16-byte chunks per run of complex samples
+    static constexpr int CPR_E = R / 4;   // 16-byte chunks per run of float envelopes
+    __device__ static __forceinline__ int u_chunk(int x) { return x ^ ((x >> 3) & (CPR_U - 1)); }
+    __device__ static __forceinline__ int e_chunk(int x) { return CPR_E > 1 ? x ^ ((x >> 3) & (CPR_E - 1)) : x; }
+    __device__ static __forceinline__ int u_phys(int m) { return (u_chunk(m >> 1) << 1) | (m & 1); }
+    __device__ static __forceinline__ int e_phys(int m) { return (e_chunk(m >> 2) << 2) | (m & 3); }
+};
+
+template <int KP, int L, int M, int R>
+__device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const float* __restrict__ esw,
+                                        const float2* __restrict__ cf, int N, int rho, float2 (&out)[R]) {
+    static_assert(R % 4 == 0, "run length must be a multiple of 4");
+    using Row = CoefRow<KP, M>;
+    using Lay = RunLayout<R>;
+    constexpr int NP = KP > 1 ? KP - 1 : 1;
+    constexpr int E_LO = ((L + M) + 3) & ~3;            // envelope samples before the run (chunk aligned)
+    constexpr int E_HI = ((R + M) + 3) & ~3;            // from the run start
+    constexpr int E_N = E_LO + E_HI;
+    constexpr int U_LO = (L + 1) & ~1;                  // input samples before the run (chunk aligned)
+    constexpr int U_N = U_LO + R;
+    const int m0 = R * rho;
+
+    float ew[NP][E_N];
+    {
+        const float4* e4 = reinterpret_cast<const float4*>(esw);
+        const int xm = N / 4 - 1;
+#pragma unroll
+        for (int c = 0; c < E_N / 4; ++c) {
+            const float4 t = e4[Lay::e_chunk(((m0 - E_LO) / 4 + c) & xm)];
+            ew[0][4 * c + 0] = t.x;
+            ew[0][4 * c + 1] = t.y;
+            ew[0][4 * c + 2] = t.z;
+            ew[0][4 * c + 3] = t.w;
+        }
+#pragma unroll
+        for (int k = 1; k < NP; ++k)
+#pragma unroll
+            for (int i = 0; i < E_N; ++i) ew[k][i] = ew[k - 1][i] * ew[0][i];
+    }
+    float2 uw[U_N];
+    {
+        const float4* u4 = reinterpret_cast<const float4*>(usw);
+        const int xm = N / 2 - 1;
+#pragma unroll
+        for (int c = 0; c < U_N / 2; ++c) {
+            const float4 t = u4[Lay::u_chunk(((m0 - U_LO) / 2 + c) & xm)];
+            uw[2 * c] = make_float2(t.x, t.y);
+            uw[2 * c + 1] = make_float2(t.z, t.w);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) out[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int l = 0; l <= L; ++l) {
+        const float4* row = reinterpret_cast<const float4*>(cf + l * Row::STRIDE);
+        float2 G[R];
+        // window index of q = m0 + i - l + delta is  i - l + delta + E_LO
+#pragma unroll
+        for (int kk = 0; kk < Row::KPE / 2; ++kk) {
+            const float4 q = row[kk];
+            const float2 a0 = make_float2(q.x, q.y), a1 = make_float2(q.z, q.w);
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                G[i] = (kk == 0) ? a0 : cfma_real(a0, ew[2 * kk - 1][i - l + E_LO], G[i]);
+                if (2 * kk + 1 < KP) G[i] = cfma_real(a1, ew[2 * kk][i - l + E_LO], G[i]);
+            }
+        }
+#pragma unroll
+        for (int k = 1; k < KP; ++k)
+#pragma unroll
+            for (int g = 1; g <= M; ++g) {
+                const float4 q = row[Row::KPE / 2 + (k - 1) * M + (g - 1)];
+                const float2 bb = make_float2(q.x, q.y), cc = make_float2(q.z, q.w);
+#pragma unroll
+                for (int i = 0; i < R; ++i) {
+                    G[i] = cfma_real(bb, ew[k - 1][i - l - g + E_LO], G[i]);
+                    G[i] = cfma_real(cc, ew[k - 1][i - l + g + E_LO], G[i]);
+                }
+            }
+#pragma unroll
+        for (int i = 0; i < R; ++i) out[i] = cfma2(uw[i - l + U_LO], G[i], out[i]);
+    }
+}
+
+// Whole symbol: relayout of the (already scaled) IDFT output held in the FFT buffer
+// (pidx layout) into the swizzled u/e layouts, then all runs; y (global) gets R
+// contiguous complex per run via 128-bit stores.  usw aliases the FFT buffer.
+template <int KP, int L, int M, int R>
+__device__ __forceinline__ void gmp_runs_symbol(float2* __restrict__ buf, float* __restrict__ esw,
+                                                const float2* __restrict__ cf, int N, float2* __restrict__ y,
+                                                int tid, int T) {
+#pragma unroll 1
+    for (int rho = tid; rho < N / R; rho += T) {
+        // keep the coefficient-row loads inside the loop (no hoisting into registers)
+        asm volatile("" ::: "memory");
+        float2 out[R];
+        gmp_run<KP, L, M, R>(buf, esw, cf, N, rho, out);
+        float4* y4 = reinterpret_cast<float4*>(y + (size_t)R * rho);
+#pragma unroll
+        for (int i = 0; i < R / 2; ++i) y4[i] = make_float4(out[2 * i].x, out[2 * i].y, out[2 * i + 1].x, out[2 * i + 1].y);
     }
 }
 

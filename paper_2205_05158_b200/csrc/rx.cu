@@ -232,3 +232,36 @@ int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace,
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, int B_loc, int U, int N_d,
+               int accumulate, cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && n_sym <= 65535 && B_loc >= 1 && U >= 1 && N_d >= 1, "ue_combine: bad sizes");
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(XPA && h_fd && yhat, "ue_combine: NULL pointer");
+    FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat), "ue_combine: misaligned pointer");
+    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
+    k_rx_combine<false><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U,
+                                                 N_d, accumulate, nullptr, nullptr, nullptr, SliceParams{});
+    return check_launch("ue_combine");
+}
+
+int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                   uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d, float boundary_eps,
+                   cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && n_sym <= 65535 && B_loc >= 1 && U >= 1 && N_d >= 1, "ue_combine_ser: bad sizes");
+    SliceParams sp;
+    int rc = validate_slice(M_qam, alpha, boundary_eps, sp);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(XPA && h_fd && yhat && tx_idx && counts, "ue_combine_ser: NULL pointer");
+    FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat) && aligned8(counts),
+               "ue_combine_ser: misaligned pointer");
+    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
+    k_rx_combine<true><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U,
+                                                N_d, 0, tx_idx, dec, counts, sp);
+    return check_launch("ue_combine_ser");
+}
+
+}  // extern "C"

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256, 2) k_gmp(const float2* __restrict__ x, co
     const int tid = threadIdx.x, T = blockDim.x;
     const size_t nb = blockIdx.x;
     const int b = (int)(nb % B);
-    for (int i = tid; i < d.n_coef; i += T) cf[i] = coef[(size_t)b * d.n_coef + i];
+    stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
     const float2* xi = x + nb * N;
     for (int i = tid; i < N; i += T) {
         const float2 t = xi[i];
@@ -96,10 +96,16 @@ __global__ void __launch_bounds__(256, 2) k_gmp(const float2* __restrict__ x, co
 // ============================================================================ fused chain_tx
 // One CTA per (symbol n, antenna b): precode at the data bins straight into the
 // pass-0 registers, IDFT in shared memory, 1/sqrt(N) scale + envelope, GMP, stream y.
-template <int LOG2N, int KP, int L, int M, int RS>
+//
+// RX = true (chain_txrx): the PA output also feeds the receive DFT in the same CTA —
+// each thread's GMP outputs are exactly its pass-0 inputs of the forward FFT, so
+// they go register -> FFT -> XPA at the data bins (Eq. 4 input) with no HBM round
+// trip of the waveform; y (the PA waveform) is still streamed out unless NULL.
+template <int LOG2N, int KP, int L, int M, int RS, bool RX>
 __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     k_chain_tx(const float2* __restrict__ P, const float2* __restrict__ s, const float2* __restrict__ coef,
-               float2* __restrict__ y, const float2* __restrict__ tw, int B, int U, int N_d, float sc, GmpDesc d) {
+               float2* __restrict__ y, float2* __restrict__ XPA, const float2* __restrict__ tw, int B, int U,
+               int N_d, float sc, GmpDesc d) {
     constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* usm = reinterpret_cast<float2*>(smem_raw);
@@ -109,17 +115,53 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     const size_t nb = blockIdx.x;
     const int b = (int)(nb % B);
     const size_t n = nb / B;
-    for (int i = tid; i < d.n_coef; i += T) cf[i] = coef[(size_t)b * d.n_coef + i];
+    stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
     float2 v[VPT];
     load_precoded<LOG2N>(v, P + (size_t)b * U * N_d, s + n * U * N_d, U, N_d, tid);
     fft_run<LOG2N, +1>(usm, v, tw, tid);
+    if constexpr (KP > 0) {
+        // run-based GMP: relayout u (scaled) and e = |u|^2 into the swizzled run layouts
+        using Lay = RunLayout<RS>;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) v[j] = cscale(usm[pidx(tid + T * j)], sc);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int i = tid + T * j;
+            usm[Lay::u_phys(i)] = v[j];
+            esm[Lay::e_phys(i)] = fmaf(v[j].x, v[j].x, v[j].y * v[j].y);
+        }
+        __syncthreads();
+        float2* yo = y + nb * N;
+        gmp_runs_symbol<KP, L, M, RS>(usm, esm, cf, N, yo, tid, T);
+        if constexpr (RX) {
+            __syncthreads();   // y of the whole CTA is written (CTA-scope visibility) and u is no longer read
+            constexpr int R0 = pass_radix<LOG2N>(0);
+#pragma unroll
+            for (int q = 0; q < VPT / R0; ++q)
+#pragma unroll
+                for (int r = 0; r < R0; ++r) v[q * R0 + r] = __ldcg(yo + pass_pos<R0, VPT, T, N>(tid, q, r));
+            fft_run<LOG2N, -1>(usm, v, tw, tid);
+            float2* xo = XPA + nb * N_d;
+            for (int j = tid; j < N_d; j += T) xo[j] = cscale(usm[pidx(data_to_bin(j, N, N_d))], sc);
+        }
+        return;
+    }
     for (int i = tid; i < N; i += T) {
         const float2 t = cscale(usm[pidx(i)], sc);
         usm[pidx(i)] = t;
         esm[i] = fmaf(t.x, t.x, t.y * t.y);
     }
     __syncthreads();
-    gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
+    if constexpr (!RX) {
+        gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
+    } else {
+        gmp_symbol_to_fft<LOG2N, KP, L, M, RS>(usm, esm, cf, d, y ? y + nb * N : nullptr, tid, v);
+        __syncthreads();                       // every lagged read of u is done before the FFT overwrites it
+        fft_run<LOG2N, -1>(usm, v, tw, tid);
+        float2* xo = XPA + nb * N_d;
+        for (int j = tid; j < N_d; j += T) xo[j] = cscale(usm[pidx(data_to_bin(j, N, N_d))], sc);
+    }
 }
 
 // ============================================================================ host side
@@ -181,33 +223,33 @@ static int launch_ofdm(const float2* X, float2* x, long long n_sym, int B, int N
 template <int KP, int L, int M, int RS>
 static int launch_gmp(const float2* x, const float2* coef, float2* y, long long n_sym, int B, int N, const GmpDesc& d,
                       cudaStream_t st) {
-    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * d.n_coef;
+    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * coef_smem_elems(d.Kp, d.L, d.M);
     set_smem(k_gmp<KP, L, M, RS>, smem);
     k_gmp<KP, L, M, RS><<<(unsigned)(n_sym * B), 256, smem, st>>>(x, coef, y, B, N, d);
     return check_launch("gmp_pa");
 }
 
-template <int LOG2N, int KP, int L, int M, int RS>
-static int launch_chain_one(const float2* P, const float2* s, const float2* coef, float2* y, long long n_sym, int B,
-                            int U, int N_d, const GmpDesc& d, cudaStream_t st) {
+template <int LOG2N, int KP, int L, int M, int RS, bool RX>
+static int launch_chain_one(const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
+                            long long n_sym, int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
     constexpr int N = 1 << LOG2N;
     const float2* tw = twiddle_table(N, st);
     if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
-    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * d.n_coef;
-    set_smem(k_chain_tx<LOG2N, KP, L, M, RS>, smem);
-    k_chain_tx<LOG2N, KP, L, M, RS><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(
-        P, s, coef, y, tw, B, U, N_d, (float)(1.0 / std::sqrt((double)N)), d);
-    return check_launch("chain_tx");
+    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * coef_smem_elems(d.Kp, d.L, d.M);
+    set_smem(k_chain_tx<LOG2N, KP, L, M, RS, RX>, smem);
+    k_chain_tx<LOG2N, KP, L, M, RS, RX><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(
+        P, s, coef, y, XPA, tw, B, U, N_d, (float)(1.0 / std::sqrt((double)N)), d);
+    return check_launch(RX ? "chain_txrx" : "chain_tx");
 }
 
-template <int LOG2N>
-static int launch_chain(int variant, const float2* P, const float2* s, const float2* coef, float2* y, long long n_sym,
-                        int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
+template <int LOG2N, bool RX>
+static int launch_chain(int variant, const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
+                        long long n_sym, int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
     switch (variant) {
-        case 1: return launch_chain_one<LOG2N, 3, 2, 1, 4>(P, s, coef, y, n_sym, B, U, N_d, d, st);
-        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 4>(P, s, coef, y, n_sym, B, U, N_d, d, st);
-        case 3: return launch_chain_one<LOG2N, 5, 6, 3, 2>(P, s, coef, y, n_sym, B, U, N_d, d, st);
-        default: return launch_chain_one<LOG2N, 0, 0, 0, 1>(P, s, coef, y, n_sym, B, U, N_d, d, st);
+        case 1: return launch_chain_one<LOG2N, 3, 2, 1, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
+        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
+        case 3: return launch_chain_one<LOG2N, 5, 6, 3, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
+        default: return launch_chain_one<LOG2N, 0, 0, 0, 1, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
     }
 }
 
@@ -280,9 +322,6 @@ int gmp_pa(const void* x, const void* coef, void* y, const int* orders, int n_or
 
 int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y, const int* orders, int n_orders, int L,
              int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream) {
-    FD_REQUIRE(n_sym == 0 || (P && s_tilde && coef && y), "chain_tx: NULL pointer");
-    FD_REQUIRE(n_sym == 0 || (aligned16(P) && aligned16(s_tilde) && aligned8(coef) && aligned16(y)),
-               "chain_tx: misaligned pointer");
     FD_REQUIRE(U >= 1 && U <= 1024, "chain_tx: bad U=%d", U);
     int rc = validate_ofdm(n_sym, B_loc, N_d, N_ifft);
     if (rc) return rc;
@@ -291,9 +330,33 @@ int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y, cons
     rc = validate_gmp(orders, n_orders, L, M, N_ifft, d, variant);
     if (rc) return rc;
     if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(P && s_tilde && coef && y, "chain_tx: NULL pointer");
+    FD_REQUIRE(aligned16(P) && aligned16(s_tilde) && aligned8(coef) && aligned16(y), "chain_tx: misaligned pointer");
     const float2 *Pp = (const float2*)P, *sp = (const float2*)s_tilde, *cp = (const float2*)coef;
     float2* yp = (float2*)y;
-    FD_LOG2N_SWITCH(ilog2(N_ifft), launch_chain<LG>(variant, Pp, sp, cp, yp, n_sym, B_loc, U, N_d, d, stream));
+    FD_LOG2N_SWITCH(ilog2(N_ifft),
+                    (launch_chain<LG, false>(variant, Pp, sp, cp, yp, nullptr, n_sym, B_loc, U, N_d, d, stream)));
+}
+
+int chain_txrx(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA, const int* orders,
+               int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft,
+               cudaStream_t stream) {
+    FD_REQUIRE(U >= 1 && U <= 1024, "chain_txrx: bad U=%d", U);
+    int rc = validate_ofdm(n_sym, B_loc, N_d, N_ifft);
+    if (rc) return rc;
+    GmpDesc d;
+    int variant = 0;
+    rc = validate_gmp(orders, n_orders, L, M, N_ifft, d, variant);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(P && s_tilde && coef && y && XPA, "chain_txrx: NULL pointer");
+    FD_REQUIRE(aligned16(P) && aligned16(s_tilde) && aligned8(coef) && aligned8(XPA) && aligned16(y),
+               "chain_txrx: misaligned pointer");
+    FD_REQUIRE(y != XPA, "chain_txrx: XPA must not alias y");
+    const float2 *Pp = (const float2*)P, *sp = (const float2*)s_tilde, *cp = (const float2*)coef;
+    float2 *yp = (float2*)y, *xp = (float2*)XPA;
+    FD_LOG2N_SWITCH(ilog2(N_ifft),
+                    (launch_chain<LG, true>(variant, Pp, sp, cp, yp, xp, n_sym, B_loc, U, N_d, d, stream)));
 }
 
 }  // extern "C"

@@ -33,6 +33,9 @@ SIGNATURES = {
     "ofdm_modulate": (_i, [_vp, _vp, _ll, _i, _i, _i, _vp]),
     "gmp_pa": (_i, [_vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _vp]),
     "chain_tx": (_i, [_vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _vp]),
+    "chain_txrx": (_i, [_vp, _vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _vp]),
+    "ue_combine": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _i, _vp]),
+    "ue_combine_ser": (_i, [_vp, _vp, _vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _f, _vp]),
     "ue_receive_workspace_bytes": (_sz, [_ll, _i, _i]),
     "ue_receive": (_i, [_vp, _vp, _vp, _vp, _sz, _ll, _i, _i, _i, _i, _i, _vp]),
     "ue_slice_ser": (_i, [_vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
@@ -170,7 +173,49 @@ def chain_tx(P, s_tilde, coef, orders, L, M, N_ifft, out=None):
     return out
 
 
+def chain_txrx(P, s_tilde, coef, orders, L, M, N_ifft, y=None, XPA=None):
+    """Fused precode -> IDFT -> GMP -> receive DFT.  Returns (y [n_sym][B_loc][N_ifft], XPA [n_sym][B_loc][N_d])."""
+    _dev(P, torch.complex64, "P")
+    _dev(s_tilde, torch.complex64, "s_tilde")
+    _dev(coef, torch.complex64, "coef")
+    B, U, N_d = P.shape
+    n_sym = s_tilde.shape[0]
+    if y is None:
+        y = torch.empty((n_sym, B, N_ifft), dtype=torch.complex64, device=P.device)
+    if XPA is None:
+        XPA = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=P.device)
+    _check(lib().chain_txrx(_ptr(P), _ptr(s_tilde), _ptr(coef), _ptr(y), _ptr(XPA),
+                            _ints(orders), len(orders), L, M, n_sym, B, U, N_d, N_ifft, _stream(P)))
+    return y, XPA
+
+
 # ----------------------------------------------------------------------------- a6
+def ue_combine(XPA, h_fd, out=None, accumulate=False):
+    _dev(XPA, torch.complex64, "XPA")
+    _dev(h_fd, torch.complex64, "h_fd")
+    n_sym, B, N_d = XPA.shape
+    U = h_fd.shape[0]
+    if out is None:
+        out = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=XPA.device)
+    _check(lib().ue_combine(_ptr(XPA), _ptr(h_fd), _ptr(out), n_sym, B, U, N_d, int(bool(accumulate)),
+                            _stream(XPA)))
+    return out
+
+
+def ue_combine_ser(XPA, h_fd, alpha, tx_idx, M_qam, yhat=None, counts=None, dec=None, boundary_eps=1e-4):
+    _dev(XPA, torch.complex64, "XPA")
+    _dev(h_fd, torch.complex64, "h_fd")
+    _dev(tx_idx, torch.uint16, "tx_idx")
+    n_sym, B, N_d = XPA.shape
+    U = h_fd.shape[0]
+    if yhat is None:
+        yhat = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=XPA.device)
+    if counts is None:
+        counts = torch.zeros(3, dtype=torch.int64, device=XPA.device)
+    _check(lib().ue_combine_ser(_ptr(XPA), _ptr(h_fd), _ptr(yhat), float(alpha), _ptr(tx_idx), M_qam, _ptr(dec),
+                                _ptr(counts), n_sym, B, U, N_d, float(boundary_eps), _stream(XPA)))
+    return yhat, counts, dec
+
 def ue_receive(y, h_fd, out=None, accumulate=False, workspace=None):
     _dev(y, torch.complex64, "y")
     _dev(h_fd, torch.complex64, "h_fd")

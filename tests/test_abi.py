@@ -79,4 +79,6 @@ def test_workspace_queries(lib):
     lib.fdcnn_workspace_bytes.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_longlong,
                                           ctypes.c_int, ctypes.c_int]
     ch = (ctypes.c_int * 4)(2, 16, 16, 2)
-    assert lib.fdcnn_workspace_bytes(ch, 3, 1024, 4, 600) == 2 * 4 * 1024 * 4 * 16 * 625
+    assert lib.fdcnn_workspace_bytes(ch, 3, 1024, 4, 600) == 0          # C2: whole network in shared memory
+    ch = (ctypes.c_int * 5)(2, 32, 32, 32, 2)
+    assert lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) == 2 * 4 * 16 * 8 * 32 * 35 * 35   # C3: per-layer

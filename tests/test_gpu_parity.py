@@ -157,6 +157,38 @@ def test_chain_tx_vs_oracle_and_unfused(F, name):
     assert rel(host(y), want) < TOL
 
 
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_chain_txrx_vs_unfused(F, name):
+    """chain_txrx = chain_tx + the receive FFT of ue_receive, in one kernel; XPA feeds ue_combine."""
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg, range(3))
+    h_fd, P, alpha = F.zf_precoder_build(dev(inp["h_taps"]), cfg.N_ifft, cfg.N_d, cfg.rho)
+    s, coef = dev(inp["s"]), dev(inp["coef"])
+    y, XPA = F.chain_txrx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+    y_ref = F.chain_tx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+    assert torch.equal(y, y_ref)
+    want = np.fft.fft(host(y).astype(np.complex128), axis=-1, norm="ortho")[..., O.data_bins(cfg.N_d, cfg.N_ifft)]
+    assert rel(host(XPA), want) < 2e-6
+    yhat = F.ue_combine(XPA, h_fd)
+    assert rel(host(yhat), host(F.ue_receive(y, h_fd))) < 2e-6
+
+
+@pytest.mark.parametrize("orders,L,M", [((1, 5, 9), 3, 0), ((1, 3), 1, 1)])
+def test_chain_txrx_generic_gmp(F, orders, L, M):
+    cfg = configs.C2
+    rng = np.random.default_rng(4)
+    Kp = len(orders)
+    ncoef = Kp * (L + 1) + 2 * (Kp - 1) * (L + 1) * M
+    P = crandn(rng, cfg.B, cfg.U, cfg.N_d, scale=0.05)
+    s = crandn(rng, 2, cfg.U, cfg.N_d)
+    coef = crandn(rng, cfg.B, ncoef, scale=0.1)
+    y, XPA = F.chain_txrx(dev(P), dev(s), dev(coef), orders, L, M, cfg.N_ifft)
+    want_y = O.gmp_pa(O.ofdm_modulate(O.precode(P.transpose(2, 0, 1), s), cfg.N_ifft), coef, orders, L, M)
+    assert rel(host(y), want_y) < TOL
+    want = np.fft.fft(want_y, axis=-1, norm="ortho")[..., O.data_bins(cfg.N_d, cfg.N_ifft)]
+    assert rel(host(XPA), want) < TOL
+
+
 # ============================================================================ a6 / receive + SER
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_ue_receive(F, name):
@@ -201,24 +233,24 @@ def _near_mask(yhat, alpha, M):
 
 
 # ============================================================================ end to end
-def _gpu_chain(F, cfg, inp):
+def _gpu_chain(F, cfg, inp, fused=True):
     from paper_2205_05158_b200.chain import Chain, Shapes
     ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], max_batch=len(inp["symbols"]))
     s = dev(inp["s"])
     idx = dev(inp["idx"], torch.uint16)
     dec = torch.zeros(idx.shape, dtype=torch.uint16, device="cuda")
-    yhat, counts, _ = ch.step(s, idx, dec=dec)
+    yhat, counts, _ = ch.step(s, idx, dec=dec, fused=fused)
     torch.cuda.synchronize()
     return ch, host(ch.s_tilde[:s.shape[0]]), host(ch.y[:s.shape[0]]), host(yhat), host(counts), host(dec)
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
-def test_end_to_end(F, name):
+@pytest.mark.parametrize("name,fused", [("C1", True), ("C1", False), ("C2", True), ("C2", False)])
+def test_end_to_end(F, name, fused):
     """C1: all 4 symbols.  C2: the full 1024-symbol batch in one call (the bench's
     launch configuration); symbols 0, 517, 1023 compared with the oracle."""
     cfg = configs.get(name)
     inp = gen.make_inputs(cfg)
-    ch, st, y, yhat, counts, dec = _gpu_chain(F, cfg, inp)
+    ch, st, y, yhat, counts, dec = _gpu_chain(F, cfg, inp, fused=fused)
     pick = list(range(cfg.n_sym)) if cfg.n_sym <= 4 else [0, 517, cfg.n_sym - 1]
     sub = gen.make_inputs(cfg, pick)
     o = O.run_config(cfg, sub)
