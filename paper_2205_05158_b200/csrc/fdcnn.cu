@@ -209,7 +209,7 @@ constexpr int FUSED_THREADS = 256;
 constexpr int FUSED_MAX_LAYERS = 8;
 
 struct FusedDesc {
-    int n_layers, S, N_d, buflen;
+    int n_layers, S, N_d, buflen, rs, cs;   // rs: padded row stride, cs: channel stride (floats)
     int chans[FUSED_MAX_LAYERS + 1];
     int woff[FUSED_MAX_LAYERS];   // layer weights (transposed) in smem, floats from wsm
     int boff[FUSED_MAX_LAYERS];   // layer biases in smem
@@ -219,14 +219,17 @@ struct FusedDesc {
 
 __host__ __device__ inline int round4(int v) { return (v + 3) & ~3; }
 
-template <int PX>
+// One layer of the fused network on smem activations [c][row][col] (row stride rs,
+// channel stride cs, one-pixel zero halo).  Thread item = PX pixels of one row x CO_T
+// output channels; weights Wt[ci][tap][co] with co padded to cop (multiple of 4).
+template <int PX, int CO_T>
 __device__ __forceinline__ void fused_layer(const float* __restrict__ in, int Cin, float* __restrict__ out, int Cout,
                                             const float* __restrict__ Wt, const float* __restrict__ bias, int S,
-                                            bool last, const float2* __restrict__ s_img, float2* __restrict__ o_img,
-                                            int N_d) {
-    const int SP = S + 2;
-    const int co4 = round4(Cout);
-    const int n_cob = co4 / 4;
+                                            int rs, int cs, bool last, const float2* __restrict__ s_img,
+                                            float2* __restrict__ o_img, int N_d) {
+    static_assert(CO_T == 2 || CO_T == 4 || CO_T == 8, "CO_T");
+    const int cop = round4(Cout);
+    const int n_cob = (Cout + CO_T - 1) / CO_T;
     const int pxb = (S + PX - 1) / PX;
     const int n_items = S * pxb * n_cob;
     for (int item = threadIdx.x; item < n_items; item += FUSED_THREADS) {
@@ -235,27 +238,39 @@ __device__ __forceinline__ void fused_layer(const float* __restrict__ in, int Ci
         const int xb = rest % pxb;
         const int y = rest / pxb;
         const int x0 = xb * PX;
-        float2 acc[PX][2];
+        float2 acc[PX][CO_T / 2];
 #pragma unroll
-        for (int p = 0; p < PX; ++p) acc[p][0] = acc[p][1] = make_float2(0.f, 0.f);
-        const float* wp = Wt + cob * 4;
+        for (int p = 0; p < PX; ++p)
+#pragma unroll
+            for (int h = 0; h < CO_T / 2; ++h) acc[p][h] = make_float2(0.f, 0.f);
+        const float* wp = Wt + cob * CO_T;
         for (int ci = 0; ci < Cin; ++ci) {
-            const float* ip = in + (ci * SP + y) * SP + x0;
+            const float* ip = in + ci * cs + y * rs + x0;
             float iv[3][PX + 2];
 #pragma unroll
             for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-                for (int dx = 0; dx < PX + 2; ++dx) iv[dy][dx] = ip[dy * SP + dx];
+                for (int dx = 0; dx < PX + 2; ++dx) iv[dy][dx] = ip[dy * rs + dx];
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
-                const float4 w = *reinterpret_cast<const float4*>(wp + (ci * 9 + tap) * co4);
-                const float2 w01 = make_float2(w.x, w.y), w23 = make_float2(w.z, w.w);
+                float2 w[CO_T / 2];
+                const float* wt = wp + (ci * 9 + tap) * cop;
+                if constexpr (CO_T == 2) {
+                    w[0] = *reinterpret_cast<const float2*>(wt);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < CO_T / 4; ++h) {
+                        const float4 q = *reinterpret_cast<const float4*>(wt + 4 * h);
+                        w[2 * h] = make_float2(q.x, q.y);
+                        w[2 * h + 1] = make_float2(q.z, q.w);
+                    }
+                }
                 const int dy = tap / 3, dx = tap % 3;
 #pragma unroll
                 for (int p = 0; p < PX; ++p) {
                     const float xv = iv[dy][p + dx];
-                    acc[p][0] = ffma2(w01, make_float2(xv, xv), acc[p][0]);
-                    acc[p][1] = ffma2(w23, make_float2(xv, xv), acc[p][1]);
+#pragma unroll
+                    for (int h = 0; h < CO_T / 2; ++h) acc[p][h] = ffma2(w[h], make_float2(xv, xv), acc[p][h]);
                 }
             }
         }
@@ -264,13 +279,13 @@ __device__ __forceinline__ void fused_layer(const float* __restrict__ in, int Ci
             const int x = x0 + p;
             if (x >= S) continue;
             if (!last) {
-                float* o = out + ((cob * 4) * SP + y + 1) * SP + x + 1;
-                const int cs = SP * SP;
-                const float* bb = bias + cob * 4;
-                if (cob * 4 + 0 < Cout) o[0] = tanhf(acc[p][0].x + bb[0]);
-                if (cob * 4 + 1 < Cout) o[cs] = tanhf(acc[p][0].y + bb[1]);
-                if (cob * 4 + 2 < Cout) o[2 * cs] = tanhf(acc[p][1].x + bb[2]);
-                if (cob * 4 + 3 < Cout) o[3 * cs] = tanhf(acc[p][1].y + bb[3]);
+                float* o = out + (cob * CO_T) * cs + (y + 1) * rs + x + 1;
+                const float* bb = bias + cob * CO_T;
+#pragma unroll
+                for (int h = 0; h < CO_T / 2; ++h) {
+                    if (cob * CO_T + 2 * h < Cout) o[(2 * h) * cs] = tanhf(acc[p][h].x + bb[2 * h]);
+                    if (cob * CO_T + 2 * h + 1 < Cout) o[(2 * h + 1) * cs] = tanhf(acc[p][h].y + bb[2 * h + 1]);
+                }
             } else {
                 const int k = y * S + x;          // Cout == 2: the residual on the first N_d pixels
                 if (k < N_d) {
@@ -283,6 +298,15 @@ __device__ __forceinline__ void fused_layer(const float* __restrict__ in, int Ci
 }
 
 template <int PX>
+__device__ __forceinline__ void fused_layer_any(const float* in, int Cin, float* out, int Cout, const float* Wt,
+                                                const float* bias, int S, int rs, int cs, bool last,
+                                                const float2* s_img, float2* o_img, int N_d) {
+    if (Cout % 8 == 0) fused_layer<PX, 8>(in, Cin, out, Cout, Wt, bias, S, rs, cs, last, s_img, o_img, N_d);
+    else if (Cout == 2) fused_layer<PX, 2>(in, Cin, out, Cout, Wt, bias, S, rs, cs, last, s_img, o_img, N_d);
+    else fused_layer<PX, 4>(in, Cin, out, Cout, Wt, bias, S, rs, cs, last, s_img, o_img, N_d);
+}
+
+template <int PX>
 __global__ void __launch_bounds__(FUSED_THREADS, 2) k_cnn_fused(const float* __restrict__ params,
                                                              const float2* __restrict__ s_in,
                                                              float2* __restrict__ s_out, long long n_img, FusedDesc fd) {
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) k_cnn_fused(const float* __r
     float* bufA = fsm;
     float* bufB = fsm + fd.buflen;
     float* wsm = fsm + 2 * fd.buflen;
-    const int S = fd.S, SP = S + 2;
+    const int S = fd.S, rs = fd.rs, cs = fd.cs;
     // stage all layers' weights (transposed, co padded to 4) and biases
     for (int l = 0; l < fd.n_layers; ++l) {
         const int ci_n = fd.chans[l], co_n = fd.chans[l + 1], co4 = round4(co_n);
@@ -309,19 +333,21 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) k_cnn_fused(const float* __r
         for (int i = threadIdx.x; i < S * S; i += FUSED_THREADS) {
             const float2 z = i < fd.N_d ? s_img[i] : make_float2(0.f, 0.f);
             const int r = i / S, c = i % S;
-            bufA[(0 * SP + r + 1) * SP + c + 1] = z.x;
-            bufA[(1 * SP + r + 1) * SP + c + 1] = z.y;
+            bufA[0 * cs + (r + 1) * rs + c + 1] = z.x;
+            bufA[1 * cs + (r + 1) * rs + c + 1] = z.y;
         }
         __syncthreads();
         for (int l = 0; l < fd.n_layers; ++l) {
             const float* in = (l & 1) ? bufB : bufA;
             float* out = (l & 1) ? bufA : bufB;
-            fused_layer<PX>(in, fd.chans[l], out, fd.chans[l + 1], wsm + fd.woff[l], wsm + fd.boff[l], S,
-                            l == fd.n_layers - 1, s_img, s_out + img * fd.N_d, fd.N_d);
+            fused_layer_any<PX>(in, fd.chans[l], out, fd.chans[l + 1], wsm + fd.woff[l], wsm + fd.boff[l], S, rs, cs,
+                                l == fd.n_layers - 1, s_img, s_out + img * fd.N_d, fd.N_d);
             __syncthreads();
         }
     }
 }
+
+static int pick_px(int S);
 
 // Returns the dynamic smem bytes of the fused kernel (0 if it does not apply).
 static size_t fused_plan(const int* chans, int n_layers, int S, int N_d, FusedDesc& fd) {
@@ -331,7 +357,31 @@ static size_t fused_plan(const int* chans, int n_layers, int S, int N_d, FusedDe
     fd.n_layers = n_layers;
     fd.S = S;
     fd.N_d = N_d;
-    fd.buflen = round4(cmax * (S + 2) * (S + 2) + 16);   // slack for the over-read of the last px block
+    // row stride: S + 2 padded so that the input rows one warp's items read hit distinct
+    // banks (simulated for the widest layer's item mapping; same address = broadcast)
+    {
+        const int px = pick_px(S), pxb = (S + px - 1) / px;
+        const int n_cob = cmax % 8 == 0 ? cmax / 8 : (cmax + 3) / 4;
+        int best = S + 2, best_deg = 1 << 30;
+        for (int rs = S + 2; rs < S + 2 + 32; ++rs) {
+            int deg = 0;
+            for (int warp = 0; warp < 8; ++warp) {
+                int addr[32];
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int item = warp * 32 + lane, rest = item / n_cob;
+                    addr[lane] = (rest / pxb) * rs + (rest % pxb) * px;
+                }
+                std::sort(addr, addr + 32);
+                const int nu = (int)(std::unique(addr, addr + 32) - addr);
+                int cnt[32] = {0};
+                for (int i = 0; i < nu; ++i) deg = std::max(deg, ++cnt[addr[i] & 31]);
+            }
+            if (deg < best_deg) { best_deg = deg; best = rs; }
+        }
+        fd.rs = best;
+    }
+    fd.cs = fd.rs * (S + 2);
+    fd.buflen = round4(cmax * fd.cs + 16);   // slack for the over-read of the last px block
     int w = 0, p = 0;
     for (int l = 0; l < n_layers; ++l) {
         const int ci = chans[l], co = chans[l + 1];
