@@ -351,10 +351,11 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
 // Whole symbol: relayout of the (already scaled) IDFT output held in the FFT buffer
 // (pidx layout) into the swizzled u/e layouts, then all runs; y (global) gets R
 // contiguous complex per run via 128-bit stores.  usw aliases the FFT buffer.
-template <int KP, int L, int M, int R>
+// ysm (optional): also store the outputs in shared memory in the FFT's pidx layout.
+template <int KP, int L, int M, int R, bool YS = false>
 __device__ __forceinline__ void gmp_runs_symbol(float2* __restrict__ buf, float* __restrict__ esw,
                                                 const float2* __restrict__ cf, int N, float2* __restrict__ y,
-                                                int tid, int T) {
+                                                int tid, int T, float2* __restrict__ ysm = nullptr) {
 #pragma unroll 1
     for (int rho = tid; rho < N / R; rho += T) {
         // keep the coefficient-row loads inside the loop (no hoisting into registers)
@@ -364,6 +365,10 @@ __device__ __forceinline__ void gmp_runs_symbol(float2* __restrict__ buf, float*
         float4* y4 = reinterpret_cast<float4*>(y + (size_t)R * rho);
 #pragma unroll
         for (int i = 0; i < R / 2; ++i) y4[i] = make_float4(out[2 * i].x, out[2 * i].y, out[2 * i + 1].x, out[2 * i + 1].y);
+        if constexpr (YS) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) ysm[pidx(R * rho + i)] = out[i];
+        }
     }
 }
 
