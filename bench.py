@@ -192,6 +192,7 @@ def run_ours(args, cfg):
     import torch.distributed as dist
 
     from paper_2205_05158_b200 import fdpd
+    from paper_2205_05158_b200 import dist as D
     from paper_2205_05158_b200.chain import Chain, Shapes
 
     ws, rank, local = init_dist()
@@ -201,7 +202,7 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     fdpd.lib()
     n = args.batch or cfg.n_sym
-    symbols = range(rank * n, rank * n + n)
+    symbols = D.symbol_range(n, rank)          # Mode S, weak scaling
     inp = gen.make_inputs(cfg, symbols)
 
     t_zf0 = time.perf_counter()
@@ -232,7 +233,7 @@ def run_ours(args, cfg):
         if ev is not None:
             ev[2].record(stream)
         if ws > 1:
-            dist.all_reduce(counts)
+            D.allreduce_counts(counts)
 
     for _ in range(args.warmup):
         step()
@@ -270,7 +271,7 @@ def run_ours(args, cfg):
             counts.zero_()
             ch.step(s_d, i_d, counts=counts, fused=not args.unfused)
             if ws > 1:
-                dist.all_reduce(counts)
+                D.allreduce_counts(counts)
             c_h.copy_(counts, non_blocking=True)
             e2e_ev[i][1].record(stream)
         torch.cuda.synchronize()

@@ -1,0 +1,95 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the N>1 partitioning logic in
+paper_2205_05158_b200/dist.py, with the fp64 oracle as the per-rank compute:
+  * Mode S (symbol batches): per-rank SER counters all-reduced == unsharded counters.
+  * Mode A (antennas): all-gathered symbol-sharded s_tilde == unsharded s_tilde, and
+    the all-reduced per-rank partial channel sums == the unsharded received signal."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import fdpd_oracle as O
+from workload import configs, gen
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, mode, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2205_05158_b200 import dist as D
+    try:
+        cfg = configs.C1
+        if mode == "S":
+            per = 3
+            inp = gen.make_inputs(cfg, D.symbol_range(per, rank))
+            out = O.run_config(cfg, inp)
+            c = torch.tensor(out["counts"], dtype=torch.int64)
+            D.allreduce_counts(c)
+            q.put((rank, c.numpy()))
+        else:
+            n_total = 5
+            inp = gen.make_inputs(cfg, range(n_total))
+            s0, n_loc = D.split(n_total, world, rank)
+            st_loc = O.fdcnn_forward(inp["s"][s0:s0 + n_loc], inp["params"], cfg.chans, cfg.N_d)
+            st = D.allgather_symbols(torch.from_numpy(st_loc), n_total).numpy()
+            Hfd = O.channel_fd(inp["h_taps"], cfg.N_ifft, cfg.N_d)
+            P, alpha, _ = O.zf_precoder(Hfd, cfg.N_ifft, cfg.rho)
+            b0, B_loc = D.antenna_shard(cfg.B, world, rank)
+            X = O.precode(P[:, b0:b0 + B_loc, :], st)
+            y = O.gmp_pa(O.ofdm_modulate(X, cfg.N_ifft), inp["coef"][b0:b0 + B_loc], cfg.orders, cfg.L, cfg.M)
+            part = O.ue_receive(y, Hfd[:, :, b0:b0 + B_loc], cfg.N_d)
+            yhat = D.allreduce_partial(torch.from_numpy(part)).numpy()
+            q.put((rank, (st, yhat)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(mode, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_symbol_batch_counts_allreduce():
+    res = _run("S")
+    cfg = configs.C1
+    want = O.run_config(cfg, gen.make_inputs(cfg, range(6)))["counts"]
+    for r in (0, 1):
+        assert np.array_equal(res[r], want)
+
+
+def test_antenna_mode_allgather_and_partial_sum():
+    res = _run("A")
+    cfg = configs.C1
+    full = O.run_config(cfg, gen.make_inputs(cfg, range(5)))
+    for r in (0, 1):
+        st, yhat = res[r]
+        assert np.max(np.abs(st - full["s_tilde"])) < 1e-12
+        assert np.max(np.abs(yhat - full["yhat"])) < 1e-12 * max(1.0, np.max(np.abs(full["yhat"])))
+
+
+def test_split_covers_everything():
+    from paper_2205_05158_b200 import dist as D
+    for n in (1, 7, 64, 512):
+        for w in (1, 2, 3, 8):
+            parts = [D.split(n, w, r) for r in range(w)]
+            assert sum(c for _, c in parts) == n
+            assert all(parts[i][0] + parts[i][1] == parts[i + 1][0] for i in range(w - 1))

@@ -275,6 +275,26 @@ def test_invariant_zero_cnn_linear_pa(F, name):
     assert counts[0] == 0 and np.array_equal(dec, inp["idx"])
 
 
+@pytest.mark.parametrize("name,shards", [("C1", 2), ("C2", 4)])
+def test_antenna_shards_accumulate_to_full(F, name, shards):
+    """Mode A through the ABI on one GPU: per-shard ZF rows, chain_txrx on the shard's
+    antennas and ue_combine(accumulate) over shards == the unsharded received signal."""
+    from paper_2205_05158_b200 import dist as D
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg, range(3))
+    h, s, coef = dev(inp["h_taps"]), dev(inp["s"]), dev(inp["coef"])
+    h_fd, P, _ = F.zf_precoder_build(h, cfg.N_ifft, cfg.N_d, cfg.rho)
+    _, XPA = F.chain_txrx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+    full = F.ue_combine(XPA, h_fd)
+    acc = torch.zeros_like(full)
+    for r in range(shards):
+        b0, bl = D.antenna_shard(cfg.B, shards, r)
+        hf_r, P_r, _ = F.zf_precoder_build(h, cfg.N_ifft, cfg.N_d, cfg.rho, b0=b0, B_loc=bl)
+        _, X_r = F.chain_txrx(P_r, s, coef[b0:b0 + bl].contiguous(), cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+        F.ue_combine(X_r, hf_r, out=acc, accumulate=True)
+    assert rel(host(acc), host(full)) < 1e-6
+
+
 # ============================================================================ edge cases / errors
 def test_empty_batch_is_noop(F):
     cfg = configs.C1
