@@ -178,6 +178,40 @@ int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace,
                    long long n_sym, int B_loc, int U, int N_d, int N_ifft, float boundary_eps,
                    cudaStream_t stream);
 
+/* -------------------------------------------------------------------------
+ * Native chain runtime: a plan owning the device-resident state of one channel
+ * realisation and running the whole hot path per batch of OFDM symbols
+ * (a1 -> a3..a5 -> a6 = fdcnn_forward -> chain_txrx -> ue_combine_ser).
+ * Unlike the calls above, the plan allocates (cudaMalloc at create) and the host
+ * variant synchronises; everything else follows the conventions above.
+ * ------------------------------------------------------------------------- */
+#define FD_CHAIN_MAX_LAYERS 8
+typedef struct fd_chain_desc {
+    int U, B, T, N_d, N_ifft, M_qam;
+    int n_layers, chans[FD_CHAIN_MAX_LAYERS + 1];   /* FD-CNN (fdcnn_forward) */
+    int n_orders, orders[8], L, M;                   /* GMP PA (gmp_pa) */
+    float rho;                                       /* TD RMS target for alpha (A12) */
+    float boundary_eps;                              /* SER near-boundary band (1e-4) */
+} fd_chain_desc;
+typedef struct fd_chain fd_chain;
+
+/* Copies the HOST arrays h_taps [T][U][B] complex64, coef [B][n_coef] complex64 and
+ * params (float) to the device, builds the ZF precoder (zf_precoder_build; synchronises)
+ * and reserves buffers for batches of up to max_batch symbols. */
+int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_taps, const void* coef,
+                    const float* params, long long max_batch, cudaStream_t stream);
+float fd_chain_alpha(const fd_chain* chain);
+void fd_chain_destroy(fd_chain* chain);
+/* Device buffers: s [n_sym][U][N_d] complex64, tx_idx uint16 same shape, counts device
+ * int64[3] accumulated (caller zeroes); yhat optional device [n_sym][U][N_d] output
+ * (NULL: plan-owned).  Asynchronous. */
+int fd_chain_run_device(fd_chain* chain, const void* s, const uint16_t* tx_idx, long long n_sym,
+                        long long* counts, void* yhat, cudaStream_t stream);
+/* HOST buffers (pinned for async copies): copies s and tx_idx in, runs the step, copies
+ * the three SER counters (errors, total, near) back and synchronises `stream`. */
+int fd_chain_run_host(fd_chain* chain, const void* s_host, const uint16_t* tx_idx_host, long long n_sym,
+                      long long* counts_host, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

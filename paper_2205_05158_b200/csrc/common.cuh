@@ -63,6 +63,26 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
     return f2_unpack(d);
 }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(d);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(d);
+}
+// complex product with packed FP32 (FMUL2 + FFMA2), rounding identical to cmul()
+__device__ __forceinline__ float2 cmul2(float2 a, float2 b) {
+    const float2 t = fmul2(make_float2(-a.y, a.y), make_float2(b.y, b.x));
+    return ffma2(make_float2(a.x, a.x), b, t);
+}
 // complex coefficient times real feature, accumulated: acc += a * w
 __device__ __forceinline__ float2 cfma_real(float2 a, float w, float2 acc) { return ffma2(a, make_float2(w, w), acc); }
 // acc += a * b (complex), as two FFMA2: (a.x, a.x)*(b.x, b.y) + (-a.y, a.y)*(b.y, b.x)

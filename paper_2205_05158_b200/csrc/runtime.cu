@@ -1,0 +1,160 @@
+// runtime.cu — native chain runtime: a device-resident plan for one channel
+// realisation (CNN weights, PA coefficients, ZF precoder, workspaces) and the step
+// entry points that run the whole hot path from host or device buffers.
+//
+// Step = fdcnn_forward -> chain_txrx -> ue_combine_ser (include/fdpd.h); the host
+// variant adds the host->device copy of the step's inputs and the device->host copy
+// of the SER counters on the same stream (cudaMemcpyAsync, one per buffer).
+#include "common.cuh"
+
+#include <new>
+#include <vector>
+
+struct fd_chain {
+    fd_chain_desc d;
+    int n_coef = 0, n_params = 0, N_d_pad = 0;
+    long long cap = 0;
+    float alpha = 0.f;
+    // device buffers owned by the plan
+    float2 *h_taps = nullptr, *coef = nullptr, *h_fd = nullptr, *P = nullptr;
+    float* params = nullptr;
+    float2 *s = nullptr, *s_tilde = nullptr, *y = nullptr, *XPA = nullptr, *yhat = nullptr;
+    uint16_t* idx = nullptr;
+    long long* counts = nullptr;
+    void* ws_cnn = nullptr;
+    size_t ws_cnn_bytes = 0;
+    void* ws_zf = nullptr;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+    if (n == 0) n = 1;
+    if (cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)) != cudaSuccess) {
+        fdpd::set_error("fd_chain: cudaMalloc of %zu bytes failed", n * sizeof(T));
+        return FD_ERR_CUDA;
+    }
+    return FD_OK;
+}
+
+void release(fd_chain* c) {
+    if (!c) return;
+    void* ptrs[] = {c->h_taps, c->coef, c->h_fd, c->P, c->params, c->s, c->s_tilde, c->y,
+                    c->XPA, c->yhat, c->idx, c->counts, c->ws_cnn, c->ws_zf};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete c;
+}
+
+int ensure_batch(fd_chain* c, long long n) {
+    if (n <= c->cap) return FD_OK;
+    const fd_chain_desc& d = c->d;
+    void* old[] = {c->s, c->s_tilde, c->y, c->XPA, c->yhat, c->idx, c->ws_cnn};
+    for (void* p : old)
+        if (p) cudaFree(p);
+    c->s = c->s_tilde = c->y = c->XPA = c->yhat = nullptr;
+    c->idx = nullptr;
+    c->ws_cnn = nullptr;
+    int rc;
+    if ((rc = dalloc(&c->s, (size_t)n * d.U * d.N_d))) return rc;
+    if ((rc = dalloc(&c->s_tilde, (size_t)n * d.U * d.N_d))) return rc;
+    if ((rc = dalloc(&c->y, (size_t)n * d.B * d.N_ifft))) return rc;
+    if ((rc = dalloc(&c->XPA, (size_t)n * d.B * d.N_d))) return rc;
+    if ((rc = dalloc(&c->yhat, (size_t)n * d.U * d.N_d))) return rc;
+    if ((rc = dalloc(&c->idx, (size_t)n * d.U * d.N_d))) return rc;
+    c->ws_cnn_bytes = fdcnn_workspace_bytes(d.chans, d.n_layers, n, d.U, d.N_d);
+    if (c->ws_cnn_bytes && (rc = dalloc(reinterpret_cast<char**>(&c->ws_cnn), c->ws_cnn_bytes))) return rc;
+    c->cap = n;
+    return FD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_taps, const void* coef,
+                    const float* params, long long max_batch, cudaStream_t stream) {
+    FD_REQUIRE(out && desc && h_taps && coef && params, "fd_chain_create: NULL pointer");
+    *out = nullptr;
+    const fd_chain_desc& d = *desc;
+    FD_REQUIRE(d.U >= 1 && d.B >= d.U && d.T >= 1 && d.N_d >= 2 && d.N_ifft >= d.N_d, "fd_chain_create: bad sizes");
+    FD_REQUIRE(d.n_layers >= 1 && d.n_layers <= FD_CHAIN_MAX_LAYERS, "fd_chain_create: n_layers");
+    FD_REQUIRE(d.n_orders >= 1 && d.n_orders <= 8, "fd_chain_create: n_orders");
+    FD_REQUIRE(max_batch >= 0, "fd_chain_create: max_batch < 0");
+    fd_chain* c = new (std::nothrow) fd_chain();
+    if (!c) return fdpd::fail_arg("fd_chain_create: out of host memory");
+    c->d = d;
+    c->n_coef = d.n_orders * (d.L + 1) + 2 * (d.n_orders - 1) * (d.L + 1) * d.M;
+    for (int l = 0; l < d.n_layers; ++l) c->n_params += d.chans[l + 1] * d.chans[l] * 9 + d.chans[l + 1];
+    int rc;
+    const cudaMemcpyKind h2d = cudaMemcpyHostToDevice;
+#define FD_TRY(x)              \
+    if ((rc = (x)) != FD_OK) { \
+        release(c);            \
+        return rc;             \
+    }
+    FD_TRY(dalloc(&c->h_taps, (size_t)d.T * d.U * d.B));
+    FD_TRY(dalloc(&c->coef, (size_t)d.B * c->n_coef));
+    FD_TRY(dalloc(&c->params, (size_t)c->n_params));
+    FD_TRY(dalloc(&c->h_fd, (size_t)d.U * d.B * d.N_d));
+    FD_TRY(dalloc(&c->P, (size_t)d.B * d.U * d.N_d));
+    FD_TRY(dalloc(&c->counts, 3));
+    FD_TRY(dalloc(reinterpret_cast<char**>(&c->ws_zf), zf_workspace_bytes(d.N_d)));
+    if (cudaMemcpyAsync(c->h_taps, h_taps, sizeof(float2) * (size_t)d.T * d.U * d.B, h2d, stream) != cudaSuccess ||
+        cudaMemcpyAsync(c->coef, coef, sizeof(float2) * (size_t)d.B * c->n_coef, h2d, stream) != cudaSuccess ||
+        cudaMemcpyAsync(c->params, params, sizeof(float) * (size_t)c->n_params, h2d, stream) != cudaSuccess) {
+        release(c);
+        return fdpd::check_launch("fd_chain_create (upload)");
+    }
+    // a2: ZF precoder, once per channel realisation (synchronises)
+    FD_TRY(zf_precoder_build(c->h_taps, d.T, d.U, d.B, d.N_ifft, d.N_d, d.rho, 0, d.B, c->h_fd, c->P, &c->alpha,
+                             c->ws_zf, zf_workspace_bytes(d.N_d), stream));
+    FD_TRY(ensure_batch(c, max_batch));
+#undef FD_TRY
+    *out = c;
+    return FD_OK;
+}
+
+float fd_chain_alpha(const fd_chain* c) { return c ? c->alpha : 0.f; }
+
+void fd_chain_destroy(fd_chain* c) { release(c); }
+
+int fd_chain_run_device(fd_chain* c, const void* s, const uint16_t* tx_idx, long long n_sym, long long* counts,
+                        void* yhat, cudaStream_t stream) {
+    FD_REQUIRE(c && s && tx_idx && counts, "fd_chain_run_device: NULL pointer");
+    FD_REQUIRE(n_sym >= 0 && n_sym <= c->cap, "fd_chain_run_device: n_sym=%lld exceeds the plan's batch %lld", n_sym,
+               c->cap);
+    if (n_sym == 0) return FD_OK;
+    const fd_chain_desc& d = c->d;
+    int rc = fdcnn_forward(c->params, d.chans, d.n_layers, s, c->s_tilde, c->ws_cnn, c->ws_cnn_bytes, n_sym, d.U,
+                           d.N_d, stream);
+    if (rc) return rc;
+    rc = chain_txrx(c->P, c->s_tilde, c->coef, c->y, c->XPA, d.orders, d.n_orders, d.L, d.M, n_sym, d.B, d.U, d.N_d,
+                    d.N_ifft, stream);
+    if (rc) return rc;
+    return ue_combine_ser(c->XPA, c->h_fd, yhat ? yhat : c->yhat, c->alpha, tx_idx, d.M_qam, nullptr, counts, n_sym,
+                          d.B, d.U, d.N_d, d.boundary_eps, stream);
+}
+
+int fd_chain_run_host(fd_chain* c, const void* s_host, const uint16_t* idx_host, long long n_sym,
+                      long long* counts_host, cudaStream_t stream) {
+    FD_REQUIRE(c && s_host && idx_host && counts_host, "fd_chain_run_host: NULL pointer");
+    FD_REQUIRE(n_sym >= 0 && n_sym <= c->cap, "fd_chain_run_host: n_sym=%lld exceeds the plan's batch %lld", n_sym,
+               c->cap);
+    const fd_chain_desc& d = c->d;
+    const size_t ns = (size_t)n_sym * d.U * d.N_d;
+    if (cudaMemcpyAsync(c->s, s_host, sizeof(float2) * ns, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+        cudaMemcpyAsync(c->idx, idx_host, sizeof(uint16_t) * ns, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+        cudaMemsetAsync(c->counts, 0, 3 * sizeof(long long), stream) != cudaSuccess)
+        return fdpd::check_launch("fd_chain_run_host (h2d)");
+    int rc = fd_chain_run_device(c, c->s, c->idx, n_sym, c->counts, nullptr, stream);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(counts_host, c->counts, 3 * sizeof(long long), cudaMemcpyDeviceToHost, stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+        return fdpd::check_launch("fd_chain_run_host (d2h)");
+    return FD_OK;
+}
+
+}  // extern "C"

@@ -146,6 +146,8 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     {
         const float2* Pb = P + (size_t)b * U * N_d;
         const float2* sn = s + n * U * N_d;
+        // (Measured: a 4-subcarrier x 4-user predicated batch of 32 loads was 3% slower on
+        // C2 than this loop — the extra address arithmetic outweighs the fewer round trips.)
         for (int j = tid; j < N_d; j += T) {
             const float2* pp = Pb + j;
             const float2* sp = sn + j;

@@ -20,6 +20,19 @@ FD_OK, FD_ERR_ARG, FD_ERR_NUMERIC, FD_ERR_CUDA = 0, 2, 3, 4
 _vp, _i, _ll, _f, _sz = C.c_void_p, C.c_int, C.c_longlong, C.c_float, C.c_size_t
 _ip = C.POINTER(C.c_int)
 
+FD_CHAIN_MAX_LAYERS = 8
+
+
+class ChainDesc(C.Structure):
+    """fd_chain_desc (include/fdpd.h)."""
+    _fields_ = [("U", C.c_int), ("B", C.c_int), ("T", C.c_int), ("N_d", C.c_int), ("N_ifft", C.c_int),
+                ("M_qam", C.c_int), ("n_layers", C.c_int), ("chans", C.c_int * (FD_CHAIN_MAX_LAYERS + 1)),
+                ("n_orders", C.c_int), ("orders", C.c_int * 8), ("L", C.c_int), ("M", C.c_int),
+                ("rho", C.c_float), ("boundary_eps", C.c_float)]
+
+
+_cp = C.POINTER(C.c_void_p)
+
 # name -> (restype, argtypes), mirroring include/fdpd.h
 SIGNATURES = {
     "fd_last_error": (C.c_char_p, []),
@@ -40,6 +53,11 @@ SIGNATURES = {
     "ue_receive": (_i, [_vp, _vp, _vp, _vp, _sz, _ll, _i, _i, _i, _i, _i, _vp]),
     "ue_slice_ser": (_i, [_vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
     "ue_receive_ser": (_i, [_vp, _vp, _vp, _vp, _sz, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _i, _f, _vp]),
+    "fd_chain_create": (_i, [_cp, C.POINTER(ChainDesc), _vp, _vp, _vp, _ll, _vp]),
+    "fd_chain_alpha": (_f, [_vp]),
+    "fd_chain_destroy": (None, [_vp]),
+    "fd_chain_run_device": (_i, [_vp, _vp, _vp, _ll, _vp, _vp, _vp]),
+    "fd_chain_run_host": (_i, [_vp, _vp, _vp, _ll, _vp, _vp]),
 }
 
 
@@ -261,3 +279,59 @@ def ue_receive_ser(y, h_fd, alpha, tx_idx, M_qam, yhat=None, counts=None, dec=No
                                 _ptr(tx_idx), M_qam, _ptr(dec), _ptr(counts), n_sym, B, U, N_d, N,
                                 float(boundary_eps), _stream(y)))
     return yhat, counts, dec
+
+
+# ----------------------------------------------------------------------------- native runtime
+class NativeChain:
+    """The C runtime plan (fd_chain_*): device-resident state of one channel realisation;
+    run_host() is the end-to-end entry point (host inputs in, SER counters out)."""
+
+    def __init__(self, cfg_shapes, h_taps, coef, params, max_batch, device=None):
+        import numpy as np
+        sh = cfg_shapes
+        d = ChainDesc()
+        d.U, d.B, d.T = sh.U, sh.B, int(np.asarray(h_taps).shape[0])
+        d.N_d, d.N_ifft, d.M_qam = sh.N_d, sh.N_ifft, sh.M_qam
+        d.n_layers = len(sh.chans) - 1
+        for i, c in enumerate(sh.chans):
+            d.chans[i] = c
+        d.n_orders = len(sh.orders)
+        for i, o in enumerate(sh.orders):
+            d.orders[i] = o
+        d.L, d.M, d.rho, d.boundary_eps = sh.L, sh.M, sh.rho, sh.eps
+        self.desc = d
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self._keep = [np.ascontiguousarray(h_taps, dtype=np.complex64), np.ascontiguousarray(coef, dtype=np.complex64),
+                      np.ascontiguousarray(params, dtype=np.float32)]
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+            _check(lib().fd_chain_create(C.byref(h), C.byref(d), self._keep[0].ctypes.data, self._keep[1].ctypes.data,
+                                         self._keep[2].ctypes.data, int(max_batch), st))
+        self.h = h
+        self.alpha = float(lib().fd_chain_alpha(h))
+
+    def run_device(self, s, tx_idx, counts, yhat=None):
+        _dev(s, torch.complex64, "s")
+        _dev(tx_idx, torch.uint16, "tx_idx")
+        _check(lib().fd_chain_run_device(self.h, _ptr(s), _ptr(tx_idx), s.shape[0], _ptr(counts), _ptr(yhat),
+                                         _stream(s)))
+        return counts
+
+    def run_host(self, s_host, idx_host, counts_host):
+        """s_host, idx_host, counts_host: (pinned) CPU tensors; returns counts_host."""
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().fd_chain_run_host(self.h, C.c_void_p(s_host.data_ptr()), C.c_void_p(idx_host.data_ptr()),
+                                       s_host.shape[0], C.c_void_p(counts_host.data_ptr()), st))
+        return counts_host
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().fd_chain_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

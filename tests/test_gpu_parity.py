@@ -295,6 +295,35 @@ def test_antenna_shards_accumulate_to_full(F, name, shards):
     assert rel(host(acc), host(full)) < 1e-6
 
 
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_native_runtime_matches(F, name):
+    """fd_chain_* (C runtime) == the per-call path; host entry == device entry; oracle counters."""
+    from paper_2205_05158_b200.chain import Chain, Shapes
+    cfg = configs.get(name)
+    nsym = cfg.n_sym if cfg.n_sym <= 4 else 64
+    inp = gen.make_inputs(cfg, range(nsym))
+    sh = Shapes.from_config(cfg)
+    nat = F.NativeChain(sh, inp["h_taps"], inp["coef"], inp["params"], max_batch=nsym)
+    ch = Chain(sh, inp["h_taps"], inp["coef"], inp["params"], max_batch=nsym)
+    assert nat.alpha == ch.alpha
+    s, idx = dev(inp["s"]), dev(inp["idx"], torch.uint16)
+    yh_ref, c_ref, _ = ch.step(s, idx)
+    yhat = torch.empty_like(yh_ref)
+    c_dev = torch.zeros(3, dtype=torch.int64, device="cuda")
+    nat.run_device(s, idx, c_dev, yhat=yhat)
+    torch.cuda.synchronize()
+    assert torch.equal(yhat, yh_ref) and torch.equal(c_dev, c_ref)
+    c_host = torch.zeros(3, dtype=torch.int64).pin_memory()
+    nat.run_host(torch.from_numpy(inp["s"]).pin_memory(), torch.from_numpy(inp["idx"]).pin_memory(), c_host)
+    assert torch.equal(c_host, c_ref.cpu())
+    if name == "C1":
+        o = O.run_config(cfg, inp)
+        assert c_host[1] == o["counts"][1] and abs(int(c_host[0]) - int(o["counts"][0])) <= int(o["counts"][2])
+    with pytest.raises(F.FdpdError):
+        nat.run_device(torch.cat([s, s]), torch.cat([idx, idx]), c_dev)     # beyond the plan's batch
+    nat.close()
+
+
 # ============================================================================ edge cases / errors
 def test_empty_batch_is_noop(F):
     cfg = configs.C1
