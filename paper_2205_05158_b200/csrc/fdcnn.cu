@@ -2,119 +2,145 @@
 // readings A1-A6): per (symbol, UE) an S x S two-channel image, 3x3 "same" convs
 // with tanh, residual output.
 //
-// Layer kernel: shared-memory-tiled direct convolution.  A CTA owns (image, tile of
-// TR rows, group of COG output channels); input channels are staged 8 at a time
-// with a one-pixel zero halo, weights are staged transposed W[ci][tap][co] so one
-// 128-bit broadcast load feeds 4 output channels x 4 pixels of FMAs.  The first
-// layer reads the complex symbols directly (Re/Im channels, row-major, tail zero
-// pad); the last layer writes the residual s_out = s_in + out on the first N_d
-// pixels.  tanhf is the accurate libdevice routine (no fast-math).
+// Two SIMT direct-convolution kernels (FP32, accurate tanhf, no fast-math):
+//  * k_cnn_fused — the whole network per image in shared memory (C1, C2);
+//  * k_conv      — one layer per launch through HBM activations (C3-C5).
+// Tensor cores are not used: the 2e-5 parity bar rules out TF32 (the residual is
+// not small against s at C4/C5), see DESIGN.md §6.
 #include "common.cuh"
 
 namespace fdpd {
 
 constexpr int CNN_THREADS = 256;
-constexpr int CI_T = 8;     // input channels staged per chunk
-constexpr int PX = 4;       // output pixels per thread (along a row)
 
+// Row stride (floats) of a zero-haloed activation tile, padded so that the input rows
+// read by one warp's items (item = PX pixels x CO_T channels, co-block fastest) hit
+// distinct banks; found by simulating the warp's first load (same address = broadcast).
+static int pick_rs(int S, int px, int n_cob) {
+    const int pxb = (S + px - 1) / px;
+    int best = S + 2, best_deg = 1 << 30;
+    for (int rs = S + 2; rs < S + 2 + 32; ++rs) {
+        int deg = 0;
+        for (int warp = 0; warp < 8; ++warp) {
+            int addr[32];
+            for (int lane = 0; lane < 32; ++lane) {
+                const int item = warp * 32 + lane, rest = item / n_cob;
+                addr[lane] = (rest / pxb) * rs + (rest % pxb) * px;
+            }
+            std::sort(addr, addr + 32);
+            const int nu = (int)(std::unique(addr, addr + 32) - addr);
+            int cnt[32] = {0};
+            for (int i = 0; i < nu; ++i) deg = std::max(deg, ++cnt[addr[i] & 31]);
+        }
+        if (deg < best_deg) { best_deg = deg; best = rs; }
+    }
+    return best;
+}
+
+static int pick_px(int S);
+
+// ============================================================================ per-layer kernel (C3-C5)
+// A CTA owns (image, band of TR rows, group of COG output channels); input channels
+// are staged CI_T at a time with a one-pixel zero halo and a bank-conflict-free row
+// stride, weights transposed W[ci][tap][co]; each thread computes PX pixels x CO_T
+// output channels with packed FP32 (FFMA2).  The first layer reads the complex
+// symbols directly (Re/Im, row-major, tail zero pad); the last layer writes the
+// residual s_out = s_in + out on the first N_d pixels (A2-A5).  Accurate tanhf.
 struct ConvGeom {
-    int Cin, Cout, S, N_d, TR, COG, n_rt, n_cg, pxb;
+    int Cin, Cout, S, N_d;
+    int px, co_t, cog, cogp, n_cob, pxb;   // item geometry
+    int TR, n_rt, n_cg, rs, ci_t;          // tiling
 };
 
-// in_mode: 0 = fp32 activations [img][Cin][S][S], 1 = complex symbols [img][N_d] (Cin = 2)
-// out_mode: 0 = tanh activations [img][Cout][S][S], 1 = residual complex s_out (Cout = 2)
-template <int CO_T, int IN_MODE, int OUT_MODE>
-__global__ void __launch_bounds__(CNN_THREADS)
+template <int PX, int CO_T, int IN_MODE, int OUT_MODE>
+__global__ void __launch_bounds__(CNN_THREADS, 2)
     k_conv(const float* __restrict__ in, const float2* __restrict__ s_in, const float* __restrict__ W,
            const float* __restrict__ bias, float* __restrict__ out, float2* __restrict__ s_out, ConvGeom g) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int S = g.S, SP = S + 2, TRP = g.TR + 2;
-    float* sin_ = reinterpret_cast<float*>(smem_raw);                 // [CI_T][TRP][SP]
-    float* sw = sin_ + CI_T * TRP * SP;                                // [CI_T][9][COG]
-    sw = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(sw) + 15) & ~uintptr_t(15));
-
+    extern __shared__ __align__(16) float csm[];
+    const int S = g.S, rs = g.rs, TRP = g.TR + 2;
+    const int tile = TRP * rs;
+    float* sin_ = csm;                                             // [ci_t][TRP][rs] (+ slack)
+    float* sw = csm + ((g.ci_t * tile + 16 + 3) & ~3);             // [ci_t][9][cogp]
     int blk = blockIdx.x;
     const int cg = blk % g.n_cg;
     blk /= g.n_cg;
     const int rt = blk % g.n_rt;
     const size_t img = blk / g.n_rt;
     const int r0 = rt * g.TR;
-    const int co0 = cg * g.COG;
-    const int cog = min(g.COG, g.Cout - co0);
+    const int co0 = cg * g.cog;
+    const int cog = min(g.cog, g.Cout - co0);
 
-    // work item of this thread
-    const int n_cob = (cog + CO_T - 1) / CO_T;
     const int item = threadIdx.x;
-    const int n_items = g.TR * g.pxb * n_cob;
+    const int n_items = g.TR * g.pxb * g.n_cob;
     const bool active = item < n_items;
-    const int cob = item % n_cob;
-    const int rest = item / n_cob;
+    const int cob = item % g.n_cob;
+    const int rest = item / g.n_cob;
     const int xb = rest % g.pxb;
-    const int ry = rest / g.pxb;              // row inside the tile
+    const int ry = rest / g.pxb;
     const int x0 = xb * PX;
-    const int c_lo = cob * CO_T;              // relative to co0
 
-    float acc[PX][CO_T];
+    float2 acc[PX][CO_T / 2];
 #pragma unroll
     for (int p = 0; p < PX; ++p)
 #pragma unroll
-        for (int c = 0; c < CO_T; ++c) acc[p][c] = 0.f;
+        for (int h = 0; h < CO_T / 2; ++h) acc[p][h] = make_float2(0.f, 0.f);
 
-    for (int ci0 = 0; ci0 < g.Cin; ci0 += CI_T) {
-        const int nci = min(CI_T, g.Cin - ci0);
-        // stage inputs with zero halo
-        for (int i = threadIdx.x; i < nci * TRP * SP; i += CNN_THREADS) {
-            const int c = i / (TRP * SP);
-            const int rem = i % (TRP * SP);
-            const int yy = rem / SP - 1 + r0;
-            const int xx = rem % SP - 1;
+    for (int ci0 = 0; ci0 < g.Cin; ci0 += g.ci_t) {
+        const int nci = min(g.ci_t, g.Cin - ci0);
+        for (int i = threadIdx.x; i < nci * TRP * (S + 2); i += CNN_THREADS) {
+            const int c = i / (TRP * (S + 2));
+            const int rem = i % (TRP * (S + 2));
+            const int rr = rem / (S + 2), xx = rem % (S + 2);
+            const int yy = rr - 1 + r0, xs = xx - 1;
             float v = 0.f;
-            if (yy >= 0 && yy < S && xx >= 0 && xx < S) {
+            if (yy >= 0 && yy < S && xs >= 0 && xs < S) {
                 if (IN_MODE == 1) {
-                    const int k = yy * S + xx;
+                    const int k = yy * S + xs;
                     if (k < g.N_d) {
                         const float2 z = s_in[img * g.N_d + k];
                         v = (ci0 + c) == 0 ? z.x : z.y;
                     }
                 } else {
-                    v = in[((img * g.Cin + ci0 + c) * S + yy) * S + xx];
+                    v = in[((img * g.Cin + ci0 + c) * S + yy) * S + xs];
                 }
             }
-            sin_[i] = v;
+            sin_[c * tile + rr * rs + xx] = v;
         }
-        // stage weights transposed: sw[c][tap][co - co0]
-        for (int i = threadIdx.x; i < nci * 9 * g.COG; i += CNN_THREADS) {
-            const int c = i / (9 * g.COG);
-            const int rem = i % (9 * g.COG);
-            const int tap = rem / g.COG;
-            const int co = rem % g.COG;
+        for (int i = threadIdx.x; i < nci * 9 * g.cogp; i += CNN_THREADS) {
+            const int co = i % g.cogp, r2 = i / g.cogp, tap = r2 % 9, c = r2 / 9;
             sw[i] = co < cog ? W[((size_t)(co0 + co) * g.Cin + ci0 + c) * 9 + tap] : 0.f;
         }
         __syncthreads();
         if (active) {
+            const float* wp = sw + cob * CO_T;
             for (int c = 0; c < nci; ++c) {
-                const float* ip = sin_ + (c * TRP + ry) * SP + x0;
+                const float* ip = sin_ + c * tile + ry * rs + x0;
                 float iv[3][PX + 2];
 #pragma unroll
                 for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-                    for (int dx = 0; dx < PX + 2; ++dx) iv[dy][dx] = (x0 + dx < SP) ? ip[dy * SP + dx] : 0.f;
-                const float* wp = sw + c * 9 * g.COG + c_lo;
+                    for (int dx = 0; dx < PX + 2; ++dx) iv[dy][dx] = ip[dy * rs + dx];
 #pragma unroll
                 for (int tap = 0; tap < 9; ++tap) {
-                    float wv[CO_T];
-                    if constexpr (CO_T == 4) {
-                        const float4 w4 = *reinterpret_cast<const float4*>(wp + tap * g.COG);
-                        wv[0] = w4.x; wv[1] = w4.y; wv[2] = w4.z; wv[3] = w4.w;
+                    float2 w[CO_T / 2];
+                    const float* wt = wp + (c * 9 + tap) * g.cogp;
+                    if constexpr (CO_T == 2) {
+                        w[0] = *reinterpret_cast<const float2*>(wt);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < CO_T; ++q) wv[q] = wp[tap * g.COG + q];
+                        for (int h = 0; h < CO_T / 4; ++h) {
+                            const float4 q = *reinterpret_cast<const float4*>(wt + 4 * h);
+                            w[2 * h] = make_float2(q.x, q.y);
+                            w[2 * h + 1] = make_float2(q.z, q.w);
+                        }
                     }
                     const int dy = tap / 3, dx = tap % 3;
 #pragma unroll
-                    for (int p = 0; p < PX; ++p)
+                    for (int p = 0; p < PX; ++p) {
+                        const float xv = iv[dy][p + dx];
 #pragma unroll
-                        for (int q = 0; q < CO_T; ++q) acc[p][q] = fmaf(wv[q], iv[dy][p + dx], acc[p][q]);
+                        for (int h = 0; h < CO_T / 2; ++h) acc[p][h] = ffma2(w[h], make_float2(xv, xv), acc[p][h]);
+                    }
                 }
             }
         }
@@ -129,22 +155,24 @@ __global__ void __launch_bounds__(CNN_THREADS)
         if (x >= S) continue;
         if constexpr (OUT_MODE == 0) {
 #pragma unroll
-            for (int q = 0; q < CO_T; ++q) {
-                const int co = co0 + c_lo + q;
-                if (c_lo + q < cog) out[((img * g.Cout + co) * S + y) * S + x] = tanhf(acc[p][q] + bias[co]);
+            for (int h = 0; h < CO_T / 2; ++h) {
+                const int c0 = cob * CO_T + 2 * h;
+                if (c0 < cog)
+                    out[((img * g.Cout + co0 + c0) * S + y) * S + x] = tanhf(acc[p][h].x + bias[co0 + c0]);
+                if (c0 + 1 < cog)
+                    out[((img * g.Cout + co0 + c0 + 1) * S + y) * S + x] = tanhf(acc[p][h].y + bias[co0 + c0 + 1]);
             }
-        } else if constexpr (CO_T >= 2) {
+        } else {
             const int k = y * S + x;
             if (k < g.N_d) {
                 const float2 z = s_in[img * g.N_d + k];
-                s_out[img * g.N_d + k] = make_float2(z.x + acc[p][0] + bias[0], z.y + acc[p][1] + bias[1]);
+                s_out[img * g.N_d + k] = make_float2(z.x + (acc[p][0].x + bias[0]), z.y + (acc[p][0].y + bias[1]));
             }
         }
     }
 }
 
-// output channels per thread; must match dispatch_conv
-static int conv_cot(int Cout) { return (Cout >= 4 && Cout % 4 == 0) ? 4 : (Cout % 2 == 0 ? 2 : 1); }
+static int conv_cot(int Cout) { return Cout % 8 == 0 ? 8 : (Cout % 4 == 0 ? 4 : 2); }
 
 static ConvGeom make_geom(int Cin, int Cout, int S, int N_d) {
     ConvGeom g;
@@ -152,41 +180,60 @@ static ConvGeom make_geom(int Cin, int Cout, int S, int N_d) {
     g.Cout = Cout;
     g.S = S;
     g.N_d = N_d;
-    g.pxb = (S + PX - 1) / PX;
-    const int co_t = conv_cot(Cout);
-    g.COG = Cout >= 16 ? 16 : Cout;
-    const int n_cob = g.COG / co_t;
-    int tr = CNN_THREADS / (g.pxb * n_cob);
-    if (tr < 1) tr = 1;
-    if (tr > S) tr = S;
+    g.px = pick_px(S);
+    g.pxb = (S + g.px - 1) / g.px;
+    g.co_t = conv_cot(Cout);
+    g.cog = Cout;
+    // shrink the output-channel group until at least one full row of items fits the CTA
+    while (g.cog > g.co_t && g.pxb * ((g.cog + g.co_t - 1) / g.co_t) * 2 > CNN_THREADS) g.cog = (g.cog + 1) / 2;
+    g.cog = ((g.cog + g.co_t - 1) / g.co_t) * g.co_t;
+    g.cogp = (g.cog + 3) & ~3;
+    g.n_cob = g.cog / g.co_t;
+    int tr = CNN_THREADS / (g.pxb * g.n_cob);
+    tr = std::max(1, std::min(tr, S));
     const int n_rt = (S + tr - 1) / tr;
-    g.TR = (S + n_rt - 1) / n_rt;   // balance the row tiles
+    g.TR = (S + n_rt - 1) / n_rt;   // balance the row bands
     g.n_rt = (S + g.TR - 1) / g.TR;
-    g.n_cg = (Cout + g.COG - 1) / g.COG;
+    g.n_cg = (Cout + g.cog - 1) / g.cog;
+    g.rs = pick_rs(S, g.px, g.n_cob);
+    // input channels per staging chunk: keep the tile + weights under ~56 KB (>= 2 CTAs/SM)
+    const int per_ci = (g.TR + 2) * g.rs + 9 * g.cogp;
+    g.ci_t = std::max(1, std::min(Cin, (56 * 1024 / 4 - 32) / per_ci));
     return g;
 }
 
 static size_t conv_smem(const ConvGeom& g) {
-    return sizeof(float) * ((size_t)CI_T * (g.TR + 2) * (g.S + 2) + 4 + (size_t)CI_T * 9 * g.COG);
+    return sizeof(float) * ((((size_t)g.ci_t * (g.TR + 2) * g.rs + 16 + 3) & ~(size_t)3) + (size_t)g.ci_t * 9 * g.cogp);
 }
 
-template <int CO_T, int IN_MODE, int OUT_MODE>
+template <int PX, int CO_T, int IN_MODE, int OUT_MODE>
 static int launch_conv(const ConvGeom& g, long long n_img, const float* in, const float2* s_in, const float* W,
                        const float* b, float* out, float2* s_out, cudaStream_t st) {
     const size_t smem = conv_smem(g);
-    cudaFuncSetAttribute(k_conv<CO_T, IN_MODE, OUT_MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_conv<PX, CO_T, IN_MODE, OUT_MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const long long blocks = n_img * g.n_rt * g.n_cg;
     if (blocks > 0x7fffffffLL) return fail_arg("fdcnn_forward: too many images per call");
-    k_conv<CO_T, IN_MODE, OUT_MODE><<<(unsigned)blocks, CNN_THREADS, smem, st>>>(in, s_in, W, b, out, s_out, g);
+    k_conv<PX, CO_T, IN_MODE, OUT_MODE><<<(unsigned)blocks, CNN_THREADS, smem, st>>>(in, s_in, W, b, out, s_out, g);
     return check_launch("fdcnn_forward");
+}
+
+template <int IN_MODE, int OUT_MODE, int CO_T>
+static int dispatch_px(const ConvGeom& g, long long n_img, const float* in, const float2* s_in, const float* W,
+                       const float* b, float* out, float2* s_out, cudaStream_t st) {
+    switch (g.px) {
+        case 6: return launch_conv<6, CO_T, IN_MODE, OUT_MODE>(g, n_img, in, s_in, W, b, out, s_out, st);
+        case 5: return launch_conv<5, CO_T, IN_MODE, OUT_MODE>(g, n_img, in, s_in, W, b, out, s_out, st);
+        default: return launch_conv<4, CO_T, IN_MODE, OUT_MODE>(g, n_img, in, s_in, W, b, out, s_out, st);
+    }
 }
 
 template <int IN_MODE, int OUT_MODE>
 static int dispatch_conv(const ConvGeom& g, long long n_img, const float* in, const float2* s_in, const float* W,
                          const float* b, float* out, float2* s_out, cudaStream_t st) {
-    if (g.Cout >= 4 && g.Cout % 4 == 0) return launch_conv<4, IN_MODE, OUT_MODE>(g, n_img, in, s_in, W, b, out, s_out, st);
-    if (g.Cout % 2 == 0) return launch_conv<2, IN_MODE, OUT_MODE>(g, n_img, in, s_in, W, b, out, s_out, st);
-    return launch_conv<1, IN_MODE, OUT_MODE>(g, n_img, in, s_in, W, b, out, s_out, st);
+    if (OUT_MODE == 1) return dispatch_px<IN_MODE, OUT_MODE, 2>(g, n_img, in, s_in, W, b, out, s_out, st);
+    if (g.co_t == 8) return dispatch_px<IN_MODE, OUT_MODE, 8>(g, n_img, in, s_in, W, b, out, s_out, st);
+    if (g.co_t == 4) return dispatch_px<IN_MODE, OUT_MODE, 4>(g, n_img, in, s_in, W, b, out, s_out, st);
+    return dispatch_px<IN_MODE, OUT_MODE, 2>(g, n_img, in, s_in, W, b, out, s_out, st);
 }
 
 static int fdcnn_validate(const int* chans, int n_layers, long long n_sym, int U, int N_d) {
@@ -359,27 +406,7 @@ static size_t fused_plan(const int* chans, int n_layers, int S, int N_d, FusedDe
     fd.N_d = N_d;
     // row stride: S + 2 padded so that the input rows one warp's items read hit distinct
     // banks (simulated for the widest layer's item mapping; same address = broadcast)
-    {
-        const int px = pick_px(S), pxb = (S + px - 1) / px;
-        const int n_cob = cmax % 8 == 0 ? cmax / 8 : (cmax + 3) / 4;
-        int best = S + 2, best_deg = 1 << 30;
-        for (int rs = S + 2; rs < S + 2 + 32; ++rs) {
-            int deg = 0;
-            for (int warp = 0; warp < 8; ++warp) {
-                int addr[32];
-                for (int lane = 0; lane < 32; ++lane) {
-                    const int item = warp * 32 + lane, rest = item / n_cob;
-                    addr[lane] = (rest / pxb) * rs + (rest % pxb) * px;
-                }
-                std::sort(addr, addr + 32);
-                const int nu = (int)(std::unique(addr, addr + 32) - addr);
-                int cnt[32] = {0};
-                for (int i = 0; i < nu; ++i) deg = std::max(deg, ++cnt[addr[i] & 31]);
-            }
-            if (deg < best_deg) { best_deg = deg; best = rs; }
-        }
-        fd.rs = best;
-    }
+    fd.rs = pick_rs(S, pick_px(S), cmax % 8 == 0 ? cmax / 8 : (cmax + 3) / 4);
     fd.cs = fd.rs * (S + 2);
     fd.buflen = round4(cmax * fd.cs + 16);   // slack for the over-read of the last px block
     int w = 0, p = 0;
@@ -484,8 +511,7 @@ int fdcnn_forward(const float* params, const int* chans, int n_layers, const voi
         const float* b = W + (size_t)co * ci * 9;
         off += (size_t)co * ci * 9 + co;
         const ConvGeom g = make_geom(ci, co, S, N_d);
-        FD_REQUIRE(conv_smem(g) <= 200 * 1024 && g.pxb * (g.COG / conv_cot(co)) <= CNN_THREADS,
-                   "fdcnn_forward: image too large");
+        FD_REQUIRE(conv_smem(g) <= 200 * 1024 && g.pxb * g.n_cob <= CNN_THREADS, "fdcnn_forward: image too large");
         const bool first = l == 0, last = l == n_layers - 1;
         const float* in = first ? nullptr : buf[(l - 1) & 1];
         float* out = last ? nullptr : buf[l & 1];

@@ -125,7 +125,7 @@ __host__ __device__ constexpr int fft_threads() { return LOG2N <= 12 ? (1 << LOG
 // resident CTAs per SM requested from ptxas (register cap 65536 / (T * this) = 128).
 // (Measured: N/32 threads with 4 CTAs/SM at N = 4096 was 11% slower — register spills.)
 template <int LOG2N>
-__host__ __device__ constexpr int fft_min_blocks() { return fft_threads<LOG2N>() <= 256 ? 2 : 1; }
+__host__ __device__ constexpr int fft_min_blocks() { return fft_threads<LOG2N>() <= 256 ? 3 : 1; }
 
 // Register layout of a pass with radix R: element (q, r), q < VPT/R, r < R, is
 // position j + r * (N/R) with j = tid + q * T.

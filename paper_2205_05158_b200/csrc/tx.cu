@@ -111,7 +111,7 @@ __host__ __device__ inline ChainSmem chain_smem(int N, int N_d, const GmpDesc& d
 }
 // keep a shared-memory copy of y for the receive DFT when it still allows 2 CTAs/SM
 template <int LOG2N>
-__host__ __device__ constexpr bool chain_ysm() { return LOG2N <= 12; }
+__host__ __device__ constexpr bool chain_ysm() { return LOG2N <= 11; }
 
 // One CTA per (symbol n, antenna b): precode at the data bins straight into the
 // pass-0 registers, IDFT in shared memory, 1/sqrt(N) scale + envelope, GMP, stream y.
@@ -321,7 +321,7 @@ static int launch_chain(int variant, const float2* P, const float2* s, const flo
                         long long n_sym, int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
     switch (variant) {
         case 1: return launch_chain_one<LOG2N, 3, 2, 1, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
-        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
+        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
         case 3: return launch_chain_one<LOG2N, 5, 6, 3, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
         default: return launch_chain_one<LOG2N, 0, 0, 0, 1, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
     }
