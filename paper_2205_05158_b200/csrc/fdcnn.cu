@@ -54,7 +54,7 @@ struct ConvGeom {
 
 template <int PX, int CO_T, int IN_MODE, int OUT_MODE>
 __global__ void __launch_bounds__(CNN_THREADS, 2)
-    k_conv(const float* __restrict__ in, const float2* __restrict__ s_in, const float* __restrict__ W,
+    k_conv(const float* __restrict__ in, const float2* __restrict__ s_in, const float* __restrict__ Wt,
            const float* __restrict__ bias, float* __restrict__ out, float2* __restrict__ s_out, ConvGeom g) {
     extern __shared__ __align__(16) float csm[];
     const int S = g.S, rs = g.rs, TRP = g.TR + 2;
@@ -87,28 +87,36 @@ __global__ void __launch_bounds__(CNN_THREADS, 2)
 
     for (int ci0 = 0; ci0 < g.Cin; ci0 += g.ci_t) {
         const int nci = min(g.ci_t, g.Cin - ci0);
-        for (int i = threadIdx.x; i < nci * TRP * (S + 2); i += CNN_THREADS) {
-            const int c = i / (TRP * (S + 2));
-            const int rem = i % (TRP * (S + 2));
-            const int rr = rem / (S + 2), xx = rem % (S + 2);
-            const int yy = rr - 1 + r0, xs = xx - 1;
-            float v = 0.f;
-            if (yy >= 0 && yy < S && xs >= 0 && xs < S) {
-                if (IN_MODE == 1) {
-                    const int k = yy * S + xs;
-                    if (k < g.N_d) {
-                        const float2 z = s_in[img * g.N_d + k];
-                        v = (ci0 + c) == 0 ? z.x : z.y;
+        {   // input rows: warp w stages rows w, w + 8, ... of the (channel, row) tile; lanes over columns
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (int row = warp; row < nci * TRP; row += CNN_THREADS / 32) {
+                const int c = row / TRP, rr = row - c * TRP;
+                const int yy = rr - 1 + r0;
+                const bool yok = yy >= 0 && yy < S;
+                float* dst = sin_ + c * tile + rr * rs;
+                const float* src = IN_MODE == 1 ? nullptr : in + ((img * g.Cin + ci0 + c) * S + (yok ? yy : 0)) * S;
+                for (int xx = lane; xx < S + 2; xx += 32) {
+                    const int xs = xx - 1;
+                    float v = 0.f;
+                    if (yok && xs >= 0 && xs < S) {
+                        if constexpr (IN_MODE == 1) {
+                            const int k = yy * S + xs;
+                            if (k < g.N_d) {
+                                const float2 z = s_in[img * g.N_d + k];
+                                v = (ci0 + c) == 0 ? z.x : z.y;
+                            }
+                        } else {
+                            v = src[xs];
+                        }
                     }
-                } else {
-                    v = in[((img * g.Cin + ci0 + c) * S + yy) * S + xs];
+                    dst[xx] = v;
                 }
             }
-            sin_[c * tile + rr * rs + xx] = v;
         }
-        for (int i = threadIdx.x; i < nci * 9 * g.cogp; i += CNN_THREADS) {
-            const int co = i % g.cogp, r2 = i / g.cogp, tap = r2 % 9, c = r2 / 9;
-            sw[i] = co < cog ? W[((size_t)(co0 + co) * g.Cin + ci0 + c) * 9 + tap] : 0.f;
+        {   // weights: contiguous chunk of the pre-transposed Wt[cg][ci][tap][cogp]
+            const float4* src = reinterpret_cast<const float4*>(Wt + ((size_t)cg * g.Cin + ci0) * 9 * g.cogp);
+            float4* dst = reinterpret_cast<float4*>(sw);
+            for (int i = threadIdx.x; i < nci * 9 * g.cogp / 4; i += CNN_THREADS) dst[i] = __ldg(src + i);
         }
         __syncthreads();
         if (active) {
@@ -169,6 +177,21 @@ __global__ void __launch_bounds__(CNN_THREADS, 2)
                 s_out[img * g.N_d + k] = make_float2(z.x + (acc[p][0].x + bias[0]), z.y + (acc[p][0].y + bias[1]));
             }
         }
+    }
+}
+
+// Wt[cg][ci][tap][cogp] (cogp >= cog, zero padded) from W[co][ci][3][3]: each CTA of
+// k_conv then stages its weight chunk with contiguous 128-bit loads.
+__global__ void k_transpose_w(const float* __restrict__ W, float* __restrict__ Wt, ConvGeom g, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int cc = (int)(i % g.cogp);
+        long long r = i / g.cogp;
+        const int tap = (int)(r % 9);
+        r /= 9;
+        const int ci = (int)(r % g.Cin);
+        const int cg = (int)(r / g.Cin);
+        const int co = cg * g.cog + cc;
+        Wt[i] = (cc < g.cog && co < g.Cout) ? W[((size_t)co * g.Cin + ci) * 9 + tap] : 0.f;
     }
 }
 
@@ -456,19 +479,23 @@ using namespace fdpd;
 extern "C" {
 
 size_t fdcnn_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d) {
-    if (!chans || n_layers < 2 || n_sym <= 0 || U <= 0 || N_d <= 0) return 0;
+    if (!chans || n_layers < 1 || n_sym <= 0 || U <= 0 || N_d <= 0) return 0;
+    int S = 1;
+    while (S * S < N_d) ++S;
     {
-        int S = 1;
-        while (S * S < N_d) ++S;
         FusedDesc fd;
         if (fused_plan(chans, n_layers, S, N_d, fd)) return 0;   // fused path needs no workspace
     }
     int cmax = 0;
     for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
-    int S = 1;
-    while (S * S < N_d) ++S;
     const size_t one = sizeof(float) * (size_t)n_sym * U * cmax * S * S;
-    return n_layers > 2 ? 2 * one : one;
+    size_t bytes = n_layers > 2 ? 2 * one : (n_layers == 2 ? one : 0);
+    bytes = (bytes + 255) & ~(size_t)255;
+    for (int l = 0; l < n_layers; ++l) {   // pre-transposed weights Wt[cg][ci][tap][cogp]
+        const ConvGeom g = make_geom(chans[l], chans[l + 1], S, N_d);
+        bytes += (sizeof(float) * (size_t)g.n_cg * g.Cin * 9 * g.cogp + 255) & ~(size_t)255;
+    }
+    return bytes;
 }
 
 int fdcnn_forward(const float* params, const int* chans, int n_layers, const void* s_in, void* s_out, void* workspace,
@@ -498,12 +525,12 @@ int fdcnn_forward(const float* params, const int* chans, int n_layers, const voi
             }
         }
     }
-    float* buf[2] = {(float*)workspace, nullptr};
-    if (n_layers > 2) {
-        int cmax = 0;
-        for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
-        buf[1] = buf[0] + (size_t)n_img * cmax * S * S;
-    }
+    int cmax = 0;
+    for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
+    const size_t one = (size_t)n_img * cmax * S * S;
+    float* buf[2] = {(float*)workspace, (float*)workspace + one};
+    size_t act_bytes = sizeof(float) * (n_layers > 2 ? 2 * one : (n_layers == 2 ? one : 0));
+    char* wt_ptr = (char*)workspace + ((act_bytes + 255) & ~(size_t)255);
     size_t off = 0;
     for (int l = 0; l < n_layers; ++l) {
         const int ci = chans[l], co = chans[l + 1];
@@ -512,13 +539,18 @@ int fdcnn_forward(const float* params, const int* chans, int n_layers, const voi
         off += (size_t)co * ci * 9 + co;
         const ConvGeom g = make_geom(ci, co, S, N_d);
         FD_REQUIRE(conv_smem(g) <= 200 * 1024 && g.pxb * g.n_cob <= CNN_THREADS, "fdcnn_forward: image too large");
+        float* Wt = reinterpret_cast<float*>(wt_ptr);
+        const long long nwt = (long long)g.n_cg * g.Cin * 9 * g.cogp;
+        wt_ptr += (sizeof(float) * (size_t)nwt + 255) & ~(size_t)255;
+        k_transpose_w<<<(unsigned)std::min<long long>((nwt + 255) / 256, 1024), 256, 0, stream>>>(W, Wt, g, nwt);
+        if ((rc = check_launch("fdcnn_forward (weights)"))) return rc;
         const bool first = l == 0, last = l == n_layers - 1;
         const float* in = first ? nullptr : buf[(l - 1) & 1];
         float* out = last ? nullptr : buf[l & 1];
-        if (first && last) rc = dispatch_conv<1, 1>(g, n_img, in, sin2, W, b, out, sout2, stream);
-        else if (first) rc = dispatch_conv<1, 0>(g, n_img, in, sin2, W, b, out, sout2, stream);
-        else if (last) rc = dispatch_conv<0, 1>(g, n_img, in, sin2, W, b, out, sout2, stream);
-        else rc = dispatch_conv<0, 0>(g, n_img, in, sin2, W, b, out, sout2, stream);
+        if (first && last) rc = dispatch_conv<1, 1>(g, n_img, in, sin2, Wt, b, out, sout2, stream);
+        else if (first) rc = dispatch_conv<1, 0>(g, n_img, in, sin2, Wt, b, out, sout2, stream);
+        else if (last) rc = dispatch_conv<0, 1>(g, n_img, in, sin2, Wt, b, out, sout2, stream);
+        else rc = dispatch_conv<0, 0>(g, n_img, in, sin2, Wt, b, out, sout2, stream);
         if (rc) return rc;
     }
     return FD_OK;
