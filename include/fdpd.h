@@ -69,6 +69,18 @@ int fdcnn_forward(const float* params, const int* chans, int n_layers,
                   const void* s_in, void* s_out, void* workspace, size_t workspace_bytes,
                   long long n_sym, int U, int N_d, cudaStream_t stream);
 
+/* a1 (paper head) — the paper's own FD-CNN, P:170-177, P:206:
+ * per (symbol, UE) the S x S Re/Im image (as above, L_U = 1), n_conv 3x3 "same" kernels
+ * with bias, ReLU, flatten in (kernel, row, column) order, fully connected linear layer
+ * to 2 N_d outputs with bias: s_out[j] = out[j] + i out[N_d + j].
+ *  params  device float: W1[n_conv][2][3][3], b1[n_conv], W2[2 N_d][n_conv S^2], b2[2 N_d]
+ *          (any float offset; W2 is copied to an aligned workspace slot each call).
+ *  n_conv * S^2 must be a multiple of 4.  workspace >= fdcnn_paper_workspace_bytes(...). */
+size_t fdcnn_paper_workspace_bytes(int n_conv, long long n_sym, int U, int N_d);
+int fdcnn_paper_forward(const float* params, int n_conv, const void* s_in, void* s_out,
+                        void* workspace, size_t workspace_bytes, long long n_sym, int U, int N_d,
+                        cudaStream_t stream);
+
 /* -------------------------------------------------------------------------
  * a2. Zero-forcing precoder build — Eq. (6), FD channel P:72 (A9),
  * power normalisation P:84 (reading A12).  Once per channel realisation.
@@ -192,6 +204,8 @@ typedef struct fd_chain_desc {
     int n_orders, orders[8], L, M;                   /* GMP PA (gmp_pa) */
     float rho;                                       /* TD RMS target for alpha (A12) */
     float boundary_eps;                              /* SER near-boundary band (1e-4) */
+    int head;                                        /* 0: residual stack (fdcnn_forward), 1: paper head */
+    int n_conv;                                      /* paper head: N^Conv (fdcnn_paper_forward) */
 } fd_chain_desc;
 typedef struct fd_chain fd_chain;
 

@@ -94,6 +94,49 @@ def fdcnn_forward(s: np.ndarray, params: np.ndarray, chans, N_d: int) -> np.ndar
     return s + r.reshape(n, U, N_d)
 
 
+def fdcnn_paper_forward(s: np.ndarray, params: np.ndarray, N_d: int, n_conv: int = 2) -> np.ndarray:
+    """The paper's own FD-CNN (NEXT f2): per (symbol n, UE u), L_U = 1:
+      * S x S matrix of the N_d symbols, S = ceil(sqrt(N_d)), contiguous row-major order, zero
+        padding (P:170 and footnote); Re and Im matrices as 2 channels (P:175);
+      * N^Conv 3x3 kernels, stride K_S = 1, zero padding keeping S x S (P:206), with bias;
+      * element-wise ReLU (P:206), flatten to n_conv S^2 in (kernel, row, column) order (P:177);
+      * fully connected linear output layer with 2 N_d neurons, with bias; neurons
+        0..N_d-1 are the real parts and N_d..2N_d-1 the imaginary parts of s_tilde (reading P1).
+    params: W1[n_conv][2][3][3], b1[n_conv], W2[2 N_d][n_conv S^2], b2[2 N_d]."""
+    s = np.asarray(s, dtype=np.complex128)
+    n, U, nd = s.shape
+    assert nd == N_d
+    S = int(np.ceil(np.sqrt(N_d)))
+    p = np.asarray(params, dtype=np.float64)
+    K = n_conv * S * S
+    o = 0
+    W1 = p[o:o + n_conv * 18].reshape(n_conv, 2, 3, 3); o += n_conv * 18
+    b1 = p[o:o + n_conv]; o += n_conv
+    W2 = p[o:o + 2 * N_d * K].reshape(2 * N_d, K); o += 2 * N_d * K
+    b2 = p[o:o + 2 * N_d]; o += 2 * N_d
+    assert o == p.size
+    flat = np.zeros((n * U, S * S), dtype=np.complex128)
+    flat[:, :N_d] = s.reshape(n * U, N_d)
+    img = flat.reshape(n * U, S, S)
+    h = np.stack([img.real, img.imag], axis=1)                      # [img][2][S][S]
+    hp = np.zeros((h.shape[0], 2, S + 2, S + 2))
+    hp[:, :, 1:S + 1, 1:S + 1] = h
+    conv = np.broadcast_to(b1[None, :, None, None], (h.shape[0], n_conv, S, S)).copy()
+    for dy in range(3):
+        for dx in range(3):
+            conv += np.einsum("oc,ncyx->noyx", W1[:, :, dy, dx], hp[:, :, dy:dy + S, dx:dx + S])
+    feat = np.maximum(conv, 0.0).reshape(h.shape[0], K)            # ReLU, flatten
+    out = feat @ W2.T + b2                                          # FC
+    return (out[:, :N_d] + 1j * out[:, N_d:]).reshape(n, U, N_d)
+
+
+def dpd_forward(cfg_head: str, s, params, chans, N_d, n_conv=2):
+    """Dispatch on the FD-CNN variant: BASELINE residual stack (A1) or the paper head."""
+    if cfg_head == "paper":
+        return fdcnn_paper_forward(s, params, N_d, n_conv)
+    return fdcnn_forward(s, params, chans, N_d)
+
+
 # ============================================================================ channel / ZF
 def channel_fd(h_taps: np.ndarray, N_ifft: int, N_d: int) -> np.ndarray:
     """H_hat_k = sum_t H_t exp(-j k 2 pi t / N) at the data bins (A9: unnormalised).
@@ -229,12 +272,13 @@ def slice_ser(yhat: np.ndarray, alpha: float, idx: np.ndarray, M_qam: int, eps: 
 
 
 # ============================================================================ composition
-def run_chain(s, idx, h_taps, coef, params, *, chans, orders, L, M, N_ifft, M_qam, rho=0.3):
+def run_chain(s, idx, h_taps, coef, params, *, chans, orders, L, M, N_ifft, M_qam, rho=0.3, head="residual",
+              n_conv=2):
     """The whole hot path, stage by stage.  Returns every stage output."""
     s = np.asarray(s, dtype=np.complex128)
     N_d = s.shape[-1]
     out = {}
-    out["s_tilde"] = fdcnn_forward(s, params, chans, N_d)
+    out["s_tilde"] = dpd_forward(head, s, params, chans, N_d, n_conv)
     out["Hfd"] = channel_fd(h_taps, N_ifft, N_d)
     out["P"], out["alpha"], _ = zf_precoder(out["Hfd"], N_ifft, rho)
     out["X"] = precode(out["P"], out["s_tilde"])
@@ -249,4 +293,4 @@ def run_config(cfg, inp):
     """run_chain with a workload.configs.ChainConfig and a workload.gen.make_inputs bundle."""
     return run_chain(inp["s"], inp["idx"], inp["h_taps"], inp["coef"], inp["params"],
                      chans=cfg.chans, orders=cfg.orders, L=cfg.L, M=cfg.M,
-                     N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, rho=cfg.rho)
+                     N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, rho=cfg.rho, head=cfg.head, n_conv=cfg.n_conv)

@@ -31,11 +31,13 @@ class Shapes:
     M: int
     rho: float = 0.3
     eps: float = 1e-4
+    head: str = "residual"      # FD-CNN variant: BASELINE residual stack or the paper's conv + FC head
+    n_conv: int = 2
 
     @classmethod
     def from_config(cls, cfg):
         return cls(U=cfg.U, B=cfg.B, N_d=cfg.N_d, N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, chans=tuple(cfg.chans),
-                   orders=tuple(cfg.orders), L=cfg.L, M=cfg.M, rho=cfg.rho)
+                   orders=tuple(cfg.orders), L=cfg.L, M=cfg.M, rho=cfg.rho, head=cfg.head, n_conv=cfg.n_conv)
 
 
 class Chain:
@@ -60,13 +62,19 @@ class Chain:
         self.y = torch.empty((n, self.B_loc, sh.N_ifft), dtype=torch.complex64, device=dev)
         self.yhat = torch.empty((n, sh.U, sh.N_d), dtype=torch.complex64, device=dev)
         self.counts = torch.zeros(3, dtype=torch.int64, device=dev)
-        ch = fdpd._ints(sh.chans)
-        self.ws_cnn = fdpd._ws(fdpd.lib().fdcnn_workspace_bytes(ch, len(sh.chans) - 1, n, sh.U, sh.N_d), self.y)
+        if sh.head == "paper":
+            need = fdpd.lib().fdcnn_paper_workspace_bytes(sh.n_conv, n, sh.U, sh.N_d)
+        else:
+            need = fdpd.lib().fdcnn_workspace_bytes(fdpd._ints(sh.chans), len(sh.chans) - 1, n, sh.U, sh.N_d)
+        self.ws_cnn = fdpd._ws(need, self.y)
         self.ws_rx = fdpd._ws(fdpd.lib().ue_receive_workspace_bytes(n, self.B_loc, sh.N_d), self.y)
 
     # ------------------------------------------------------------------ stages
     def dpd(self, s):
         n = s.shape[0]
+        if self.sh.head == "paper":
+            return fdpd.fdcnn_paper_forward(self.params, self.sh.n_conv, s, out=self.s_tilde[:n],
+                                            workspace=self.ws_cnn)
         return fdpd.fdcnn_forward(self.params, self.sh.chans, s, out=self.s_tilde[:n], workspace=self.ws_cnn)
 
     def tx(self, s_tilde):

@@ -63,7 +63,8 @@ int ensure_batch(fd_chain* c, long long n) {
     if ((rc = dalloc(&c->XPA, (size_t)n * d.B * d.N_d))) return rc;
     if ((rc = dalloc(&c->yhat, (size_t)n * d.U * d.N_d))) return rc;
     if ((rc = dalloc(&c->idx, (size_t)n * d.U * d.N_d))) return rc;
-    c->ws_cnn_bytes = fdcnn_workspace_bytes(d.chans, d.n_layers, n, d.U, d.N_d);
+    c->ws_cnn_bytes = d.head == 1 ? fdcnn_paper_workspace_bytes(d.n_conv, n, d.U, d.N_d)
+                                  : fdcnn_workspace_bytes(d.chans, d.n_layers, n, d.U, d.N_d);
     if (c->ws_cnn_bytes && (rc = dalloc(reinterpret_cast<char**>(&c->ws_cnn), c->ws_cnn_bytes))) return rc;
     c->cap = n;
     return FD_OK;
@@ -86,7 +87,14 @@ int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_tap
     if (!c) return fdpd::fail_arg("fd_chain_create: out of host memory");
     c->d = d;
     c->n_coef = d.n_orders * (d.L + 1) + 2 * (d.n_orders - 1) * (d.L + 1) * d.M;
-    for (int l = 0; l < d.n_layers; ++l) c->n_params += d.chans[l + 1] * d.chans[l] * 9 + d.chans[l + 1];
+    if (d.head == 1) {
+        FD_REQUIRE(d.n_conv >= 1, "fd_chain_create: n_conv");
+        int S = 1;
+        while (S * S < d.N_d) ++S;
+        c->n_params = d.n_conv * 19 + 2 * d.N_d * d.n_conv * S * S + 2 * d.N_d;
+    } else {
+        for (int l = 0; l < d.n_layers; ++l) c->n_params += d.chans[l + 1] * d.chans[l] * 9 + d.chans[l + 1];
+    }
     int rc;
     const cudaMemcpyKind h2d = cudaMemcpyHostToDevice;
 #define FD_TRY(x)              \
@@ -127,8 +135,10 @@ int fd_chain_run_device(fd_chain* c, const void* s, const uint16_t* tx_idx, long
                c->cap);
     if (n_sym == 0) return FD_OK;
     const fd_chain_desc& d = c->d;
-    int rc = fdcnn_forward(c->params, d.chans, d.n_layers, s, c->s_tilde, c->ws_cnn, c->ws_cnn_bytes, n_sym, d.U,
-                           d.N_d, stream);
+    int rc = d.head == 1 ? fdcnn_paper_forward(c->params, d.n_conv, s, c->s_tilde, c->ws_cnn, c->ws_cnn_bytes, n_sym,
+                                               d.U, d.N_d, stream)
+                         : fdcnn_forward(c->params, d.chans, d.n_layers, s, c->s_tilde, c->ws_cnn, c->ws_cnn_bytes,
+                                         n_sym, d.U, d.N_d, stream);
     if (rc) return rc;
     rc = chain_txrx(c->P, c->s_tilde, c->coef, c->y, c->XPA, d.orders, d.n_orders, d.L, d.M, n_sym, d.B, d.U, d.N_d,
                     d.N_ifft, stream);

@@ -261,6 +261,7 @@ static int validate_gmp(const int* orders, int n_orders, int L, int M, int N, Gm
         if (n_orders == 3 && L == 2 && M == 1) variant = 1;
         else if (n_orders == 4 && L == 4 && M == 2) variant = 2;
         else if (n_orders == 5 && L == 6 && M == 3) variant = 3;
+        else if (n_orders == 4 && L == 3 && M == 1) variant = 4;   // the paper's PA/DPD shape
     }
     return FD_OK;
 }
@@ -323,6 +324,7 @@ static int launch_chain(int variant, const float2* P, const float2* s, const flo
         case 1: return launch_chain_one<LOG2N, 3, 2, 1, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
         case 2: return launch_chain_one<LOG2N, 4, 4, 2, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
         case 3: return launch_chain_one<LOG2N, 5, 6, 3, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
+        case 4: return launch_chain_one<LOG2N, 4, 3, 1, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
         default: return launch_chain_one<LOG2N, 0, 0, 0, 1, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
     }
 }
@@ -390,6 +392,7 @@ int gmp_pa(const void* x, const void* coef, void* y, const int* orders, int n_or
         case 1: return launch_gmp<3, 2, 1, 4>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
         case 2: return launch_gmp<4, 4, 2, 4>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
         case 3: return launch_gmp<5, 6, 3, 2>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
+        case 4: return launch_gmp<4, 3, 1, 4>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
         default: return launch_gmp<0, 0, 0, 1>(xp, cp, yp, n_sym, B, N_ifft, d, stream);
     }
 }

@@ -28,7 +28,7 @@ class ChainDesc(C.Structure):
     _fields_ = [("U", C.c_int), ("B", C.c_int), ("T", C.c_int), ("N_d", C.c_int), ("N_ifft", C.c_int),
                 ("M_qam", C.c_int), ("n_layers", C.c_int), ("chans", C.c_int * (FD_CHAIN_MAX_LAYERS + 1)),
                 ("n_orders", C.c_int), ("orders", C.c_int * 8), ("L", C.c_int), ("M", C.c_int),
-                ("rho", C.c_float), ("boundary_eps", C.c_float)]
+                ("rho", C.c_float), ("boundary_eps", C.c_float), ("head", C.c_int), ("n_conv", C.c_int)]
 
 
 _cp = C.POINTER(C.c_void_p)
@@ -40,6 +40,8 @@ SIGNATURES = {
     "fd_shutdown": (None, []),
     "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
     "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
+    "fdcnn_paper_workspace_bytes": (_sz, [_i, _ll, _i, _i]),
+    "fdcnn_paper_forward": (_i, [_vp, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
     "zf_workspace_bytes": (_sz, [_i]),
     "zf_precoder_build": (_i, [_vp, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, C.POINTER(C.c_float), _vp, _sz, _vp]),
     "precode": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _vp]),
@@ -132,6 +134,20 @@ def fdcnn_forward(params, chans, s_in, out=None, workspace=None):
         workspace = _ws(need, s_in)
     _check(lib().fdcnn_forward(_ptr(params), ch, nl, _ptr(s_in), _ptr(out), _ptr(workspace), workspace.numel(),
                                n_sym, U, N_d, _stream(s_in)))
+    return out
+
+
+def fdcnn_paper_forward(params, n_conv, s_in, out=None, workspace=None):
+    """Paper FD-CNN head (include/fdpd.h fdcnn_paper_forward).  s_in complex64 [n_sym][U][N_d]."""
+    _dev(params, torch.float32, "params")
+    _dev(s_in, torch.complex64, "s_in")
+    n_sym, U, N_d = s_in.shape
+    out = torch.empty_like(s_in) if out is None else _dev(out, torch.complex64, "out")
+    need = lib().fdcnn_paper_workspace_bytes(n_conv, n_sym, U, N_d)
+    if workspace is None or workspace.numel() < need:
+        workspace = _ws(need, s_in)
+    _check(lib().fdcnn_paper_forward(_ptr(params), n_conv, _ptr(s_in), _ptr(out), _ptr(workspace),
+                                     workspace.numel(), n_sym, U, N_d, _stream(s_in)))
     return out
 
 
@@ -299,6 +315,7 @@ class NativeChain:
         for i, o in enumerate(sh.orders):
             d.orders[i] = o
         d.L, d.M, d.rho, d.boundary_eps = sh.L, sh.M, sh.rho, sh.eps
+        d.head, d.n_conv = (1 if getattr(sh, "head", "residual") == "paper" else 0), getattr(sh, "n_conv", 2)
         self.desc = d
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self._keep = [np.ascontiguousarray(h_taps, dtype=np.complex64), np.ascontiguousarray(coef, dtype=np.complex64),

@@ -64,7 +64,7 @@ def test_ofdm_vs_brute_force_small(F):
 
 
 # ============================================================================ a5 / GMP
-GMP_CASES = [((1, 3, 5), 2, 1), ((1, 3, 5, 7), 4, 2), ((1, 3, 5, 7, 9), 6, 3),   # specialised
+GMP_CASES = [((1, 3, 5), 2, 1), ((1, 3, 5, 7), 4, 2), ((1, 3, 5, 7, 9), 6, 3), ((1, 3, 5, 7), 3, 1),  # specialised
              ((1, 5, 9), 3, 0), ((1, 3), 1, 1), ((1,), 0, 0), ((1, 3, 5, 7, 9, 11), 2, 2)]  # generic
 
 
@@ -100,6 +100,23 @@ def test_fdcnn_forward(F, name, nsym):
     want = O.fdcnn_forward(inp["s"], inp["params"], cfg.chans, cfg.N_d)
     assert rel(got, want) < TOL
     assert rel(got - inp["s"], want - inp["s"]) < 1e-4       # the residual itself
+
+
+@pytest.mark.parametrize("nsym", [1, 3, 40])
+def test_fdcnn_paper_forward(F, nsym):
+    """Paper FD-CNN head (NEXT f2): conv + ReLU + FC GEMM vs the oracle; ragged M, N tails."""
+    cfg = configs.PAPER
+    inp = gen.make_inputs(cfg, range(nsym))
+    got = host(F.fdcnn_paper_forward(dev(inp["params"], torch.float32), cfg.n_conv, dev(inp["s"])))
+    want = O.fdcnn_paper_forward(inp["s"], inp["params"], cfg.N_d, cfg.n_conv)
+    assert rel(got, want) < TOL
+
+
+def test_fdcnn_paper_identity_head(F):
+    cfg = configs.PAPER
+    inp = gen.make_inputs(cfg, range(5), zero_cnn=True)
+    got = host(F.fdcnn_paper_forward(dev(inp["params"], torch.float32), cfg.n_conv, dev(inp["s"])))
+    assert rel(got, inp["s"]) < 2e-6
 
 
 def test_fdcnn_zero_weights_identity(F):
@@ -244,7 +261,7 @@ def _gpu_chain(F, cfg, inp, fused=True):
     return ch, host(ch.s_tilde[:s.shape[0]]), host(ch.y[:s.shape[0]]), host(yhat), host(counts), host(dec)
 
 
-@pytest.mark.parametrize("name,fused", [("C1", True), ("C1", False), ("C2", True), ("C2", False)])
+@pytest.mark.parametrize("name,fused", [("C1", True), ("C1", False), ("C2", True), ("C2", False), ("P", True)])
 def test_end_to_end(F, name, fused):
     """C1: all 4 symbols.  C2: the full 1024-symbol batch in one call (the bench's
     launch configuration); symbols 0, 517, 1023 compared with the oracle."""
@@ -265,7 +282,7 @@ def test_end_to_end(F, name, fused):
         assert abs(int(counts[0]) - int(o["counts"][0])) <= int(near.sum())
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
+@pytest.mark.parametrize("name", ["C1", "C2", "P"])
 def test_invariant_zero_cnn_linear_pa(F, name):
     cfg = configs.get(name)
     inp = gen.make_inputs(cfg, range(8 if name == "C2" else 4), zero_cnn=True, linear_pa=True)

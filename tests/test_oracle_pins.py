@@ -383,3 +383,58 @@ def test_full_chain_c1_runs_and_is_sane():
     assert 0 <= out["counts"][0] <= out["counts"][1]
     rms = np.sqrt(np.mean(np.abs(out["x"]) ** 2))
     assert 0.2 < rms < 0.4
+
+
+# ============================================================================ paper FD-CNN head (NEXT f2)
+def test_fdcnn_paper_golden_hand_computed():
+    g = _read_golden("fdcnn_paper_2x2.txt")
+    W1 = np.zeros((1, 2, 3, 3))
+    W1[0, 0, 1, 1] = 1.0
+    W1[0, 1, 0, 0] = 2.0
+    W2 = np.array([[1, 0, 1, 0], [2, 0, -1, 0], [-1, 0, 0, 0], [0, 0, 0.5, 0]], dtype=float)
+    params = np.concatenate([W1.ravel(), [0.5], W2.ravel(), [0.1, 0.2, 0.3, 0.4]])
+    st = O.fdcnn_paper_forward(g["s"][None, None, :], params, 2, n_conv=1)
+    assert np.max(np.abs(st[0, 0] - g["st"])) < 1e-14
+
+
+def test_fdcnn_paper_vs_torch_float64():
+    torch = pytest.importorskip("torch")
+    F = torch.nn.functional
+    cfg = configs.PAPER
+    inp = gen.make_inputs(cfg, range(2))
+    s = inp["s"].astype(np.complex128)
+    p = inp["params"].astype(np.float64)
+    S, Nd, nc = cfg.S, cfg.N_d, cfg.n_conv
+    K = nc * S * S
+    W1 = torch.tensor(p[:nc * 18].reshape(nc, 2, 3, 3))
+    b1 = torch.tensor(p[nc * 18:nc * 19])
+    W2 = torch.tensor(p[nc * 19:nc * 19 + 2 * Nd * K].reshape(2 * Nd, K))
+    b2 = torch.tensor(p[nc * 19 + 2 * Nd * K:])
+    flat = np.zeros((s.shape[0] * cfg.U, S * S), complex)
+    flat[:, :Nd] = s.reshape(-1, Nd)
+    img = torch.tensor(np.stack([flat.real, flat.imag], 1).reshape(-1, 2, S, S))
+    out = F.linear(torch.relu(F.conv2d(img, W1, b1, padding=1)).flatten(1), W2, b2).numpy()
+    want = (out[:, :Nd] + 1j * out[:, Nd:]).reshape(s.shape)
+    assert np.max(np.abs(O.fdcnn_paper_forward(s, p, Nd, nc) - want)) < 1e-12
+
+
+def test_fdcnn_paper_identity_head_and_chain_invariant():
+    cfg = configs.PAPER
+    inp = gen.make_inputs(cfg, range(2), zero_cnn=True, linear_pa=True)
+    st = O.fdcnn_paper_forward(inp["s"], inp["params"], cfg.N_d, cfg.n_conv)
+    assert np.max(np.abs(st - inp["s"])) < 1e-12
+    out = O.run_config(cfg, inp)
+    assert np.max(np.abs(out["yhat"] / out["alpha"] - inp["s"])) < 1e-12 and out["counts"][0] == 0
+
+
+def test_paper_flop_formula_eqs_16_18():
+    """C_Conv = 2 N^Conv L_U (2 K_C^2 - 1) (S/K_S)^2, C_FC = 8 N_d L_U (S/K_S)^2:
+    1,256,000 at the paper's N_d = 384 (S = 20); Fig. 3 prints 1,205,760 = the same with
+    S^2 -> N_d (reading A23).  Counts the MACs the oracle's head performs (x2 FLOP)."""
+    Nd, S, nc = 384, 20, 2
+    conv = 2 * nc * 1 * (2 * 9 - 1) * S * S
+    fc = 8 * Nd * 1 * S * S
+    assert conv + fc == 1_256_000
+    assert 2 * nc * (2 * 9 - 1) * Nd + 8 * Nd * Nd == 1_205_760
+    # the oracle's FC is a (2 N_d) x (N^Conv S^2) matrix: 2 * MACs == C_FC
+    assert 2 * (2 * Nd) * (nc * S * S) == fc

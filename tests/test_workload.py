@@ -15,10 +15,13 @@ def test_determinism_and_substreams():
 
 
 def test_config_derived_sizes():
-    assert [c.N_ifft for c in configs.CONFIGS.values()] == [128, 4096, 8192, 16384, 16384]
-    assert [c.S for c in configs.CONFIGS.values()] == [6, 25, 35, 58, 58]
-    assert [c.n_coef for c in configs.CONFIGS.values()] == [21, 80, 80, 203, 203]
-    assert [c.n_params for c in configs.CONFIGS.values()] == [150, 2914, 19682, 19682, 113154]
+    base = [configs.C1, configs.C2, configs.C3, configs.C4, configs.C5]
+    assert [c.N_ifft for c in base] == [128, 4096, 8192, 16384, 16384]
+    assert [c.S for c in base] == [6, 25, 35, 58, 58]
+    assert [c.n_coef for c in base] == [21, 80, 80, 203, 203]
+    assert [c.n_params for c in base] == [150, 2914, 19682, 19682, 113154]
+    p = configs.PAPER                       # paper workload P:204-206 with the paper head
+    assert (p.N_ifft, p.S, p.n_params) == (4096, 20, 2 * 19 + 768 * 800 + 768)
 
 
 def test_channel_pdp_and_moments():

@@ -35,6 +35,8 @@ class ChainConfig:
     seed: int
     rho: float = 0.3            # per-antenna TD RMS target (reading A12, BASELINE C1)
     w_std: float = 0.05         # CNN init std (reading A6, BASELINE C1)
+    head: str = "residual"      # "residual": BASELINE conv stack (A1); "paper": conv + FC
+    n_conv: int = 2             # paper head: N^Conv conv kernels
 
     @property
     def N_ifft(self) -> int:
@@ -60,7 +62,15 @@ class ChainConfig:
 
     @property
     def n_params(self) -> int:
+        if self.head == "paper":
+            return paper_head_n_params(self.n_conv, self.N_d)
         return sum(co * ci * 9 + co for ci, co in zip(self.chans[:-1], self.chans[1:]))
+
+
+def paper_head_n_params(n_conv: int, N_d: int) -> int:
+    """Paper FD-CNN: conv W1[n_conv][2][3][3] + b1[n_conv], FC W2[2 N_d][n_conv S^2] + b2[2 N_d]."""
+    S = int(math.isqrt(N_d - 1)) + 1
+    return n_conv * 2 * 9 + n_conv + 2 * N_d * n_conv * S * S + 2 * N_d
 
 
 C1 = ChainConfig("C1", U=2, B=8, N_fft=64, N_d=36, os=2, M_qam=16, n_sym=4, T=4,
@@ -79,7 +89,15 @@ C5 = ChainConfig("C5", U=32, B=512, N_fft=4096, N_d=3300, os=4, M_qam=256, n_sym
                  pdp="exp3dB", orders=(1, 3, 5, 7, 9), L=6, M=3,
                  chans=(2, 64, 64, 64, 64, 2), spread=0.10, seed=4)
 
-CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5)}
+# The paper's own workload with the paper's FD-CNN head (NEXT f2):
+# N = 4096 IDFT, N_d = 384, U = 8, B = 32, 256-QAM, T = 10 uniform-PDP taps, FD-CNN
+# ceil(sqrt(N_d)) = 20, L_U = 1, 3x3 kernels, stride 1, N^Conv = 2, ReLU, FC to 2 N_d.
+# The PA keeps the odd-order GMP of reading A13 (K = 7 -> orders 1..7, memory 3, G = 1).
+PAPER = ChainConfig("P", U=8, B=32, N_fft=1024, N_d=384, os=4, M_qam=256, n_sym=1024, T=10,
+                    pdp="uniform", orders=(1, 3, 5, 7), L=3, M=1, chans=(2, 2), spread=0.05, seed=5,
+                    head="paper", n_conv=2)
+
+CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5, PAPER)}
 
 
 def get(name: str) -> ChainConfig:

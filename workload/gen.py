@@ -130,6 +130,35 @@ def cnn_zero(cfg: ChainConfig) -> np.ndarray:
     return np.zeros(cfg.n_params, dtype=np.float32)
 
 
+def paper_head_params(cfg: ChainConfig) -> np.ndarray:
+    """Paper FD-CNN head, random init: conv N(0, 0.05^2), FC N(0, 1/fan_in).
+    Layout: W1[n_conv][2][3][3], b1[n_conv], W2[2 N_d][n_conv S^2], b2[2 N_d]."""
+    gw = rng(cfg.seed, STREAM_CNN_W)
+    gb = rng(cfg.seed, STREAM_CNN_B)
+    K = cfg.n_conv * cfg.S * cfg.S
+    parts = [gw.normal(0.0, cfg.w_std, size=cfg.n_conv * 18), gb.normal(0.0, cfg.w_std, size=cfg.n_conv),
+             gw.normal(0.0, 1.0 / np.sqrt(K), size=2 * cfg.N_d * K), gb.normal(0.0, cfg.w_std, size=2 * cfg.N_d)]
+    return np.concatenate(parts).astype(np.float32)
+
+
+def paper_head_identity(cfg: ChainConfig, offset: float = 4.0) -> np.ndarray:
+    """A paper head that passes s through: conv kernel 0 = Re, kernel 1 = Im (centre tap) with
+    bias +offset so ReLU never clips (|s| < offset), FC selects pixel i of each map, bias -offset.
+    Only kernels 0 and 1 are used (n_conv >= 2)."""
+    S, Nd, n_conv = cfg.S, cfg.N_d, cfg.n_conv
+    W1 = np.zeros((n_conv, 2, 3, 3))
+    W1[0, 0, 1, 1] = 1.0
+    W1[1, 1, 1, 1] = 1.0
+    b1 = np.zeros(n_conv)
+    b1[:2] = offset
+    W2 = np.zeros((2 * Nd, n_conv * S * S))
+    for i in range(Nd):
+        W2[i, 0 * S * S + i] = 1.0
+        W2[Nd + i, 1 * S * S + i] = 1.0
+    b2 = np.full(2 * Nd, -offset)
+    return np.concatenate([W1.ravel(), b1, W2.ravel(), b2]).astype(np.float32)
+
+
 # ----------------------------------------------------------------------------- bundle
 def make_inputs(cfg: ChainConfig, symbols=None, *, zero_cnn=False, linear_pa=False):
     """All inputs of one run (or of a subset of its symbols)."""
@@ -143,5 +172,6 @@ def make_inputs(cfg: ChainConfig, symbols=None, *, zero_cnn=False, linear_pa=Fal
         "s": qam_symbols(idx, cfg.M_qam),
         "h_taps": channel_taps(cfg),
         "coef": gmp_identity(cfg) if linear_pa else gmp_coefficients(cfg),
-        "params": cnn_zero(cfg) if zero_cnn else cnn_params(cfg),
+        "params": (paper_head_identity(cfg) if zero_cnn else paper_head_params(cfg)) if cfg.head == "paper"
+        else (cnn_zero(cfg) if zero_cnn else cnn_params(cfg)),
     }
