@@ -271,20 +271,97 @@ def slice_ser(yhat: np.ndarray, alpha: float, idx: np.ndarray, M_qam: int, eps: 
     return dec.astype(np.uint16), counts
 
 
+# ============================================================================ impairments (NEXT f3)
+# Counter-based RNG: Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11).  The GPU implements the
+# same generator, so the noise of any (symbol, antenna/UE, sample) is reproducible anywhere.
+PHILOX_M = (0xD2511F53, 0xCD9E8D57)
+PHILOX_W = (0x9E3779B9, 0xBB67AE85)
+STREAM_PA_NOISE, STREAM_AWGN = 1, 2
+
+
+def philox4x32_10(ctr, key):
+    """ctr uint32 [..., 4], key (k0, k1) -> uint32 [..., 4]; 10 rounds, key bumped between rounds."""
+    mask = np.uint64(0xFFFFFFFF)
+    c = [np.asarray(ctr)[..., i].astype(np.uint64) for i in range(4)]
+    k0, k1 = np.uint64(key[0]), np.uint64(key[1])
+    for _ in range(10):
+        p0 = np.uint64(PHILOX_M[0]) * c[0]
+        p1 = np.uint64(PHILOX_M[1]) * c[2]
+        c = [(p1 >> np.uint64(32)) ^ c[1] ^ k0, p1 & mask, (p0 >> np.uint64(32)) ^ c[3] ^ k1, p0 & mask]
+        k0 = (k0 + np.uint64(PHILOX_W[0])) & mask
+        k1 = (k1 + np.uint64(PHILOX_W[1])) & mask
+    return np.stack(c, axis=-1).astype(np.uint32)
+
+
+def complex_gaussian(idx, stream, key64, std):
+    """CN(0, std^2) noise for global sample indices idx: Philox counter (idx lo, idx hi, stream, 0),
+    key (key64 lo, key64 hi); Box-Muller on the first two words, u = (x + 1/2) 2^-32."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    ctr = np.stack([idx & np.uint64(0xFFFFFFFF), idx >> np.uint64(32),
+                    np.full(idx.shape, stream, np.uint64), np.zeros(idx.shape, np.uint64)], axis=-1)
+    x = philox4x32_10(ctr, (key64 & 0xFFFFFFFF, key64 >> 32)).astype(np.float64)
+    u1 = (x[..., 0] + 0.5) * 2.0 ** -32
+    u2 = (x[..., 1] + 0.5) * 2.0 ** -32
+    r = np.sqrt(-2.0 * np.log(u1))
+    return (std / np.sqrt(2.0)) * r * (np.cos(2 * np.pi * u2) + 1j * np.sin(2 * np.pi * u2))
+
+
+def pa_impair(y, clip, noise_std, key64, symbols, B_total, b0=0):
+    """PA saturation then measurement noise (order as SPEC pa_forward S:214): |y| > clip is
+    scaled to clip with the phase kept; then + CN(0, noise_std^2) with the global sample index
+    ((symbol * B_total + b0 + b) * N + m)."""
+    y = np.asarray(y, dtype=np.complex128).copy()
+    if clip > 0:
+        a = np.abs(y)
+        y = np.where(a > clip, y * (clip / np.maximum(a, 1e-300)), y)
+    if noise_std > 0:
+        n, Bl, N = y.shape
+        sym = np.asarray(symbols, dtype=np.uint64)[:, None, None]
+        b = np.arange(Bl, dtype=np.uint64)[None, :, None] + np.uint64(b0)
+        m = np.arange(N, dtype=np.uint64)[None, None, :]
+        y = y + complex_gaussian((sym * np.uint64(B_total) + b) * np.uint64(N) + m, STREAM_PA_NOISE, key64, noise_std)
+    return y
+
+
+def ue_awgn(yhat, n0, key64, symbols):
+    """AWGN at the UEs: w_n ~ CN(0, N_0 I) per TD sample; under the unitary DFT (A9) its
+    data-subcarrier image is CN(0, N_0) i.i.d., drawn here per global index ((symbol U + u) N_d + j)."""
+    yhat = np.asarray(yhat, dtype=np.complex128)
+    if n0 <= 0:
+        return yhat
+    n, U, Nd = yhat.shape
+    sym = np.asarray(symbols, dtype=np.uint64)[:, None, None]
+    u = np.arange(U, dtype=np.uint64)[None, :, None]
+    j = np.arange(Nd, dtype=np.uint64)[None, None, :]
+    return yhat + complex_gaussian((sym * np.uint64(U) + u) * np.uint64(Nd) + j, STREAM_AWGN, key64, np.sqrt(n0))
+
+
+def csi_estimate(h_taps, h_err, eta):
+    """H_t^est = sqrt(1 - eta) H_t + sqrt(eta) H_t^err (P:85)."""
+    return np.sqrt(1.0 - eta) * np.asarray(h_taps, np.complex128) + np.sqrt(eta) * np.asarray(h_err, np.complex128)
+
+
 # ============================================================================ composition
 def run_chain(s, idx, h_taps, coef, params, *, chans, orders, L, M, N_ifft, M_qam, rho=0.3, head="residual",
-              n_conv=2):
-    """The whole hot path, stage by stage.  Returns every stage output."""
+              n_conv=2, clip=0.0, pa_noise_std=0.0, awgn_n0=0.0, csi_eta=0.0, h_err=None, noise_key=0,
+              symbols=None):
+    """The whole hot path, stage by stage, optionally with the impairments
+    of NEXT f3 (PA clip + measurement noise, AWGN, imperfect CSI).  Returns every stage output."""
     s = np.asarray(s, dtype=np.complex128)
     N_d = s.shape[-1]
+    B = np.asarray(h_taps).shape[2]
+    symbols = np.arange(s.shape[0]) if symbols is None else np.asarray(symbols)
     out = {}
     out["s_tilde"] = dpd_forward(head, s, params, chans, N_d, n_conv)
     out["Hfd"] = channel_fd(h_taps, N_ifft, N_d)
-    out["P"], out["alpha"], _ = zf_precoder(out["Hfd"], N_ifft, rho)
+    Hest = out["Hfd"] if csi_eta <= 0 else channel_fd(csi_estimate(h_taps, h_err, csi_eta), N_ifft, N_d)
+    out["P"], out["alpha"], _ = zf_precoder(Hest, N_ifft, rho)
     out["X"] = precode(out["P"], out["s_tilde"])
     out["x"] = ofdm_modulate(out["X"], N_ifft)
     out["y"] = gmp_pa(out["x"], coef, orders, L, M)
-    out["yhat"] = ue_receive(out["y"], out["Hfd"], N_d)
+    if clip > 0 or pa_noise_std > 0:
+        out["y"] = pa_impair(out["y"], clip, pa_noise_std, noise_key, symbols, B)
+    out["yhat"] = ue_awgn(ue_receive(out["y"], out["Hfd"], N_d), awgn_n0, noise_key, symbols)
     out["dec"], out["counts"] = slice_ser(out["yhat"], out["alpha"], idx, M_qam)
     return out
 
@@ -293,4 +370,6 @@ def run_config(cfg, inp):
     """run_chain with a workload.configs.ChainConfig and a workload.gen.make_inputs bundle."""
     return run_chain(inp["s"], inp["idx"], inp["h_taps"], inp["coef"], inp["params"],
                      chans=cfg.chans, orders=cfg.orders, L=cfg.L, M=cfg.M,
-                     N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, rho=cfg.rho, head=cfg.head, n_conv=cfg.n_conv)
+                     N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, rho=cfg.rho, head=cfg.head, n_conv=cfg.n_conv,
+                     clip=cfg.clip, pa_noise_std=cfg.pa_noise_std, awgn_n0=cfg.awgn_n0, csi_eta=cfg.csi_eta,
+                     h_err=inp.get("h_err"), noise_key=inp.get("noise_key", 0), symbols=inp.get("symbols"))

@@ -37,6 +37,11 @@ class ChainConfig:
     w_std: float = 0.05         # CNN init std (reading A6, BASELINE C1)
     head: str = "residual"      # "residual": BASELINE conv stack (A1); "paper": conv + FC
     n_conv: int = 2             # paper head: N^Conv conv kernels
+    # impairments; all off on the hot path (reading A11, A16)
+    clip: float = 0.0           # PA saturation amplitude ("saturation point"), 0 = off
+    pa_noise_std: float = 0.0   # PA measurement noise std per complex sample, CN(0, std^2)
+    awgn_n0: float = 0.0        # AWGN variance N_0 at the UEs, per data subcarrier (unitary DFT)
+    csi_eta: float = 0.0        # imperfect-CSI weight eta
 
     @property
     def N_ifft(self) -> int:
@@ -98,6 +103,18 @@ PAPER = ChainConfig("P", U=8, B=32, N_fft=1024, N_d=384, os=4, M_qam=256, n_sym=
                     head="paper", n_conv=2)
 
 CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5, PAPER)}
+
+
+def impaired(cfg: ChainConfig, clip: float = 1.0, pa_noise_std: float = None, awgn_n0: float = 1e-3,
+             csi_eta: float = 1e-3) -> ChainConfig:
+    """cfg with the paper's impairments switched on (NEXT f3).  In the normalised units of the
+    chain (TD RMS rho = 0.3): clip at `clip`; PA noise std defaults to the paper's ratio
+    0.053 V / 24.02 V of the saturation amplitude; eta = 0.001 as in P:204."""
+    import dataclasses
+    if pa_noise_std is None:
+        pa_noise_std = clip * 0.053 / 24.02
+    return dataclasses.replace(cfg, name=cfg.name + "i", clip=clip, pa_noise_std=pa_noise_std, awgn_n0=awgn_n0,
+                               csi_eta=csi_eta)
 
 
 def get(name: str) -> ChainConfig:

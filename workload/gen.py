@@ -30,6 +30,8 @@ STREAM_CHANNEL = 1
 STREAM_SPREAD = 2
 STREAM_CNN_W = 3
 STREAM_CNN_B = 4
+STREAM_CSI = 5
+STREAM_NOISE = 6
 
 
 def rng(seed: int, stream: int, index: int = 0) -> np.random.Generator:
@@ -74,6 +76,19 @@ def channel_taps(cfg: ChainConfig) -> np.ndarray:
     z = g.standard_normal((cfg.T, cfg.U, cfg.B, 2))
     h = (z[..., 0] + 1j * z[..., 1]) * np.sqrt(pdp(cfg) / 2.0)[:, None, None]
     return h.astype(np.complex64)
+
+
+def csi_error_taps(cfg: ChainConfig) -> np.ndarray:
+    """complex64 [T][U][B] H^err ~ CN(0, I) per tap entry."""
+    g = rng(cfg.seed, STREAM_CSI)
+    z = g.standard_normal((cfg.T, cfg.U, cfg.B, 2))
+    return ((z[..., 0] + 1j * z[..., 1]) / np.sqrt(2.0)).astype(np.complex64)
+
+
+def noise_key(cfg: ChainConfig) -> int:
+    """64-bit key of the counter-based (Philox4x32-10) noise generator shared by the oracle
+    and the GPU; counters are global sample indices, so any shard regenerates its noise."""
+    return int(np.random.SeedSequence([cfg.seed, STREAM_NOISE]).generate_state(1, dtype=np.uint64)[0])
 
 
 # ----------------------------------------------------------------------------- PA bank
@@ -171,6 +186,8 @@ def make_inputs(cfg: ChainConfig, symbols=None, *, zero_cnn=False, linear_pa=Fal
         "idx": idx,
         "s": qam_symbols(idx, cfg.M_qam),
         "h_taps": channel_taps(cfg),
+        "h_err": csi_error_taps(cfg),
+        "noise_key": noise_key(cfg),
         "coef": gmp_identity(cfg) if linear_pa else gmp_coefficients(cfg),
         "params": (paper_head_identity(cfg) if zero_cnn else paper_head_params(cfg)) if cfg.head == "paper"
         else (cnn_zero(cfg) if zero_cnn else cnn_params(cfg)),
