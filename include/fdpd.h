@@ -154,6 +154,36 @@ int chain_txrx(const void* P, const void* s_tilde, const void* coef, void* y, vo
                long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream);
 
 /* -------------------------------------------------------------------------
+ * Impairments (all off on the hot path, readings A11/A16).
+ * Noise is drawn from the counter-based Philox4x32-10 generator (Salmon et al., SC'11)
+ * with counter (global index lo, hi, stream, 0) and key (noise_key lo, hi): stream 1 = PA
+ * measurement noise at index ((sym0 + n) B_total + b0 + b) N_ifft + m, stream 2 = AWGN
+ * at index ((sym0 + n) U + u) N_d + j; Box-Muller on the first two output words.  Any
+ * batch / shard therefore reproduces the same noise as the whole run (and the oracle).
+ * ------------------------------------------------------------------------- */
+typedef struct fd_impair {
+    float clip;                    /* PA saturation amplitude, phase kept; 0 = off */
+    float pa_noise_std;            /* PA measurement noise std, CN(0, std^2); 0 = off */
+    float awgn_n0;                 /* UE noise variance N_0 per data subcarrier; 0 = off */
+    float csi_eta;                 /* imperfect-CSI weight eta, zf_precoder_build_ex only */
+    unsigned long long noise_key;  /* Philox key */
+    long long sym0;                /* global index of the batch's first OFDM symbol */
+    int b0, B_total;               /* antenna rows of this call within the full array (0: B_loc) */
+} fd_impair;
+
+/* chain_txrx with the PA clip + measurement noise applied to the PA output (y and XPA). */
+int chain_txrx_ex(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA,
+                  const int* orders, int n_orders, int L, int M,
+                  long long n_sym, int B_loc, int U, int N_d, int N_ifft, const fd_impair* imp,
+                  cudaStream_t stream);
+/* zf_precoder_build with imperfect CSI: the precoder is built from
+ * H_est = sqrt(1 - eta) H + sqrt(eta) H_err while h_fd (the channel the UEs see) is
+ * built from H.  h_err device complex64 [T][U][B]; eta in [0, 1]. */
+int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T, int U, int B, int N_ifft,
+                         int N_d, float rho, int b0, int B_loc, void* h_fd, void* P, float* alpha,
+                         void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
  * a6. Evaluation — Eqs. (4)-(5) P:67-77 (noiseless, reading A11), SER P:351.
  *
  * ue_receive: XPA[n][b][j] = N^-1/2 sum_m y[n][b][m] exp(-j 2 pi k_j m / N);
@@ -184,6 +214,10 @@ int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, i
 int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
                    uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d,
                    float boundary_eps, cudaStream_t stream);
+/* ue_combine_ser with AWGN (imp->awgn_n0) added to yhat before slicing. */
+int ue_combine_ser_ex(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                      uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d,
+                      float boundary_eps, const fd_impair* imp, cudaStream_t stream);
 /* ue_receive (accumulate = 0) then ue_slice_ser, single GPU. */
 int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace, size_t workspace_bytes,
                    float alpha, const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts,

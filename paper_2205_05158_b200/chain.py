@@ -41,7 +41,9 @@ class Shapes:
 
 
 class Chain:
-    def __init__(self, shapes: Shapes, h_taps, coef, params, device="cuda", max_batch=1, b0=0, B_loc=None):
+    def __init__(self, shapes: Shapes, h_taps, coef, params, device="cuda", max_batch=1, b0=0, B_loc=None,
+                 impair=None):
+        """impair (NEXT f3, optional): dict with clip, pa_noise_std, awgn_n0, csi_eta, noise_key, h_err."""
         self.sh = shapes
         self.device = torch.device(device)
         dev = self.device
@@ -50,10 +52,22 @@ class Chain:
         self.h_taps = torch.as_tensor(h_taps).to(dev, torch.complex64).contiguous()
         self.coef = torch.as_tensor(coef).to(dev, torch.complex64)[b0:b0 + self.B_loc].contiguous()
         self.params = torch.as_tensor(params).to(dev, torch.float32).contiguous()
+        self.impair = dict(impair) if impair else None
         # a2, once per channel realisation
-        self.h_fd, self.P, self.alpha = fdpd.zf_precoder_build(self.h_taps, shapes.N_ifft, shapes.N_d, shapes.rho,
-                                                               b0=b0, B_loc=self.B_loc)
+        if self.impair and self.impair.get("csi_eta", 0.0) > 0:
+            h_err = torch.as_tensor(self.impair["h_err"]).to(dev, torch.complex64).contiguous()
+            self.h_fd, self.P, self.alpha = fdpd.zf_precoder_build_ex(self.h_taps, h_err, self.impair["csi_eta"],
+                                                                      shapes.N_ifft, shapes.N_d, shapes.rho, b0=b0,
+                                                                      B_loc=self.B_loc)
+        else:
+            self.h_fd, self.P, self.alpha = fdpd.zf_precoder_build(self.h_taps, shapes.N_ifft, shapes.N_d,
+                                                                   shapes.rho, b0=b0, B_loc=self.B_loc)
         self.reserve(max_batch)
+
+    def _imp(self, sym0):
+        i = self.impair or {}
+        return fdpd.make_impairments(i.get("clip", 0.0), i.get("pa_noise_std", 0.0), i.get("awgn_n0", 0.0),
+                                     i.get("csi_eta", 0.0), i.get("noise_key", 0), sym0, self.b0, self.sh.B)
 
     def reserve(self, n):
         sh, dev = self.sh, self.device
@@ -90,28 +104,37 @@ class Chain:
         return fdpd.ue_receive_ser(y, self.h_fd, self.alpha, tx_idx, sh.M_qam, yhat=self.yhat[:n], counts=counts,
                                    dec=dec, workspace=self.ws_rx, boundary_eps=sh.eps)
 
-    def txrx(self, s_tilde):
+    def txrx(self, s_tilde, sym0=0):
         """Fused precode -> IDFT -> GMP (waveform stored) -> receive DFT at the data bins."""
         n = s_tilde.shape[0]
         sh = self.sh
         XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
+        if self.impair:
+            return fdpd.chain_txrx_ex(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, self._imp(sym0),
+                                      y=self.y[:n], XPA=XPA)
         return fdpd.chain_txrx(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, y=self.y[:n], XPA=XPA)
 
-    def combine(self, XPA, tx_idx, counts=None, dec=None):
+    def combine(self, XPA, tx_idx, counts=None, dec=None, sym0=0):
         n = XPA.shape[0]
         sh = self.sh
         counts = self.counts if counts is None else counts
+        if self.impair:
+            return fdpd.ue_combine_ser_ex(XPA, self.h_fd, self.alpha, tx_idx, sh.M_qam, self._imp(sym0),
+                                          yhat=self.yhat[:n], counts=counts, dec=dec, boundary_eps=sh.eps)
         return fdpd.ue_combine_ser(XPA, self.h_fd, self.alpha, tx_idx, sh.M_qam, yhat=self.yhat[:n], counts=counts,
                                    dec=dec, boundary_eps=sh.eps)
 
-    def step(self, s, tx_idx, counts=None, dec=None, fused=True):
-        """One pass of the hot path over a batch (s, tx_idx on the device):
+    def step(self, s, tx_idx, counts=None, dec=None, fused=True, sym0=0):
+        """One pass of the hot path over a batch (s, tx_idx on the device; sym0 = global index of
+        the batch's first symbol, used by the impairment noise):
         fdcnn_forward -> chain_txrx -> ue_combine_ser   (fused=True, 3 libfdpd calls)
-        fdcnn_forward -> chain_tx -> ue_receive_ser     (fused=False)."""
+        fdcnn_forward -> chain_tx -> ue_receive_ser     (fused=False, unimpaired only)."""
         if s.shape[0] > self.cap:
             self.reserve(s.shape[0])
         st = self.dpd(s)
         if not fused:
+            if self.impair:
+                raise ValueError("the unfused path has no impairment stages; use fused=True")
             return self.rx(self.tx(st), tx_idx, counts=counts, dec=dec)
-        _, XPA = self.txrx(st)
-        return self.combine(XPA, tx_idx, counts=counts, dec=dec)
+        _, XPA = self.txrx(st, sym0)
+        return self.combine(XPA, tx_idx, counts=counts, dec=dec, sym0=sym0)

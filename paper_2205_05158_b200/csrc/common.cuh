@@ -92,6 +92,51 @@ __device__ __forceinline__ float2 cfma2(float2 a, float2 b, float2 acc) {
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
+// ---------------------------------------------------------------- impairments (NEXT f3)
+// Counter-based Philox4x32-10 (Salmon et al., SC'11), the generator the oracle implements in
+// numpy: counter (idx lo, idx hi, stream, 0), key (key lo, key hi).
+struct Impair {
+    float clip;            // PA saturation amplitude, 0 = off
+    float pa_std;          // PA measurement noise std (CN), 0 = off
+    float awgn_std;        // sqrt(N_0) at the UEs, 0 = off
+    unsigned key_lo, key_hi;
+    long long sym0;        // global index of the batch's first symbol
+    int b0, B_total;       // antenna rows of this call within the full array
+};
+constexpr unsigned STREAM_PA_NOISE = 1, STREAM_AWGN = 2;
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, unsigned k0, unsigned k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const unsigned lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const unsigned lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+// CN(0, std^2) sample of global index idx (Box-Muller on the first two words, u = (x + 1/2) 2^-32)
+__device__ __forceinline__ float2 cgauss(unsigned long long idx, unsigned stream, unsigned k0, unsigned k1,
+                                         float std) {
+    const uint4 x = philox4x32_10(make_uint4((unsigned)idx, (unsigned)(idx >> 32), stream, 0u), k0, k1);
+    const float u1 = ((float)x.x + 0.5f) * 2.3283064365386963e-10f;
+    const float u2 = ((float)x.y + 0.5f) * 2.3283064365386963e-10f;
+    const float r = sqrtf(-2.f * logf(u1)) * std * 0.70710678118654752f;
+    float s, c;
+    sincospif(2.f * u2, &s, &c);
+    return make_float2(r * c, r * s);
+}
+// PA saturation (phase kept) then measurement noise, P:202 (order as SPEC pa_forward)
+__device__ __forceinline__ float2 pa_impair(float2 y, unsigned long long idx, const Impair& im) {
+    if (im.clip > 0.f) {
+        const float a2 = fmaf(y.x, y.x, y.y * y.y);
+        if (a2 > im.clip * im.clip) y = cscale(y, im.clip / sqrtf(a2));
+    }
+    if (im.pa_std > 0.f) y = cadd(y, cgauss(idx, STREAM_PA_NOISE, im.key_lo, im.key_hi, im.pa_std));
+    return y;
+}
+
 // ---------------------------------------------------------------- TMA bulk copy + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -180,7 +180,8 @@ __device__ __forceinline__ float2 gmp_sample_generic(const float2* __restrict__ 
 template <int KP, int L, int M, int RS>
 __device__ __forceinline__ void gmp_symbol(const float2* __restrict__ usm, const float* __restrict__ esm,
                                            const float2* __restrict__ cf, int N, const GmpDesc& d,
-                                           float2* __restrict__ y, int tid, int T) {
+                                           float2* __restrict__ y, int tid, int T, const Impair* im = nullptr,
+                                           unsigned long long nbase = 0) {
     if constexpr (KP > 0) {
         const int stride = N / RS;
         for (int i0 = tid; i0 < stride; i0 += T) {
@@ -193,10 +194,13 @@ __device__ __forceinline__ void gmp_symbol(const float2* __restrict__ usm, const
             for (int r = 0; r < RS; ++r) m[r] = i0 + r * stride;
             gmp_group<KP, L, M, RS>(usm, esm, cf, N, m, out);
 #pragma unroll
-            for (int r = 0; r < RS; ++r) y[m[r]] = out[r];
+            for (int r = 0; r < RS; ++r) y[m[r]] = im ? pa_impair(out[r], nbase + m[r], *im) : out[r];
         }
     } else {
-        for (int m = tid; m < N; m += T) y[m] = gmp_sample_generic(usm, esm, cf, N, m, d);
+        for (int m = tid; m < N; m += T) {
+            const float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
+            y[m] = im ? pa_impair(o, nbase + m, *im) : o;
+        }
     }
 }
 
@@ -209,7 +213,8 @@ template <int LOG2N, int KP, int L, int M, int RS>
 __device__ __forceinline__ void gmp_symbol_to_fft(const float2* __restrict__ usm, const float* __restrict__ esm,
                                                   const float2* __restrict__ cf, const GmpDesc& d,
                                                   float2* __restrict__ y, int tid,
-                                                  float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()]) {
+                                                  float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
+                                                  const Impair* im = nullptr, unsigned long long nbase = 0) {
     constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
     constexpr int QN = VPT / R0;      // pass-0 butterflies per thread
     // register slot of sample tid + T*j in the pass-0 layout: j = q + QN * r'
@@ -227,6 +232,7 @@ __device__ __forceinline__ void gmp_symbol_to_fft(const float2* __restrict__ usm
             gmp_group<KP, L, M, RS>(usm, esm, cf, N, m, out);
 #pragma unroll
             for (int r = 0; r < RS; ++r) {
+                if (im) out[r] = pa_impair(out[r], nbase + m[r], *im);
                 if (y) y[m[r]] = out[r];
                 // k is a runtime loop index: select the slot with a compile-time switch over k
 #pragma unroll
@@ -238,7 +244,8 @@ __device__ __forceinline__ void gmp_symbol_to_fft(const float2* __restrict__ usm
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
             const int m = tid + T * j;
-            const float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
+            float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
+            if (im) o = pa_impair(o, nbase + m, *im);
             if (y) y[m] = o;
             v[slot(j)] = o;
         }
@@ -355,13 +362,18 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
 template <int KP, int L, int M, int R, bool YS = false>
 __device__ __forceinline__ void gmp_runs_symbol(float2* __restrict__ buf, float* __restrict__ esw,
                                                 const float2* __restrict__ cf, int N, float2* __restrict__ y,
-                                                int tid, int T, float2* __restrict__ ysm = nullptr) {
+                                                int tid, int T, float2* __restrict__ ysm = nullptr,
+                                                const Impair* im = nullptr, unsigned long long nbase = 0) {
 #pragma unroll 1
     for (int rho = tid; rho < N / R; rho += T) {
         // keep the coefficient-row loads inside the loop (no hoisting into registers)
         asm volatile("" ::: "memory");
         float2 out[R];
         gmp_run<KP, L, M, R>(buf, esw, cf, N, rho, out);
+        if (im) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) out[i] = pa_impair(out[i], nbase + (unsigned long long)(R * rho + i), *im);
+        }
         float4* y4 = reinterpret_cast<float4*>(y + (size_t)R * rho);
 #pragma unroll
         for (int i = 0; i < R / 2; ++i) y4[i] = make_float4(out[2 * i].x, out[2 * i].y, out[2 * i + 1].x, out[2 * i + 1].y);

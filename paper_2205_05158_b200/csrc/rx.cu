@@ -81,11 +81,11 @@ __global__ void k_slice(const float2* __restrict__ yhat, const uint16_t* __restr
 
 // ============================================================================ channel sum (+ slicing)
 // yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j].  Thread per (n, j), loop over u and b.
-template <bool SER>
+template <bool SER, bool AWGN = false>
 __global__ void __launch_bounds__(128) k_rx_combine(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
                                                     float2* __restrict__ yhat, int B, int U, int N_d, int accumulate,
                                                     const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
-                                                    long long* counts, SliceParams sp) {
+                                                    long long* counts, SliceParams sp, Impair imp) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t n = blockIdx.y;
     int err = 0, near = 0, cnt = 0;
@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(128) k_rx_combine(const float2* __restrict__ X
             for (int b = 0; b < B; ++b) acc = cfma(__ldg(h + (size_t)b * N_d), __ldg(X + (size_t)b * N_d), acc);
             const size_t o = (n * U + u) * N_d + j;
             if (accumulate) acc = cadd(acc, yhat[o]);
+            if constexpr (AWGN)   // AWGN at the UEs, NEXT f3
+                acc = cadd(acc, cgauss((unsigned long long)((imp.sym0 + (long long)n) * U + u) * N_d + j, STREAM_AWGN,
+                                       imp.key_lo, imp.key_hi, imp.awgn_std));
             yhat[o] = acc;
             if (SER) {
                 bool nr = false;
@@ -193,7 +196,7 @@ int ue_receive(const void* y, const void* h_fd, void* yhat, void* workspace, siz
     if (rc) return rc;
     dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
     k_rx_combine<false><<<grid, 128, 0, stream>>>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, accumulate,
-                                                 nullptr, nullptr, nullptr, SliceParams{});
+                                                 nullptr, nullptr, nullptr, SliceParams{}, Impair{});
     return check_launch("ue_receive (combine)");
 }
 
@@ -227,7 +230,7 @@ int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace,
     if (rc) return rc;
     dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
     k_rx_combine<true><<<grid, 128, 0, stream>>>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, 0, tx_idx,
-                                                dec, counts, sp);
+                                                dec, counts, sp, Impair{});
     return check_launch("ue_receive_ser (combine)");
 }
 
@@ -243,7 +246,7 @@ int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, i
     FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat), "ue_combine: misaligned pointer");
     dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
     k_rx_combine<false><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U,
-                                                 N_d, accumulate, nullptr, nullptr, nullptr, SliceParams{});
+                                                 N_d, accumulate, nullptr, nullptr, nullptr, SliceParams{}, Impair{});
     return check_launch("ue_combine");
 }
 
@@ -260,8 +263,37 @@ int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, c
                "ue_combine_ser: misaligned pointer");
     dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
     k_rx_combine<true><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U,
-                                                N_d, 0, tx_idx, dec, counts, sp);
+                                                N_d, 0, tx_idx, dec, counts, sp, Impair{});
     return check_launch("ue_combine_ser");
+}
+
+int ue_combine_ser_ex(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                      uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d,
+                      float boundary_eps, const fd_impair* imp, cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && n_sym <= 65535 && B_loc >= 1 && U >= 1 && N_d >= 1, "ue_combine_ser_ex: bad sizes");
+    FD_REQUIRE(!imp || imp->awgn_n0 >= 0.f, "ue_combine_ser_ex: awgn_n0 < 0");
+    SliceParams sp;
+    int rc = validate_slice(M_qam, alpha, boundary_eps, sp);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(XPA && h_fd && yhat && tx_idx && counts, "ue_combine_ser_ex: NULL pointer");
+    FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat) && aligned8(counts),
+               "ue_combine_ser_ex: misaligned pointer");
+    Impair im{};
+    if (imp) {
+        im.awgn_std = imp->awgn_n0 > 0.f ? sqrtf(imp->awgn_n0) : 0.f;
+        im.key_lo = (unsigned)(imp->noise_key & 0xffffffffull);
+        im.key_hi = (unsigned)(imp->noise_key >> 32);
+        im.sym0 = imp->sym0;
+    }
+    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
+    if (im.awgn_std > 0.f)
+        k_rx_combine<true, true><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat,
+                                                          B_loc, U, N_d, 0, tx_idx, dec, counts, sp, im);
+    else
+        k_rx_combine<true, false><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat,
+                                                           B_loc, U, N_d, 0, tx_idx, dec, counts, sp, im);
+    return check_launch("ue_combine_ser_ex");
 }
 
 }  // extern "C"

@@ -124,7 +124,7 @@ template <int LOG2N, int KP, int L, int M, int RS, bool RX>
 __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     k_chain_tx(const float2* __restrict__ P, const float2* __restrict__ s, const float2* __restrict__ coef,
                float2* __restrict__ y, float2* __restrict__ XPA, const float2* __restrict__ tw, int B, int U,
-               int N_d, float sc, GmpDesc d) {
+               int N_d, float sc, GmpDesc d, Impair imp) {
     constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T;
     constexpr bool YSM = RX && KP > 0 && chain_ysm<LOG2N>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -137,6 +137,11 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     const size_t nb = blockIdx.x;
     const int b = (int)(nb % B);
     const size_t n = nb / B;
+    // PA clip / measurement noise (NEXT f3), global sample index ((sym0 + n) B_total + b0 + b) N + m
+    const bool impaired = imp.clip > 0.f || imp.pa_std > 0.f;
+    const Impair* im = impaired ? &imp : nullptr;
+    const unsigned long long nbase =
+        ((unsigned long long)(imp.sym0 + (long long)n) * imp.B_total + imp.b0 + b) * (unsigned long long)N;
     // precode (Eq. 1) of the data subcarriers into a compact smem spectrum xs (aliases the
     // e region, unused until after the IDFT), with coalesced L2 loads issued 8 at a time.
     // (Measured alternative: staging P_b and s_n with two TMA bulk copies behind an
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
         }
         __syncthreads();
         float2* yo = y + nb * N;
-        gmp_runs_symbol<KP, L, M, RS, YSM>(usm, esm, cf, N, yo, tid, T, ysm);
+        gmp_runs_symbol<KP, L, M, RS, YSM>(usm, esm, cf, N, yo, tid, T, ysm, im, nbase);
         if constexpr (RX) {
             __syncthreads();   // y of the whole CTA is written (CTA-scope visibility) and u is no longer read
             constexpr int R0 = pass_radix<LOG2N>(0);
@@ -226,9 +231,9 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     }
     __syncthreads();
     if constexpr (!RX) {
-        gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
+        gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T, im, nbase);
     } else {
-        gmp_symbol_to_fft<LOG2N, KP, L, M, RS>(usm, esm, cf, d, y ? y + nb * N : nullptr, tid, v);
+        gmp_symbol_to_fft<LOG2N, KP, L, M, RS>(usm, esm, cf, d, y ? y + nb * N : nullptr, tid, v, im, nbase);
         __syncthreads();                       // every lagged read of u is done before the FFT overwrites it
         fft_run<LOG2N, -1>(usm, v, tw, tid);
         float2* xo = XPA + nb * N_d;
@@ -304,7 +309,8 @@ static int launch_gmp(const float2* x, const float2* coef, float2* y, long long 
 
 template <int LOG2N, int KP, int L, int M, int RS, bool RX>
 static int launch_chain_one(const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
-                            long long n_sym, int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
+                            long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp,
+                            cudaStream_t st) {
     constexpr int N = 1 << LOG2N;
     const float2* tw = twiddle_table(N, st);
     if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
@@ -313,19 +319,20 @@ static int launch_chain_one(const float2* P, const float2* s, const float2* coef
     if (smem > 227 * 1024) return fail_arg("chain_tx: shared-memory footprint %zu B too large", smem);
     set_smem(k_chain_tx<LOG2N, KP, L, M, RS, RX>, smem);
     k_chain_tx<LOG2N, KP, L, M, RS, RX><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(
-        P, s, coef, y, XPA, tw, B, U, N_d, (float)(1.0 / std::sqrt((double)N)), d);
+        P, s, coef, y, XPA, tw, B, U, N_d, (float)(1.0 / std::sqrt((double)N)), d, imp);
     return check_launch(RX ? "chain_txrx" : "chain_tx");
 }
 
 template <int LOG2N, bool RX>
 static int launch_chain(int variant, const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
-                        long long n_sym, int B, int U, int N_d, const GmpDesc& d, cudaStream_t st) {
+                        long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp,
+                        cudaStream_t st) {
     switch (variant) {
-        case 1: return launch_chain_one<LOG2N, 3, 2, 1, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
-        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
-        case 3: return launch_chain_one<LOG2N, 5, 6, 3, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
-        case 4: return launch_chain_one<LOG2N, 4, 3, 1, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
-        default: return launch_chain_one<LOG2N, 0, 0, 0, 1, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, st);
+        case 1: return launch_chain_one<LOG2N, 3, 2, 1, 8, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+        case 2: return launch_chain_one<LOG2N, 4, 4, 2, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+        case 3: return launch_chain_one<LOG2N, 5, 6, 3, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+        case 4: return launch_chain_one<LOG2N, 4, 3, 1, 4, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+        default: return launch_chain_one<LOG2N, 0, 0, 0, 1, RX>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
     }
 }
 
@@ -397,8 +404,26 @@ int gmp_pa(const void* x, const void* coef, void* y, const int* orders, int n_or
     }
 }
 
-int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y, const int* orders, int n_orders, int L,
-             int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream) {
+static Impair to_impair(const fd_impair* pub, int B_loc) {
+    Impair im{};
+    im.B_total = B_loc;
+    if (pub) {
+        im.clip = pub->clip;
+        im.pa_std = pub->pa_noise_std;
+        im.awgn_std = pub->awgn_n0 > 0.f ? sqrtf(pub->awgn_n0) : 0.f;
+        im.key_lo = (unsigned)(pub->noise_key & 0xffffffffull);
+        im.key_hi = (unsigned)(pub->noise_key >> 32);
+        im.sym0 = pub->sym0;
+        im.b0 = pub->b0;
+        im.B_total = pub->B_total > 0 ? pub->B_total : B_loc;
+    }
+    return im;
+}
+
+static int chain_tx_impl(const void* P, const void* s_tilde, const void* coef, void* y, const int* orders,
+                         int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft,
+                         const fd_impair* pub, cudaStream_t stream) {
+    const Impair imp = to_impair(pub, B_loc);
     FD_REQUIRE(U >= 1 && U <= 1024, "chain_tx: bad U=%d", U);
     int rc = validate_ofdm(n_sym, B_loc, N_d, N_ifft);
     if (rc) return rc;
@@ -412,12 +437,13 @@ int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y, cons
     const float2 *Pp = (const float2*)P, *sp = (const float2*)s_tilde, *cp = (const float2*)coef;
     float2* yp = (float2*)y;
     FD_LOG2N_SWITCH(ilog2(N_ifft),
-                    (launch_chain<LG, false>(variant, Pp, sp, cp, yp, nullptr, n_sym, B_loc, U, N_d, d, stream)));
+                    (launch_chain<LG, false>(variant, Pp, sp, cp, yp, nullptr, n_sym, B_loc, U, N_d, d, imp, stream)));
 }
 
-int chain_txrx(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA, const int* orders,
-               int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft,
-               cudaStream_t stream) {
+static int chain_txrx_impl(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA,
+                           const int* orders, int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d,
+                           int N_ifft, const fd_impair* pub, cudaStream_t stream) {
+    const Impair imp = to_impair(pub, B_loc);
     FD_REQUIRE(U >= 1 && U <= 1024, "chain_txrx: bad U=%d", U);
     int rc = validate_ofdm(n_sym, B_loc, N_d, N_ifft);
     if (rc) return rc;
@@ -433,7 +459,30 @@ int chain_txrx(const void* P, const void* s_tilde, const void* coef, void* y, vo
     const float2 *Pp = (const float2*)P, *sp = (const float2*)s_tilde, *cp = (const float2*)coef;
     float2 *yp = (float2*)y, *xp = (float2*)XPA;
     FD_LOG2N_SWITCH(ilog2(N_ifft),
-                    (launch_chain<LG, true>(variant, Pp, sp, cp, yp, xp, n_sym, B_loc, U, N_d, d, stream)));
+                    (launch_chain<LG, true>(variant, Pp, sp, cp, yp, xp, n_sym, B_loc, U, N_d, d, imp, stream)));
+}
+
+int chain_tx(const void* P, const void* s_tilde, const void* coef, void* y, const int* orders, int n_orders, int L,
+             int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft, cudaStream_t stream) {
+    return chain_tx_impl(P, s_tilde, coef, y, orders, n_orders, L, M, n_sym, B_loc, U, N_d, N_ifft, nullptr, stream);
+}
+
+int chain_txrx(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA, const int* orders,
+               int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft,
+               cudaStream_t stream) {
+    return chain_txrx_impl(P, s_tilde, coef, y, XPA, orders, n_orders, L, M, n_sym, B_loc, U, N_d, N_ifft, nullptr,
+                           stream);
+}
+
+int chain_txrx_ex(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA, const int* orders,
+                  int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d, int N_ifft,
+                  const fd_impair* imp, cudaStream_t stream) {
+    if (imp) {
+        FD_REQUIRE(imp->clip >= 0.f && imp->pa_noise_std >= 0.f, "chain_txrx_ex: negative impairment");
+        FD_REQUIRE(imp->b0 >= 0 && (imp->B_total == 0 || imp->b0 + B_loc <= imp->B_total), "chain_txrx_ex: bad b0");
+    }
+    return chain_txrx_impl(P, s_tilde, coef, y, XPA, orders, n_orders, L, M, n_sym, B_loc, U, N_d, N_ifft, imp,
+                           stream);
 }
 
 }  // extern "C"

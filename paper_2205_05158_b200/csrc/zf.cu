@@ -18,9 +18,12 @@ __device__ __forceinline__ double2 dcmulc(double2 a, double2 b) {   // a * conj(
     return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
 
+// Herr != NULL (imperfect CSI): the precoder uses H_est = sqrt(1-eta) H + sqrt(eta) Herr
+// while h_fd (the channel the UEs see) is the true H.
 __global__ void __launch_bounds__(256) k_zf(const float2* __restrict__ H, int T, int U, int B, int N, int N_d, int b0,
                                             int B_loc, float2* __restrict__ hfd, float2* __restrict__ P,
-                                            double* __restrict__ tr, int* __restrict__ flag) {
+                                            double* __restrict__ tr, int* __restrict__ flag,
+                                            const float2* __restrict__ Herr, double eta) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* G = reinterpret_cast<double2*>(smem_raw);         // [U][U]  (G, then Ginv)
     double2* Lm = G + U * U;                                   // [U][U]  Cholesky factor
@@ -37,16 +40,23 @@ __global__ void __launch_bounds__(256) k_zf(const float2* __restrict__ H, int T,
         tw[t] = make_double2(c, s);
     }
     __syncthreads();
+    const double ce = sqrt(1.0 - eta), se = sqrt(eta);
     for (int i = tid; i < U * B; i += nth) {
-        double2 acc = make_double2(0.0, 0.0);
+        double2 acc = make_double2(0.0, 0.0), ace = make_double2(0.0, 0.0);
         for (int t = 0; t < T; ++t) {
             const float2 h = H[(size_t)t * U * B + i];
             const double2 w = tw[t];
             acc.x += (double)h.x * w.x - (double)h.y * w.y;
             acc.y += (double)h.x * w.y + (double)h.y * w.x;
+            if (Herr) {
+                const float2 e = Herr[(size_t)t * U * B + i];
+                const double ex = ce * h.x + se * e.x, ey = ce * h.y + se * e.y;
+                ace.x += ex * w.x - ey * w.y;
+                ace.y += ex * w.y + ey * w.x;
+            }
         }
         const float2 hf = make_float2((float)acc.x, (float)acc.y);
-        Hs[i] = hf;
+        Hs[i] = Herr ? make_float2((float)ace.x, (float)ace.y) : hf;
         const int u = i / B, b = i % B;
         if (b >= b0 && b < b0 + B_loc) hfd[((size_t)u * B_loc + (b - b0)) * N_d + j] = hf;
     }
@@ -180,7 +190,16 @@ size_t zf_workspace_bytes(int N_d) { return N_d > 0 ? sizeof(double) * (size_t)N
 int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N_d, float rho, int b0, int B_loc,
                       void* h_fd, void* P, float* alpha, void* workspace, size_t workspace_bytes,
                       cudaStream_t stream) {
+    return zf_precoder_build_ex(h_taps, nullptr, 0.f, T, U, B, N_ifft, N_d, rho, b0, B_loc, h_fd, P, alpha, workspace,
+                                workspace_bytes, stream);
+}
+
+int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T, int U, int B, int N_ifft, int N_d,
+                         float rho, int b0, int B_loc, void* h_fd, void* P, float* alpha, void* workspace,
+                         size_t workspace_bytes, cudaStream_t stream) {
     FD_REQUIRE(h_taps && h_fd && P && alpha && workspace, "zf_precoder_build: NULL pointer");
+    FD_REQUIRE(eta >= 0.f && eta <= 1.f, "zf_precoder_build_ex: eta=%g outside [0,1]", (double)eta);
+    FD_REQUIRE(eta == 0.f || (h_err && aligned8(h_err)), "zf_precoder_build_ex: h_err required when eta > 0");
     FD_REQUIRE(aligned8(h_taps) && aligned8(h_fd) && aligned8(P) && aligned8(workspace),
                "zf_precoder_build: misaligned pointer");
     FD_REQUIRE(T >= 1 && T <= 4096, "T=%d outside [1,4096]", T);
@@ -198,7 +217,8 @@ int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N
     if (cudaMemsetAsync(flag, 0, sizeof(int), stream) != cudaSuccess) return check_launch("zf memset");
     cudaFuncSetAttribute(k_zf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_zf<<<N_d, 256, smem, stream>>>((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc, (float2*)h_fd,
-                                     (float2*)P, tr, flag);
+                                     (float2*)P, tr, flag, eta > 0.f ? (const float2*)h_err : nullptr,
+                                     (double)eta);
     int rc = check_launch("zf_precoder_build");
     if (rc) return rc;
     k_zf_alpha<<<1, 256, 0, stream>>>(tr, N_d, (double)B * (double)N_ifft, (double)rho, dalpha);

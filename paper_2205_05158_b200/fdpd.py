@@ -33,6 +33,15 @@ class ChainDesc(C.Structure):
 
 _cp = C.POINTER(C.c_void_p)
 
+
+class Impairments(C.Structure):
+    """fd_impair (include/fdpd.h): PA clip + measurement noise, AWGN, imperfect CSI (NEXT f3)."""
+    _fields_ = [("clip", C.c_float), ("pa_noise_std", C.c_float), ("awgn_n0", C.c_float), ("csi_eta", C.c_float),
+                ("noise_key", C.c_ulonglong), ("sym0", C.c_longlong), ("b0", C.c_int), ("B_total", C.c_int)]
+
+
+_imp = C.POINTER(Impairments)
+
 # name -> (restype, argtypes), mirroring include/fdpd.h
 SIGNATURES = {
     "fd_last_error": (C.c_char_p, []),
@@ -55,6 +64,10 @@ SIGNATURES = {
     "ue_receive": (_i, [_vp, _vp, _vp, _vp, _sz, _ll, _i, _i, _i, _i, _i, _vp]),
     "ue_slice_ser": (_i, [_vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
     "ue_receive_ser": (_i, [_vp, _vp, _vp, _vp, _sz, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _i, _f, _vp]),
+    "chain_txrx_ex": (_i, [_vp, _vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _imp, _vp]),
+    "zf_precoder_build_ex": (_i, [_vp, _vp, _f, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, C.POINTER(C.c_float), _vp,
+                                  _sz, _vp]),
+    "ue_combine_ser_ex": (_i, [_vp, _vp, _vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _f, _imp, _vp]),
     "fd_chain_create": (_i, [_cp, C.POINTER(ChainDesc), _vp, _vp, _vp, _ll, _vp]),
     "fd_chain_alpha": (_f, [_vp]),
     "fd_chain_destroy": (None, [_vp]),
@@ -166,6 +179,27 @@ def zf_precoder_build(h_taps, N_ifft, N_d, rho, b0=0, B_loc=None):
     return h_fd, P, float(a.value)
 
 
+def zf_precoder_build_ex(h_taps, h_err, eta, N_ifft, N_d, rho, b0=0, B_loc=None):
+    """zf_precoder_build with imperfect CSI: precoder from sqrt(1-eta) H + sqrt(eta) H_err."""
+    _dev(h_taps, torch.complex64, "h_taps")
+    _dev(h_err, torch.complex64, "h_err")
+    T, U, B = h_taps.shape
+    B_loc = B - b0 if B_loc is None else B_loc
+    h_fd = torch.empty((U, B_loc, N_d), dtype=torch.complex64, device=h_taps.device)
+    P = torch.empty((B_loc, U, N_d), dtype=torch.complex64, device=h_taps.device)
+    ws = _ws(lib().zf_workspace_bytes(N_d), h_taps)
+    a = C.c_float(0.0)
+    _check(lib().zf_precoder_build_ex(_ptr(h_taps), _ptr(h_err), float(eta), T, U, B, N_ifft, N_d, float(rho), b0,
+                                      B_loc, _ptr(h_fd), _ptr(P), C.byref(a), _ptr(ws), ws.numel(),
+                                      _stream(h_taps)))
+    return h_fd, P, float(a.value)
+
+
+def make_impairments(clip=0.0, pa_noise_std=0.0, awgn_n0=0.0, csi_eta=0.0, noise_key=0, sym0=0, b0=0, B_total=0):
+    return Impairments(float(clip), float(pa_noise_std), float(awgn_n0), float(csi_eta), int(noise_key), int(sym0),
+                       int(b0), int(B_total))
+
+
 # ----------------------------------------------------------------------------- a3-a5
 def precode(P, s, out=None):
     _dev(P, torch.complex64, "P")
@@ -205,6 +239,38 @@ def chain_tx(P, s_tilde, coef, orders, L, M, N_ifft, out=None):
     _check(lib().chain_tx(_ptr(P), _ptr(s_tilde), _ptr(coef), _ptr(out), _ints(orders), len(orders), L, M,
                           n_sym, B, U, N_d, N_ifft, _stream(P)))
     return out
+
+
+def chain_txrx_ex(P, s_tilde, coef, orders, L, M, N_ifft, imp, y=None, XPA=None):
+    """chain_txrx with PA clip + measurement noise (imp: Impairments)."""
+    _dev(P, torch.complex64, "P")
+    _dev(s_tilde, torch.complex64, "s_tilde")
+    _dev(coef, torch.complex64, "coef")
+    B, U, N_d = P.shape
+    n_sym = s_tilde.shape[0]
+    if y is None:
+        y = torch.empty((n_sym, B, N_ifft), dtype=torch.complex64, device=P.device)
+    if XPA is None:
+        XPA = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=P.device)
+    _check(lib().chain_txrx_ex(_ptr(P), _ptr(s_tilde), _ptr(coef), _ptr(y), _ptr(XPA), _ints(orders), len(orders),
+                               L, M, n_sym, B, U, N_d, N_ifft, C.byref(imp), _stream(P)))
+    return y, XPA
+
+
+def ue_combine_ser_ex(XPA, h_fd, alpha, tx_idx, M_qam, imp, yhat=None, counts=None, dec=None, boundary_eps=1e-4):
+    """ue_combine_ser with AWGN at the UEs (imp.awgn_n0)."""
+    _dev(XPA, torch.complex64, "XPA")
+    _dev(h_fd, torch.complex64, "h_fd")
+    _dev(tx_idx, torch.uint16, "tx_idx")
+    n_sym, B, N_d = XPA.shape
+    U = h_fd.shape[0]
+    if yhat is None:
+        yhat = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=XPA.device)
+    if counts is None:
+        counts = torch.zeros(3, dtype=torch.int64, device=XPA.device)
+    _check(lib().ue_combine_ser_ex(_ptr(XPA), _ptr(h_fd), _ptr(yhat), float(alpha), _ptr(tx_idx), M_qam, _ptr(dec),
+                                   _ptr(counts), n_sym, B, U, N_d, float(boundary_eps), C.byref(imp), _stream(XPA)))
+    return yhat, counts, dec
 
 
 def chain_txrx(P, s_tilde, coef, orders, L, M, N_ifft, y=None, XPA=None):
