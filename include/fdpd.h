@@ -184,6 +184,31 @@ int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T
                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
 /* -------------------------------------------------------------------------
+ * Per-symbol channel redraw ("block-constant with a coherence time of
+ * one OFDM symbol"): one channel realisation per symbol, so the ZF build joins the hot
+ * path.  Shapes gain a leading per-realisation dimension n_ch (= n_sym of the batch).
+ *
+ * zf_precoder_build_batched: n_ch independent zf_precoder_build's (one alpha each, A12),
+ *  fully asynchronous.  h_taps [n_ch][T][U][B]; h_fd out [n_ch][U][B_loc][N_d]; P out
+ *  [n_ch][B_loc][U][N_d]; alpha DEVICE float out [n_ch]; status DEVICE int (nullable) set
+ *  non-zero when some Gram matrix is not positive definite; workspace >=
+ *  zf_batched_workspace_bytes(n_ch, N_d); n_ch <= 65535.
+ * chain_txrx_ps: chain_txrx with symbol n of the batch precoded by P_all[n] ([n_sym][B_loc][U][N_d]).
+ * ue_combine_ser_ps: ue_combine_ser with h_fd_all[n] ([n_sym][U][B_loc][N_d]) and alpha_dev[n].
+ * ------------------------------------------------------------------------- */
+size_t zf_batched_workspace_bytes(int n_ch, int N_d);
+int zf_precoder_build_batched(const void* h_taps, int n_ch, int T, int U, int B, int N_ifft, int N_d, float rho,
+                              int b0, int B_loc, void* h_fd, void* P, float* alpha, int* status,
+                              void* workspace, size_t workspace_bytes, cudaStream_t stream);
+int chain_txrx_ps(const void* P_all, const void* s_tilde, const void* coef, void* y, void* XPA,
+                  const int* orders, int n_orders, int L, int M,
+                  long long n_sym, int B_loc, int U, int N_d, int N_ifft, const fd_impair* imp,
+                  cudaStream_t stream);
+int ue_combine_ser_ps(const void* XPA, const void* h_fd_all, void* yhat, const float* alpha_dev,
+                      const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts, long long n_sym,
+                      int B_loc, int U, int N_d, float boundary_eps, const fd_impair* imp, cudaStream_t stream);
+
+/* -------------------------------------------------------------------------
  * a6. Evaluation — Eqs. (4)-(5) P:67-77 (noiseless, reading A11), SER P:351.
  *
  * ue_receive: XPA[n][b][j] = N^-1/2 sum_m y[n][b][m] exp(-j 2 pi k_j m / N);

@@ -366,6 +366,24 @@ def run_chain(s, idx, h_taps, coef, params, *, chans, orders, L, M, N_ifft, M_qa
     return out
 
 
+def run_config_redraw(cfg, inp, h_taps_per_symbol):
+    """Per-symbol channel redraw ("coherence time of one OFDM symbol"; NEXT f4): symbol n uses
+    its own taps, hence its own Hfd_n, P_n and alpha_n (A12 per realisation).  Stage outputs are
+    stacked over symbols; alpha is the per-symbol vector; counts are summed."""
+    outs = []
+    for i, n in enumerate(inp["symbols"]):
+        sub = dict(inp)
+        sub.update(s=inp["s"][i:i + 1], idx=inp["idx"][i:i + 1], symbols=np.array([n]),
+                   h_taps=h_taps_per_symbol[i])
+        outs.append(run_config(cfg, sub))
+    res = {k: np.concatenate([o[k] for o in outs]) for k in ("s_tilde", "x", "y", "yhat", "dec")}
+    res["P"] = np.stack([o["P"] for o in outs])
+    res["Hfd"] = np.stack([o["Hfd"] for o in outs])
+    res["alpha"] = np.array([o["alpha"] for o in outs])
+    res["counts"] = np.sum([o["counts"] for o in outs], axis=0)
+    return res
+
+
 def run_config(cfg, inp):
     """run_chain with a workload.configs.ChainConfig and a workload.gen.make_inputs bundle."""
     return run_chain(inp["s"], inp["idx"], inp["h_taps"], inp["coef"], inp["params"],

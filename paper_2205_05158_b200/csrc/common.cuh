@@ -102,6 +102,10 @@ struct Impair {
     unsigned key_lo, key_hi;
     long long sym0;        // global index of the batch's first symbol
     int b0, B_total;       // antenna rows of this call within the full array
+    // per-symbol channel redraw (NEXT f4): element strides of per-symbol P / h_fd (0 = one
+    // realisation for the whole batch) and per-symbol alpha (device, NULL = scalar)
+    long long p_stride, h_stride;
+    const float* alpha_dev;
 };
 constexpr unsigned STREAM_PA_NOISE = 1, STREAM_AWGN = 2;
 

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
 // ============================================================================ slicer
 struct SliceParams {
     float inv_ac;   // 1 / (alpha * c): yhat -> level units
+    float inv_c;    // 1 / c (per-symbol alpha: inv_ac = inv_c / alpha_n)
     float thr;      // boundary_eps / c in level units
     int m;          // sqrt(M_qam)
 };
@@ -80,40 +81,88 @@ __global__ void k_slice(const float2* __restrict__ yhat, const uint16_t* __restr
 }
 
 // ============================================================================ channel sum (+ slicing)
-// yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j].  Thread per (n, j), loop over u and b.
-template <bool SER, bool AWGN = false>
+// yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j]     (Eq. 5)
+// Thread per (subcarrier j, NB consecutive symbols): users in chunks of UC, so each XPA load
+// feeds UC complex MACs and each h_fd load feeds NB (one realisation for the batch; with
+// per-symbol channels, NB = 1).  Consecutive threads = consecutive j: coalesced loads.
+constexpr int RX_UC = 4;
+template <bool SER, bool AWGN, int NB>
 __global__ void __launch_bounds__(128) k_rx_combine(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
-                                                    float2* __restrict__ yhat, int B, int U, int N_d, int accumulate,
-                                                    const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
-                                                    long long* counts, SliceParams sp, Impair imp) {
+                                                    float2* __restrict__ yhat, int B, int U, int N_d, int n_sym,
+                                                    int accumulate, const uint16_t* __restrict__ idx,
+                                                    uint16_t* __restrict__ dec, long long* counts, SliceParams sp,
+                                                    Impair imp) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t n = blockIdx.y;
+    const int n0 = blockIdx.y * NB;
     int err = 0, near = 0, cnt = 0;
     if (j < N_d) {
-        const float2* X = XPA + n * B * N_d + j;
-        for (int u = 0; u < U; ++u) {
-            const float2* h = hfd + (size_t)u * B * N_d + j;
-            float2 acc = make_float2(0.f, 0.f);
-            for (int b = 0; b < B; ++b) acc = cfma(__ldg(h + (size_t)b * N_d), __ldg(X + (size_t)b * N_d), acc);
-            const size_t o = (n * U + u) * N_d + j;
-            if (accumulate) acc = cadd(acc, yhat[o]);
-            if constexpr (AWGN)   // AWGN at the UEs, NEXT f3
-                acc = cadd(acc, cgauss((unsigned long long)((imp.sym0 + (long long)n) * U + u) * N_d + j, STREAM_AWGN,
-                                       imp.key_lo, imp.key_hi, imp.awgn_std));
-            yhat[o] = acc;
-            if (SER) {
-                bool nr = false;
-                const int di = slice_axis(acc.x * sp.inv_ac, sp, nr);
-                const int dq = slice_axis(acc.y * sp.inv_ac, sp, nr);
-                const int dd = di + sp.m * dq;
-                if (dec) dec[o] = (uint16_t)dd;
-                err += (dd != (int)idx[o]);
-                near += nr;
-                ++cnt;
+        for (int u0 = 0; u0 < U; u0 += RX_UC) {
+            float2 acc[NB][RX_UC];
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+#pragma unroll
+                for (int uu = 0; uu < RX_UC; ++uu) acc[i][uu] = make_float2(0.f, 0.f);
+            const float2* h0 = hfd + (size_t)n0 * imp.h_stride + (size_t)u0 * B * N_d + j;
+            for (int b = 0; b < B; ++b) {
+                float2 x[NB], h[RX_UC];
+#pragma unroll
+                for (int i = 0; i < NB; ++i)
+                    x[i] = (n0 + i < n_sym) ? __ldg(XPA + ((size_t)(n0 + i) * B + b) * N_d + j) : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int uu = 0; uu < RX_UC; ++uu)
+                    h[uu] = (u0 + uu < U) ? __ldg(h0 + ((size_t)uu * B + b) * N_d) : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < NB; ++i)
+#pragma unroll
+                    for (int uu = 0; uu < RX_UC; ++uu) acc[i][uu] = cfma(h[uu], x[i], acc[i][uu]);
+            }
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const int n = n0 + i;
+                if (n >= n_sym) continue;
+#pragma unroll
+                for (int uu = 0; uu < RX_UC; ++uu) {
+                    const int u = u0 + uu;
+                    if (u >= U) continue;
+                    float2 a = acc[i][uu];
+                    const size_t o = ((size_t)n * U + u) * N_d + j;
+                    if (accumulate) a = cadd(a, yhat[o]);
+                    if constexpr (AWGN)   // AWGN at the UEs, NEXT f3
+                        a = cadd(a, cgauss((unsigned long long)((imp.sym0 + (long long)n) * U + u) * N_d + j,
+                                           STREAM_AWGN, imp.key_lo, imp.key_hi, imp.awgn_std));
+                    yhat[o] = a;
+                    if constexpr (SER) {
+                        bool nr = false;
+                        const float inv = imp.alpha_dev ? sp.inv_c / imp.alpha_dev[n] : sp.inv_ac;
+                        const int di = slice_axis(a.x * inv, sp, nr);
+                        const int dq = slice_axis(a.y * inv, sp, nr);
+                        const int dd = di + sp.m * dq;
+                        if (dec) dec[o] = (uint16_t)dd;
+                        err += (dd != (int)idx[o]);
+                        near += nr;
+                        ++cnt;
+                    }
+                }
             }
         }
     }
     if (SER) add_counts(counts, err, near, cnt);
+}
+
+// Launch helper: NB = 4 symbols per thread with a batch-wide channel, 1 with per-symbol channels.
+template <bool SER, bool AWGN>
+static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d, long long n_sym,
+                           int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
+                           const SliceParams& sp, const Impair& imp, cudaStream_t st) {
+    if (imp.h_stride == 0) {
+        dim3 grid((N_d + 127) / 128, (unsigned)((n_sym + 3) / 4));
+        k_rx_combine<SER, AWGN, 4><<<grid, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, (int)n_sym, accumulate, idx, dec,
+                                                         counts, sp, imp);
+    } else {
+        dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
+        k_rx_combine<SER, AWGN, 1><<<grid, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, (int)n_sym, accumulate, idx, dec,
+                                                         counts, sp, imp);
+    }
 }
 
 // ============================================================================ host side
@@ -126,6 +175,7 @@ static int validate_slice(int M_qam, float alpha, float eps, SliceParams& sp) {
     const double c = 1.0 / std::sqrt(2.0 * (M_qam - 1) / 3.0);
     sp.m = m;
     sp.inv_ac = (float)(1.0 / ((double)alpha * c));
+    sp.inv_c = (float)(1.0 / c);
     sp.thr = (float)((double)eps / c);
     return FD_OK;
 }
@@ -194,9 +244,7 @@ int ue_receive(const void* y, const void* h_fd, void* yhat, void* workspace, siz
     float2* XPA = (float2*)workspace;
     rc = rx_fft((const float2*)y, XPA, n_sym, B_loc, N_d, N_ifft, stream);
     if (rc) return rc;
-    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
-    k_rx_combine<false><<<grid, 128, 0, stream>>>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, accumulate,
-                                                 nullptr, nullptr, nullptr, SliceParams{}, Impair{});
+    launch_combine<false, false>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, accumulate, nullptr, nullptr, nullptr, SliceParams{}, Impair{}, stream);
     return check_launch("ue_receive (combine)");
 }
 
@@ -228,9 +276,7 @@ int ue_receive_ser(const void* y, const void* h_fd, void* yhat, void* workspace,
     float2* XPA = (float2*)workspace;
     rc = rx_fft((const float2*)y, XPA, n_sym, B_loc, N_d, N_ifft, stream);
     if (rc) return rc;
-    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
-    k_rx_combine<true><<<grid, 128, 0, stream>>>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, 0, tx_idx,
-                                                dec, counts, sp, Impair{});
+    launch_combine<true, false>(XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, 0, tx_idx, dec, counts, sp, Impair{}, stream);
     return check_launch("ue_receive_ser (combine)");
 }
 
@@ -244,9 +290,7 @@ int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, i
     if (n_sym == 0) return FD_OK;
     FD_REQUIRE(XPA && h_fd && yhat, "ue_combine: NULL pointer");
     FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat), "ue_combine: misaligned pointer");
-    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
-    k_rx_combine<false><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U,
-                                                 N_d, accumulate, nullptr, nullptr, nullptr, SliceParams{}, Impair{});
+    launch_combine<false, false>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, accumulate, nullptr, nullptr, nullptr, SliceParams{}, Impair{}, stream);
     return check_launch("ue_combine");
 }
 
@@ -261,9 +305,7 @@ int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, c
     FD_REQUIRE(XPA && h_fd && yhat && tx_idx && counts, "ue_combine_ser: NULL pointer");
     FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat) && aligned8(counts),
                "ue_combine_ser: misaligned pointer");
-    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
-    k_rx_combine<true><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U,
-                                                N_d, 0, tx_idx, dec, counts, sp, Impair{});
+    launch_combine<true, false>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, 0, tx_idx, dec, counts, sp, Impair{}, stream);
     return check_launch("ue_combine_ser");
 }
 
@@ -286,14 +328,39 @@ int ue_combine_ser_ex(const void* XPA, const void* h_fd, void* yhat, float alpha
         im.key_hi = (unsigned)(imp->noise_key >> 32);
         im.sym0 = imp->sym0;
     }
-    dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
     if (im.awgn_std > 0.f)
-        k_rx_combine<true, true><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat,
-                                                          B_loc, U, N_d, 0, tx_idx, dec, counts, sp, im);
+        launch_combine<true, true>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, 0, tx_idx, dec, counts, sp, im, stream);
     else
-        k_rx_combine<true, false><<<grid, 128, 0, stream>>>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat,
-                                                           B_loc, U, N_d, 0, tx_idx, dec, counts, sp, im);
+        launch_combine<true, false>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, 0, tx_idx, dec, counts, sp, im, stream);
     return check_launch("ue_combine_ser_ex");
+}
+
+int ue_combine_ser_ps(const void* XPA, const void* h_fd_all, void* yhat, const float* alpha_dev,
+                      const uint16_t* tx_idx, int M_qam, uint16_t* dec, long long* counts, long long n_sym, int B_loc,
+                      int U, int N_d, float boundary_eps, const fd_impair* imp, cudaStream_t stream) {
+    FD_REQUIRE(n_sym >= 0 && n_sym <= 65535 && B_loc >= 1 && U >= 1 && N_d >= 1, "ue_combine_ser_ps: bad sizes");
+    FD_REQUIRE(!imp || imp->awgn_n0 >= 0.f, "ue_combine_ser_ps: awgn_n0 < 0");
+    SliceParams sp;
+    int rc = validate_slice(M_qam, 1.f, boundary_eps, sp);
+    if (rc) return rc;
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(XPA && h_fd_all && yhat && alpha_dev && tx_idx && counts, "ue_combine_ser_ps: NULL pointer");
+    FD_REQUIRE(aligned8(XPA) && aligned8(h_fd_all) && aligned8(yhat) && aligned8(counts),
+               "ue_combine_ser_ps: misaligned pointer");
+    Impair im{};
+    if (imp) {
+        im.awgn_std = imp->awgn_n0 > 0.f ? sqrtf(imp->awgn_n0) : 0.f;
+        im.key_lo = (unsigned)(imp->noise_key & 0xffffffffull);
+        im.key_hi = (unsigned)(imp->noise_key >> 32);
+        im.sym0 = imp->sym0;
+    }
+    im.h_stride = (long long)U * B_loc * N_d;
+    im.alpha_dev = alpha_dev;
+    if (im.awgn_std > 0.f)
+        launch_combine<true, true>((const float2*)XPA, (const float2*)h_fd_all, (float2*)yhat, B_loc, U, N_d, n_sym, 0, tx_idx, dec, counts, sp, im, stream);
+    else
+        launch_combine<true, false>((const float2*)XPA, (const float2*)h_fd_all, (float2*)yhat, B_loc, U, N_d, n_sym, 0, tx_idx, dec, counts, sp, im, stream);
+    return check_launch("ue_combine_ser_ps");
 }
 
 }  // extern "C"

@@ -30,6 +30,14 @@ __global__ void __launch_bounds__(256) k_zf(const float2* __restrict__ H, int T,
     double2* Li = Lm + U * U;                                  // [U][U]  inverse of L
     double2* tw = Li + U * U;                                  // [T]
     float2* Hs = reinterpret_cast<float2*>(tw + T);            // [U][B]
+    // batched builds (per-symbol channel redraw, NEXT f4): channel realisation blockIdx.y
+    {
+        const size_t c = blockIdx.y;
+        H += c * T * U * B;
+        hfd += c * (size_t)U * B_loc * N_d;
+        P += c * (size_t)B_loc * U * N_d;
+        tr += c * N_d;
+    }
     const int j = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
     const int k = data_to_bin(j, N, N_d);
@@ -156,23 +164,31 @@ __global__ void __launch_bounds__(256) k_zf(const float2* __restrict__ H, int T,
     }
 }
 
-__global__ void k_zf_alpha(const double* __restrict__ tr, int N_d, double scale, double rho, double* alpha) {
+// One CTA per channel realisation c: fixed-order fp64 sum of tr_j, alpha_c (A12); also a
+// float copy for the slicer when alpha_f != NULL.
+__global__ void k_zf_alpha(const double* __restrict__ tr, int N_d, double scale, double rho, double* alpha,
+                           float* alpha_f) {
     __shared__ double part[256];
+    const int c = blockIdx.x;
     double s = 0.0;
-    for (int j = threadIdx.x; j < N_d; j += blockDim.x) s += tr[j];
+    for (int j = threadIdx.x; j < N_d; j += blockDim.x) s += tr[(size_t)c * N_d + j];
     part[threadIdx.x] = s;
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) alpha[0] = rho * sqrt(scale / part[0]);
+    if (threadIdx.x == 0) {
+        alpha[c] = rho * sqrt(scale / part[0]);
+        if (alpha_f) alpha_f[c] = (float)alpha[c];
+    }
 }
 
-__global__ void k_scale(float2* __restrict__ P, long long n, const double* __restrict__ alpha) {
-    const float a = (float)alpha[0];
+// P_c *= alpha_c for the n_ch realisations of `per` complex entries each
+__global__ void k_scale(float2* __restrict__ P, long long per, int n_ch, const double* __restrict__ alpha) {
+    const long long n = per * n_ch;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        P[i] = cscale(P[i], a);
+        P[i] = cscale(P[i], (float)alpha[i / per]);
 }
 
 static size_t zf_smem(int T, int U, int B) {
@@ -187,6 +203,26 @@ extern "C" {
 
 size_t zf_workspace_bytes(int N_d) { return N_d > 0 ? sizeof(double) * (size_t)N_d + 16 : 0; }
 
+size_t zf_batched_workspace_bytes(int n_ch, int N_d) {
+    return (n_ch > 0 && N_d > 0) ? sizeof(double) * ((size_t)n_ch * N_d + n_ch) + 16 : 0;
+}
+
+static int zf_validate(const void* h_taps, const void* h_fd, const void* P, const void* workspace, int T, int U, int B,
+                       int N_ifft, int N_d, float rho, int b0, int B_loc, size_t& smem) {
+    FD_REQUIRE(h_taps && h_fd && P && workspace, "zf_precoder_build: NULL pointer");
+    FD_REQUIRE(aligned8(h_taps) && aligned8(h_fd) && aligned8(P) && aligned8(workspace),
+               "zf_precoder_build: misaligned pointer");
+    FD_REQUIRE(T >= 1 && T <= 4096, "T=%d outside [1,4096]", T);
+    FD_REQUIRE(U >= 1 && U <= 64 && U <= B, "U=%d must be in [1, min(64, B)]", U);
+    FD_REQUIRE(is_pow2(N_ifft) && N_ifft <= (1 << 24), "N_ifft=%d must be a power of two", N_ifft);
+    FD_REQUIRE(N_d >= 2 && N_d % 2 == 0 && N_d <= N_ifft, "N_d=%d must be even and <= N_ifft", N_d);
+    FD_REQUIRE(b0 >= 0 && B_loc >= 1 && b0 + B_loc <= B, "antenna range [%d,%d) outside [0,%d)", b0, b0 + B_loc, B);
+    FD_REQUIRE(rho > 0.f, "rho must be > 0");
+    smem = zf_smem(T, U, B);
+    FD_REQUIRE(smem <= 227 * 1024, "U*B too large for one CTA (%zu bytes of shared memory)", smem);
+    return FD_OK;
+}
+
 int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N_d, float rho, int b0, int B_loc,
                       void* h_fd, void* P, float* alpha, void* workspace, size_t workspace_bytes,
                       cudaStream_t stream) {
@@ -197,20 +233,13 @@ int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N
 int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T, int U, int B, int N_ifft, int N_d,
                          float rho, int b0, int B_loc, void* h_fd, void* P, float* alpha, void* workspace,
                          size_t workspace_bytes, cudaStream_t stream) {
-    FD_REQUIRE(h_taps && h_fd && P && alpha && workspace, "zf_precoder_build: NULL pointer");
+    FD_REQUIRE(alpha, "zf_precoder_build: NULL alpha");
     FD_REQUIRE(eta >= 0.f && eta <= 1.f, "zf_precoder_build_ex: eta=%g outside [0,1]", (double)eta);
     FD_REQUIRE(eta == 0.f || (h_err && aligned8(h_err)), "zf_precoder_build_ex: h_err required when eta > 0");
-    FD_REQUIRE(aligned8(h_taps) && aligned8(h_fd) && aligned8(P) && aligned8(workspace),
-               "zf_precoder_build: misaligned pointer");
-    FD_REQUIRE(T >= 1 && T <= 4096, "T=%d outside [1,4096]", T);
-    FD_REQUIRE(U >= 1 && U <= 64 && U <= B, "U=%d must be in [1, min(64, B)]", U);
-    FD_REQUIRE(is_pow2(N_ifft) && N_ifft <= (1 << 24), "N_ifft=%d must be a power of two", N_ifft);
-    FD_REQUIRE(N_d >= 2 && N_d % 2 == 0 && N_d <= N_ifft, "N_d=%d must be even and <= N_ifft", N_d);
-    FD_REQUIRE(b0 >= 0 && B_loc >= 1 && b0 + B_loc <= B, "antenna range [%d,%d) outside [0,%d)", b0, b0 + B_loc, B);
-    FD_REQUIRE(rho > 0.f, "rho must be > 0");
+    size_t smem = 0;
+    int rc = zf_validate(h_taps, h_fd, P, workspace, T, U, B, N_ifft, N_d, rho, b0, B_loc, smem);
+    if (rc) return rc;
     FD_REQUIRE(workspace_bytes >= zf_workspace_bytes(N_d), "zf workspace too small");
-    const size_t smem = zf_smem(T, U, B);
-    FD_REQUIRE(smem <= 227 * 1024, "U*B too large for one CTA (%zu bytes of shared memory)", smem);
     double* tr = (double*)workspace;
     double* dalpha = tr + N_d;
     int* flag = (int*)(dalpha + 1);
@@ -219,11 +248,11 @@ int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T
     k_zf<<<N_d, 256, smem, stream>>>((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc, (float2*)h_fd,
                                      (float2*)P, tr, flag, eta > 0.f ? (const float2*)h_err : nullptr,
                                      (double)eta);
-    int rc = check_launch("zf_precoder_build");
+    rc = check_launch("zf_precoder_build");
     if (rc) return rc;
-    k_zf_alpha<<<1, 256, 0, stream>>>(tr, N_d, (double)B * (double)N_ifft, (double)rho, dalpha);
+    k_zf_alpha<<<1, 256, 0, stream>>>(tr, N_d, (double)B * (double)N_ifft, (double)rho, dalpha, nullptr);
     const long long nP = (long long)B_loc * U * N_d;
-    k_scale<<<(int)std::min<long long>((nP + 255) / 256, 148LL * 8), 256, 0, stream>>>((float2*)P, nP, dalpha);
+    k_scale<<<(int)std::min<long long>((nP + 255) / 256, 148LL * 8), 256, 0, stream>>>((float2*)P, nP, 1, dalpha);
     rc = check_launch("zf_precoder_build (alpha)");
     if (rc) return rc;
     double a = 0.0;
@@ -238,6 +267,32 @@ int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T
     }
     *alpha = (float)a;
     return FD_OK;
+}
+
+int zf_precoder_build_batched(const void* h_taps, int n_ch, int T, int U, int B, int N_ifft, int N_d, float rho,
+                              int b0, int B_loc, void* h_fd, void* P, float* alpha, int* status, void* workspace,
+                              size_t workspace_bytes, cudaStream_t stream) {
+    FD_REQUIRE(n_ch >= 0 && n_ch <= 65535, "zf_precoder_build_batched: n_ch=%d outside [0,65535]", n_ch);
+    if (n_ch == 0) return FD_OK;
+    FD_REQUIRE(alpha != nullptr, "zf_precoder_build_batched: NULL alpha");
+    size_t smem = 0;
+    int rc = zf_validate(h_taps, h_fd, P, workspace, T, U, B, N_ifft, N_d, rho, b0, B_loc, smem);
+    if (rc) return rc;
+    FD_REQUIRE(workspace_bytes >= zf_batched_workspace_bytes(n_ch, N_d), "zf batched workspace too small");
+    double* tr = (double*)workspace;
+    double* dalpha = tr + (size_t)n_ch * N_d;
+    int* flag = status ? status : (int*)(dalpha + n_ch);
+    if (cudaMemsetAsync(flag, 0, sizeof(int), stream) != cudaSuccess) return check_launch("zf memset");
+    cudaFuncSetAttribute(k_zf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_zf<<<dim3(N_d, n_ch), 256, smem, stream>>>((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc,
+                                                 (float2*)h_fd, (float2*)P, tr, flag, nullptr, 0.0);
+    rc = check_launch("zf_precoder_build_batched");
+    if (rc) return rc;
+    k_zf_alpha<<<n_ch, 256, 0, stream>>>(tr, N_d, (double)B * (double)N_ifft, (double)rho, dalpha, alpha);
+    const long long per = (long long)B_loc * U * N_d;
+    k_scale<<<(int)std::min<long long>((per * n_ch + 255) / 256, 148LL * 16), 256, 0, stream>>>((float2*)P, per, n_ch,
+                                                                                               dalpha);
+    return check_launch("zf_precoder_build_batched (alpha)");
 }
 
 }  // extern "C"

@@ -68,6 +68,10 @@ SIGNATURES = {
     "zf_precoder_build_ex": (_i, [_vp, _vp, _f, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, C.POINTER(C.c_float), _vp,
                                   _sz, _vp]),
     "ue_combine_ser_ex": (_i, [_vp, _vp, _vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _f, _imp, _vp]),
+    "zf_batched_workspace_bytes": (_sz, [_i, _i]),
+    "zf_precoder_build_batched": (_i, [_vp, _i, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "chain_txrx_ps": (_i, [_vp, _vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _imp, _vp]),
+    "ue_combine_ser_ps": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _f, _imp, _vp]),
     "fd_chain_create": (_i, [_cp, C.POINTER(ChainDesc), _vp, _vp, _vp, _ll, _vp]),
     "fd_chain_alpha": (_f, [_vp]),
     "fd_chain_destroy": (None, [_vp]),
@@ -193,6 +197,59 @@ def zf_precoder_build_ex(h_taps, h_err, eta, N_ifft, N_d, rho, b0=0, B_loc=None)
                                       B_loc, _ptr(h_fd), _ptr(P), C.byref(a), _ptr(ws), ws.numel(),
                                       _stream(h_taps)))
     return h_fd, P, float(a.value)
+
+
+def zf_precoder_build_batched(h_taps_all, N_ifft, N_d, rho, out=None):
+    """Per-symbol channel redraw (NEXT f4): h_taps_all [n_ch][T][U][B] -> (h_fd_all, P_all,
+    alpha_dev [n_ch] float32 on the device, status int32 [1] on the device); asynchronous."""
+    _dev(h_taps_all, torch.complex64, "h_taps_all")
+    n_ch, T, U, B = h_taps_all.shape
+    dv = h_taps_all.device
+    if out is None:
+        out = (torch.empty((n_ch, U, B, N_d), dtype=torch.complex64, device=dv),
+               torch.empty((n_ch, B, U, N_d), dtype=torch.complex64, device=dv),
+               torch.empty(n_ch, dtype=torch.float32, device=dv),
+               torch.zeros(1, dtype=torch.int32, device=dv),
+               _ws(lib().zf_batched_workspace_bytes(n_ch, N_d), h_taps_all))
+    h_fd, P, alpha, status, ws = out
+    _check(lib().zf_precoder_build_batched(_ptr(h_taps_all), n_ch, T, U, B, N_ifft, N_d, float(rho), 0, B,
+                                           _ptr(h_fd), _ptr(P), _ptr(alpha), _ptr(status), _ptr(ws), ws.numel(),
+                                           _stream(h_taps_all)))
+    return out
+
+
+def chain_txrx_ps(P_all, s_tilde, coef, orders, L, M, N_ifft, imp=None, y=None, XPA=None):
+    """chain_txrx with per-symbol precoders P_all [n_sym][B_loc][U][N_d]."""
+    _dev(P_all, torch.complex64, "P_all")
+    _dev(s_tilde, torch.complex64, "s_tilde")
+    _dev(coef, torch.complex64, "coef")
+    n_sym, B, U, N_d = P_all.shape
+    if y is None:
+        y = torch.empty((n_sym, B, N_ifft), dtype=torch.complex64, device=P_all.device)
+    if XPA is None:
+        XPA = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=P_all.device)
+    _check(lib().chain_txrx_ps(_ptr(P_all), _ptr(s_tilde), _ptr(coef), _ptr(y), _ptr(XPA), _ints(orders),
+                               len(orders), L, M, n_sym, B, U, N_d, N_ifft, C.byref(imp) if imp else None,
+                               _stream(P_all)))
+    return y, XPA
+
+
+def ue_combine_ser_ps(XPA, h_fd_all, alpha_dev, tx_idx, M_qam, imp=None, yhat=None, counts=None, dec=None,
+                      boundary_eps=1e-4):
+    _dev(XPA, torch.complex64, "XPA")
+    _dev(h_fd_all, torch.complex64, "h_fd_all")
+    _dev(alpha_dev, torch.float32, "alpha_dev")
+    _dev(tx_idx, torch.uint16, "tx_idx")
+    n_sym, B, N_d = XPA.shape
+    U = h_fd_all.shape[1]
+    if yhat is None:
+        yhat = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=XPA.device)
+    if counts is None:
+        counts = torch.zeros(3, dtype=torch.int64, device=XPA.device)
+    _check(lib().ue_combine_ser_ps(_ptr(XPA), _ptr(h_fd_all), _ptr(yhat), _ptr(alpha_dev), _ptr(tx_idx), M_qam,
+                                   _ptr(dec), _ptr(counts), n_sym, B, U, N_d, float(boundary_eps),
+                                   C.byref(imp) if imp else None, _stream(XPA)))
+    return yhat, counts, dec
 
 
 def make_impairments(clip=0.0, pa_noise_std=0.0, awgn_n0=0.0, csi_eta=0.0, noise_key=0, sym0=0, b0=0, B_total=0):

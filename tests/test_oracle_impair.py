@@ -70,3 +70,22 @@ def test_awgn_qpsk_ser_closed_form():
     want = 2 * p - p * p
     ser = out["counts"][0] / out["counts"][1]
     assert abs(ser / want - 1) < 0.10
+
+
+def test_redraw_with_repeated_taps_equals_single_realisation():
+    """NEXT f4 oracle: per-symbol channels that all equal the run's channel reproduce run_config."""
+    cfg = configs.C1
+    inp = gen.make_inputs(cfg)
+    taps = np.repeat(inp["h_taps"][None], cfg.n_sym, axis=0)
+    a = O.run_config_redraw(cfg, inp, taps)
+    b = O.run_config(cfg, inp)
+    assert np.allclose(a["yhat"], b["yhat"], rtol=0, atol=1e-13) and np.array_equal(a["counts"], b["counts"])
+    assert np.allclose(a["alpha"], b["alpha"])
+
+
+def test_redraw_channels_differ_per_symbol():
+    cfg = configs.C2
+    t = gen.channel_taps_per_symbol(cfg, [0, 1, 0])
+    assert np.array_equal(t[0], t[2]) and not np.allclose(t[0], t[1])
+    p = np.mean(np.abs(gen.channel_taps_per_symbol(cfg, range(64)).astype(np.complex128)) ** 2, axis=(0, 2, 3))
+    assert abs(p.sum() - 1) < 0.03                       # PDP normalised per realisation on average

@@ -78,6 +78,17 @@ def channel_taps(cfg: ChainConfig) -> np.ndarray:
     return h.astype(np.complex64)
 
 
+def channel_taps_per_symbol(cfg: ChainConfig, symbols) -> np.ndarray:
+    """complex64 [n][T][U][B]: one Rayleigh realisation per OFDM symbol (block-constant over one
+    symbol; NEXT f4), substream index 1 + symbol (0 is the single-realisation channel)."""
+    out = np.empty((len(symbols), cfg.T, cfg.U, cfg.B), dtype=np.complex64)
+    sd = np.sqrt(pdp(cfg) / 2.0)[:, None, None]
+    for i, n in enumerate(symbols):
+        z = rng(cfg.seed, STREAM_CHANNEL, 1 + int(n)).standard_normal((cfg.T, cfg.U, cfg.B, 2))
+        out[i] = (z[..., 0] + 1j * z[..., 1]) * sd
+    return out
+
+
 def csi_error_taps(cfg: ChainConfig) -> np.ndarray:
     """complex64 [T][U][B] H^err ~ CN(0, I) per tap entry."""
     g = rng(cfg.seed, STREAM_CSI)
