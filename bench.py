@@ -205,8 +205,13 @@ def run_ours(args, cfg):
     symbols = D.symbol_range(n, rank)          # Mode S, weak scaling
     inp = gen.make_inputs(cfg, symbols)
 
+    impair = None
+    if args.impair:
+        impair = dict(clip=cfg.clip, pa_noise_std=cfg.pa_noise_std, awgn_n0=cfg.awgn_n0, csi_eta=cfg.csi_eta,
+                      noise_key=inp["noise_key"], h_err=inp["h_err"])
     t_zf0 = time.perf_counter()
-    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device=dev, max_batch=n)
+    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device=dev, max_batch=n,
+               impair=impair)
     torch.cuda.synchronize()
     t_zf = time.perf_counter() - t_zf0
     native = fdpd.NativeChain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], max_batch=n,
@@ -214,24 +219,30 @@ def run_ours(args, cfg):
 
     s = torch.from_numpy(inp["s"]).to(dev)
     idx = torch.from_numpy(inp["idx"]).to(dev)
+    taps_all = torch.from_numpy(gen.channel_taps_per_symbol(cfg, symbols)).to(dev) if args.redraw else None
     counts = torch.zeros(3, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    sym0 = symbols[0]
 
     def step(ev=None):
         st = ch.dpd(s)
         if ev is not None:
             ev[0].record(stream)
-        if args.unfused:
+        if args.redraw:
+            XPA = ch.redraw_txrx(st, taps_all, sym0)       # batched per-symbol ZF + chain_txrx_ps
+        elif args.unfused:
             y = ch.tx(st)
         else:
-            _, XPA = ch.txrx(st)
+            _, XPA = ch.txrx(st, sym0)
         if ev is not None:
             ev[1].record(stream)
-        if args.unfused:
+        if args.redraw:
+            ch.redraw_combine(XPA, idx, counts=counts, sym0=sym0)
+        elif args.unfused:
             ch.rx(y, idx, counts=counts)
         else:
-            ch.combine(XPA, idx, counts=counts)
+            ch.combine(XPA, idx, counts=counts, sym0=sym0)
         if ev is not None:
             ev[2].record(stream)
         if ws > 1:
@@ -264,12 +275,27 @@ def run_ours(args, cfg):
         i_h = torch.from_numpy(inp["idx"]).pin_memory()
         c_h = torch.zeros(3, dtype=torch.int64).pin_memory()
         e2e_ev = [(E(), E()) for _ in range(args.steps)]
+        # the C runtime covers the default chain; impairments / per-symbol channels run the same
+        # per-call path as the timed step, with the host copies added around it
+        use_native = not (args.impair or args.redraw or args.unfused)
+        s_d, i_d = torch.empty_like(s), torch.empty_like(idx)
         for i in range(args.steps):
             flush.zero_()
             e2e_ev[i][0].record(stream)
-            native.run_host(s_h, i_h, c_h)
-            if ws > 1:
-                D.allreduce_counts(c_h.to(dev))
+            if use_native:
+                native.run_host(s_h, i_h, c_h)
+                if ws > 1:
+                    D.allreduce_counts(c_h.to(dev))
+            else:
+                s_d.copy_(s_h, non_blocking=True)
+                i_d.copy_(i_h, non_blocking=True)
+                counts.zero_()
+                if args.redraw:
+                    ch.step_redraw(s_d, i_d, taps_all, counts=counts, sym0=sym0)
+                else:
+                    ch.step(s_d, i_d, counts=counts, sym0=sym0, fused=not args.unfused)
+                D.allreduce_counts(counts)
+                c_h.copy_(counts, non_blocking=True)
             e2e_ev[i][1].record(stream)
         torch.cuda.synchronize()
         if int(c_h[1]) != n * cfg.U * cfg.N_d:
@@ -295,7 +321,13 @@ def run_ours(args, cfg):
     achieved = tx_flop / (st_tx / 1e3) / 1e12
     bytes_sym = chain_bytes_per_symbol(cfg, fused=not args.unfused)
     hbm_achieved = bytes_sym * n * args.steps / (ms / 1e3) / 1e9
-    launches_per_step = (len(cfg.chans) - 1) + 1 + (2 if args.unfused else 1)
+    if cfg.head == "paper":
+        cnn_launches = 2                                   # conv + FC GEMM
+    elif fdpd.lib().fdcnn_workspace_bytes(fdpd._ints(cfg.chans), len(cfg.chans) - 1, n, cfg.U, cfg.N_d) == 0:
+        cnn_launches = 1                                   # whole network in shared memory
+    else:
+        cnn_launches = 2 * (len(cfg.chans) - 1)            # weight transpose + conv per layer
+    launches_per_step = cnn_launches + 1 + (2 if args.unfused else 1) + (3 if args.redraw else 0)
     if not args.unfused:                       # chain_txrx also runs the receive FFT
         tx_flop += 5 * cfg.N_ifft * int(np.log2(cfg.N_ifft)) * cfg.B * n
         achieved = tx_flop / (st_tx / 1e3) / 1e12
@@ -310,7 +342,9 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, workload/gen.py)",
-        "config": config_dict(cfg, ws, n),
+        "config": dict(config_dict(cfg, ws, n), impairments=bool(args.impair),
+                       channel=("per-symbol redraw, ZF in the step" if args.redraw else
+                                "one realisation per run, ZF before timing")),
         "roofline": {"kernel": ("chain_tx (precode+IDFT+GMP)" if args.unfused else
                                 "chain_txrx (precode+IDFT+GMP+receive DFT)"), "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
@@ -343,10 +377,16 @@ def main():
     ap.add_argument("--ref-step-symbols", type=int, default=4, help="oracle symbols per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="chain_tx + ue_receive_ser instead of chain_txrx")
+    ap.add_argument("--impair", action="store_true", help="PA clip + noise, AWGN, imperfect CSI (NEXT f3)")
+    ap.add_argument("--redraw", action="store_true", help="per-symbol channel redraw, ZF on the hot path (NEXT f4)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     cfg = configs.get(args.config)
+    if args.impair:
+        cfg = configs.impaired(cfg)
+    if (args.impair or args.redraw) and args.unfused:
+        ap.error("--impair/--redraw run on the fused path only")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

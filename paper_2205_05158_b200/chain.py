@@ -128,20 +128,31 @@ class Chain:
         """One step with per-symbol channel redraw (NEXT f4): the batched ZF build joins the
         hot path.  h_taps_all [n][T][U][B] on the device.
         fdcnn_forward -> zf_precoder_build_batched -> chain_txrx_ps -> ue_combine_ser_ps."""
-        n = s.shape[0]
+        if s.shape[0] > self.cap:
+            self.reserve(s.shape[0])
+        st = self.dpd(s)
+        XPA = self.redraw_txrx(st, h_taps_all, sym0)
+        return self.redraw_combine(XPA, tx_idx, counts=counts, dec=dec, sym0=sym0)
+
+    def redraw_txrx(self, s_tilde, h_taps_all, sym0=0):
+        """Batched per-symbol ZF build, then chain_txrx_ps."""
+        n = s_tilde.shape[0]
         sh = self.sh
-        if n > self.cap:
-            self.reserve(n)
         if getattr(self, "_zfb_n", None) != n:
             self._zfb = None
             self._zfb_n = n
-        st = self.dpd(s)
         self._zfb = fdpd.zf_precoder_build_batched(h_taps_all, sh.N_ifft, sh.N_d, sh.rho, out=self._zfb)
         self.h_fd_all, self.P_all, self.alpha_all, self.zf_status, _ = self._zfb
         imp = self._imp(sym0) if self.impair else None
         XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
-        fdpd.chain_txrx_ps(self.P_all, st, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, imp=imp, y=self.y[:n],
-                           XPA=XPA)
+        fdpd.chain_txrx_ps(self.P_all, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, imp=imp,
+                           y=self.y[:n], XPA=XPA)
+        return XPA
+
+    def redraw_combine(self, XPA, tx_idx, counts=None, dec=None, sym0=0):
+        n = XPA.shape[0]
+        sh = self.sh
+        imp = self._imp(sym0) if self.impair else None
         counts = self.counts if counts is None else counts
         return fdpd.ue_combine_ser_ps(XPA, self.h_fd_all, self.alpha_all, tx_idx, sh.M_qam, imp=imp,
                                       yhat=self.yhat[:n], counts=counts, dec=dec, boundary_eps=sh.eps)
