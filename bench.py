@@ -69,6 +69,17 @@ def chain_bytes_per_symbol(cfg, fused=True):
     return s + 2 * cfg.U * cfg.N_d + (1 if fused else 2) * y + s + (16 * cfg.B * cfg.U * cfg.N_d) / cfg.n_sym
 
 
+def measured_traffic(cfg, n, args):
+    """DRAM bytes per chain_txrx launch from the committed ncu --set full capture of this exact
+    launch configuration (profiles/traffic_<cfg>.json), else None."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{cfg.name.lower()}.json")
+    if args.unfused or args.impair or args.redraw or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        t = json.load(f).get("chain_txrx")
+    return t["bytes_per_launch"] if t and t.get("batch") == n else None
+
+
 # ============================================================================ clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -347,7 +358,8 @@ def run_ours(args, cfg):
                                 "one realisation per run, ZF before timing")),
         "roofline": {"kernel": ("chain_tx (precode+IDFT+GMP)" if args.unfused else
                                 "chain_txrx (precode+IDFT+GMP+receive DFT)"), "bound": "alu", "achieved": achieved,
-                     "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                     "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                     "traffic": measured_traffic(cfg, n, args),
                      "peak_src": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
                      "flop_per_symbol": tx_flop / n, "ms_per_launch": st_tx},
         "hbm": {"algorithmic_bytes_per_symbol": bytes_sym, "achieved_GBps": hbm_achieved, "peak_GBps": pk["hbm_gbs"],
