@@ -225,6 +225,7 @@ def run_ours(args, cfg):
                impair=impair)
     torch.cuda.synchronize()
     t_zf = time.perf_counter() - t_zf0
+    ch.split_precode = args.split_precode
     native = fdpd.NativeChain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], max_batch=n,
                               device=dev)
 
@@ -391,6 +392,7 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="chain_tx + ue_receive_ser instead of chain_txrx")
     ap.add_argument("--impair", action="store_true", help="PA clip + noise, AWGN, imperfect CSI (NEXT f3)")
     ap.add_argument("--redraw", action="store_true", help="per-symbol channel redraw, ZF on the hot path (NEXT f4)")
+    ap.add_argument("--split-precode", action="store_true", help="precode kernel + chain_txrx_pre")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

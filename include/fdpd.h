@@ -176,6 +176,12 @@ int chain_txrx_ex(const void* P, const void* s_tilde, const void* coef, void* y,
                   const int* orders, int n_orders, int L, int M,
                   long long n_sym, int B_loc, int U, int N_d, int N_ifft, const fd_impair* imp,
                   cudaStream_t stream);
+/* chain_txrx on an already precoded spectrum X [n_sym][B_loc][N_d] (the output of precode):
+ * the split precode -> chain_txrx_pre moves the U-fold L2 gather of P_b and s_n out of the
+ * fused kernel's prologue into one bandwidth-bound kernel.  imp nullable. */
+int chain_txrx_pre(const void* X, const void* coef, void* y, void* XPA, const int* orders, int n_orders,
+                   int L, int M, long long n_sym, int B_loc, int N_d, int N_ifft, const fd_impair* imp,
+                   cudaStream_t stream);
 /* zf_precoder_build with imperfect CSI: the precoder is built from
  * H_est = sqrt(1 - eta) H + sqrt(eta) H_err while h_fd (the channel the UEs see) is
  * built from H.  h_err device complex64 [T][U][B]; eta in [0, 1]. */

@@ -109,6 +109,14 @@ class Chain:
         n = s_tilde.shape[0]
         sh = self.sh
         XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
+        if getattr(self, "split_precode", False):
+            # precode as its own bandwidth-bound kernel, then the fused chain on X
+            if getattr(self, "X", None) is None or self.X.shape[0] < n:
+                self.X = torch.empty((max(n, self.cap), self.B_loc, sh.N_d), dtype=torch.complex64,
+                                     device=self.device)
+            X = fdpd.precode(self.P, s_tilde, out=self.X[:n])
+            return fdpd.chain_txrx_pre(X, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft,
+                                       imp=self._imp(sym0) if self.impair else None, y=self.y[:n], XPA=XPA)
         if self.impair:
             return fdpd.chain_txrx_ex(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, self._imp(sym0),
                                       y=self.y[:n], XPA=XPA)

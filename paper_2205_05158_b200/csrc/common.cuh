@@ -106,6 +106,7 @@ struct Impair {
     // realisation for the whole batch) and per-symbol alpha (device, NULL = scalar)
     long long p_stride, h_stride;
     const float* alpha_dev;
+    int precoded;          // chain kernels: P is the precoded spectrum X [n_sym][B][N_d]
 };
 constexpr unsigned STREAM_PA_NOISE = 1, STREAM_AWGN = 2;
 

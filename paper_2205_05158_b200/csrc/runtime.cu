@@ -24,6 +24,10 @@ struct fd_chain {
     void* ws_cnn = nullptr;
     size_t ws_cnn_bytes = 0;
     void* ws_zf = nullptr;
+    // host-input pipelining: a copy stream and per-chunk events (fd_chain_run_host)
+    cudaStream_t copy_stream = nullptr;
+    static constexpr int kChunks = 4;
+    cudaEvent_t ev_in[kChunks] = {}, ev_free = nullptr;
 };
 
 namespace {
@@ -44,6 +48,10 @@ void release(fd_chain* c) {
                     c->XPA, c->yhat, c->idx, c->counts, c->ws_cnn, c->ws_zf};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (cudaEvent_t e : c->ev_in)
+        if (e) cudaEventDestroy(e);
+    if (c->ev_free) cudaEventDestroy(c->ev_free);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
 
@@ -68,6 +76,26 @@ int ensure_batch(fd_chain* c, long long n) {
     if (c->ws_cnn_bytes && (rc = dalloc(reinterpret_cast<char**>(&c->ws_cnn), c->ws_cnn_bytes))) return rc;
     c->cap = n;
     return FD_OK;
+}
+
+// The step on symbols [s0, s0 + n) of the plan's buffers (s, tx_idx already offset).
+int run_chunk(fd_chain* c, const void* s, const uint16_t* tx_idx, long long s0, long long n, long long* counts,
+              void* yhat, cudaStream_t stream) {
+    if (n == 0) return FD_OK;
+    const fd_chain_desc& d = c->d;
+    const size_t pu = (size_t)d.U * d.N_d, pb = (size_t)d.B * d.N_d, py = (size_t)d.B * d.N_ifft;
+    float2* st = c->s_tilde + s0 * pu;
+    int rc = d.head == 1 ? fdcnn_paper_forward(c->params, d.n_conv, s, st, c->ws_cnn, c->ws_cnn_bytes, n, d.U, d.N_d,
+                                               stream)
+                         : fdcnn_forward(c->params, d.chans, d.n_layers, s, st, c->ws_cnn, c->ws_cnn_bytes, n, d.U,
+                                         d.N_d, stream);
+    if (rc) return rc;
+    float2* XPA = c->XPA + s0 * pb;
+    rc = chain_txrx(c->P, st, c->coef, c->y + s0 * py, XPA, d.orders, d.n_orders, d.L, d.M, n, d.B, d.U, d.N_d,
+                    d.N_ifft, stream);
+    if (rc) return rc;
+    return ue_combine_ser(XPA, c->h_fd, yhat ? yhat : (void*)(c->yhat + s0 * pu), c->alpha, tx_idx, d.M_qam, nullptr,
+                          counts, n, d.B, d.U, d.N_d, d.boundary_eps, stream);
 }
 
 }  // namespace
@@ -120,6 +148,14 @@ int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_tap
                              c->ws_zf, zf_workspace_bytes(d.N_d), stream));
     FD_TRY(ensure_batch(c, max_batch));
 #undef FD_TRY
+    bool ok = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&c->ev_free, cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; ok && k < fd_chain::kChunks; ++k)
+        ok = cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        release(c);
+        return fdpd::check_launch("fd_chain_create (streams)");
+    }
     *out = c;
     return FD_OK;
 }
@@ -133,18 +169,7 @@ int fd_chain_run_device(fd_chain* c, const void* s, const uint16_t* tx_idx, long
     FD_REQUIRE(c && s && tx_idx && counts, "fd_chain_run_device: NULL pointer");
     FD_REQUIRE(n_sym >= 0 && n_sym <= c->cap, "fd_chain_run_device: n_sym=%lld exceeds the plan's batch %lld", n_sym,
                c->cap);
-    if (n_sym == 0) return FD_OK;
-    const fd_chain_desc& d = c->d;
-    int rc = d.head == 1 ? fdcnn_paper_forward(c->params, d.n_conv, s, c->s_tilde, c->ws_cnn, c->ws_cnn_bytes, n_sym,
-                                               d.U, d.N_d, stream)
-                         : fdcnn_forward(c->params, d.chans, d.n_layers, s, c->s_tilde, c->ws_cnn, c->ws_cnn_bytes,
-                                         n_sym, d.U, d.N_d, stream);
-    if (rc) return rc;
-    rc = chain_txrx(c->P, c->s_tilde, c->coef, c->y, c->XPA, d.orders, d.n_orders, d.L, d.M, n_sym, d.B, d.U, d.N_d,
-                    d.N_ifft, stream);
-    if (rc) return rc;
-    return ue_combine_ser(c->XPA, c->h_fd, yhat ? yhat : c->yhat, c->alpha, tx_idx, d.M_qam, nullptr, counts, n_sym,
-                          d.B, d.U, d.N_d, d.boundary_eps, stream);
+    return run_chunk(c, s, tx_idx, 0, n_sym, counts, yhat, stream);
 }
 
 int fd_chain_run_host(fd_chain* c, const void* s_host, const uint16_t* idx_host, long long n_sym,
@@ -153,13 +178,31 @@ int fd_chain_run_host(fd_chain* c, const void* s_host, const uint16_t* idx_host,
     FD_REQUIRE(n_sym >= 0 && n_sym <= c->cap, "fd_chain_run_host: n_sym=%lld exceeds the plan's batch %lld", n_sym,
                c->cap);
     const fd_chain_desc& d = c->d;
-    const size_t ns = (size_t)n_sym * d.U * d.N_d;
-    if (cudaMemcpyAsync(c->s, s_host, sizeof(float2) * ns, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
-        cudaMemcpyAsync(c->idx, idx_host, sizeof(uint16_t) * ns, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
-        cudaMemsetAsync(c->counts, 0, 3 * sizeof(long long), stream) != cudaSuccess)
-        return fdpd::check_launch("fd_chain_run_host (h2d)");
-    int rc = fd_chain_run_device(c, c->s, c->idx, n_sym, c->counts, nullptr, stream);
-    if (rc) return rc;
+    // Pipelined over up to kChunks symbol chunks: chunk k's host->device copy (copy stream)
+    // overlaps chunk k-1's compute (stream); only the first chunk's copy is exposed.
+    const long long per = (size_t)d.U * d.N_d;
+    const int chunks = (int)std::max(1LL, std::min<long long>(fd_chain::kChunks, n_sym / 64));
+    if (cudaMemsetAsync(c->counts, 0, 3 * sizeof(long long), stream) != cudaSuccess ||
+        cudaEventRecord(c->ev_free, stream) != cudaSuccess ||                   // previous step done with c->s
+        cudaStreamWaitEvent(c->copy_stream, c->ev_free, 0) != cudaSuccess)
+        return fdpd::check_launch("fd_chain_run_host (order)");
+    for (int k = 0; k < chunks; ++k) {
+        const long long s0 = n_sym * k / chunks, s1 = n_sym * (k + 1) / chunks;
+        const size_t off = (size_t)s0 * per, cnt = (size_t)(s1 - s0) * per;
+        if (cudaMemcpyAsync(c->s + off, (const float2*)s_host + off, sizeof(float2) * cnt, cudaMemcpyHostToDevice,
+                            c->copy_stream) != cudaSuccess ||
+            cudaMemcpyAsync(c->idx + off, idx_host + off, sizeof(uint16_t) * cnt, cudaMemcpyHostToDevice,
+                            c->copy_stream) != cudaSuccess ||
+            cudaEventRecord(c->ev_in[k], c->copy_stream) != cudaSuccess)
+            return fdpd::check_launch("fd_chain_run_host (h2d)");
+    }
+    for (int k = 0; k < chunks; ++k) {
+        const long long s0 = n_sym * k / chunks, s1 = n_sym * (k + 1) / chunks;
+        if (cudaStreamWaitEvent(stream, c->ev_in[k], 0) != cudaSuccess) return fdpd::check_launch("fd_chain (wait)");
+        const int rc = run_chunk(c, c->s + (size_t)s0 * per, c->idx + (size_t)s0 * per, s0, s1 - s0, c->counts,
+                                 nullptr, stream);
+        if (rc) return rc;
+    }
     if (cudaMemcpyAsync(counts_host, c->counts, 3 * sizeof(long long), cudaMemcpyDeviceToHost, stream) !=
             cudaSuccess ||
         cudaStreamSynchronize(stream) != cudaSuccess)

@@ -148,7 +148,12 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     // mbarrier was 6% slower on C2 — every thread then waits for the whole 38 KB.)
     float2* xs = reinterpret_cast<float2*>(esm);
     stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
-    {
+    if (imp.precoded) {
+        // P holds the precoded spectrum X [n_sym][B][N_d] (chain_txrx_pre): one coalesced
+        // pass over the symbol-antenna row into xs
+        const float2* Xr = P + nb * N_d;
+        for (int j = tid; j < N_d; j += T) xs[j] = __ldg(Xr + j);
+    } else {
         const float2* Pb = P + (size_t)n * imp.p_stride + (size_t)b * U * N_d;
         const float2* sn = s + n * U * N_d;
         // (Measured: a 4-subcarrier x 4-user predicated batch of 32 loads was 3% slower on
@@ -442,9 +447,11 @@ static int chain_tx_impl(const void* P, const void* s_tilde, const void* coef, v
 
 static int chain_txrx_impl(const void* P, const void* s_tilde, const void* coef, void* y, void* XPA,
                            const int* orders, int n_orders, int L, int M, long long n_sym, int B_loc, int U, int N_d,
-                           int N_ifft, const fd_impair* pub, cudaStream_t stream, bool per_symbol_P = false) {
+                           int N_ifft, const fd_impair* pub, cudaStream_t stream, bool per_symbol_P = false,
+                           bool precoded = false) {
     Impair imp = to_impair(pub, B_loc);
     if (per_symbol_P) imp.p_stride = (long long)B_loc * U * N_d;
+    imp.precoded = precoded ? 1 : 0;
     FD_REQUIRE(U >= 1 && U <= 1024, "chain_txrx: bad U=%d", U);
     int rc = validate_ofdm(n_sym, B_loc, N_d, N_ifft);
     if (rc) return rc;
@@ -491,6 +498,13 @@ int chain_txrx_ps(const void* P_all, const void* s_tilde, const void* coef, void
                   const fd_impair* imp, cudaStream_t stream) {
     return chain_txrx_impl(P_all, s_tilde, coef, y, XPA, orders, n_orders, L, M, n_sym, B_loc, U, N_d, N_ifft, imp,
                            stream, true);
+}
+
+int chain_txrx_pre(const void* X, const void* coef, void* y, void* XPA, const int* orders, int n_orders, int L, int M,
+                   long long n_sym, int B_loc, int N_d, int N_ifft, const fd_impair* imp, cudaStream_t stream) {
+    // s_tilde is unused on this path; pass X for the non-NULL check
+    return chain_txrx_impl(X, X, coef, y, XPA, orders, n_orders, L, M, n_sym, B_loc, 1, N_d, N_ifft, imp, stream,
+                           false, true);
 }
 
 }  // extern "C"

@@ -65,6 +65,7 @@ SIGNATURES = {
     "ue_slice_ser": (_i, [_vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
     "ue_receive_ser": (_i, [_vp, _vp, _vp, _vp, _sz, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _i, _f, _vp]),
     "chain_txrx_ex": (_i, [_vp, _vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _imp, _vp]),
+    "chain_txrx_pre": (_i, [_vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _imp, _vp]),
     "zf_precoder_build_ex": (_i, [_vp, _vp, _f, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, C.POINTER(C.c_float), _vp,
                                   _sz, _vp]),
     "ue_combine_ser_ex": (_i, [_vp, _vp, _vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _f, _imp, _vp]),
@@ -216,6 +217,20 @@ def zf_precoder_build_batched(h_taps_all, N_ifft, N_d, rho, out=None):
                                            _ptr(h_fd), _ptr(P), _ptr(alpha), _ptr(status), _ptr(ws), ws.numel(),
                                            _stream(h_taps_all)))
     return out
+
+
+def chain_txrx_pre(X, coef, orders, L, M, N_ifft, imp=None, y=None, XPA=None):
+    """chain_txrx on a precoded spectrum X [n_sym][B_loc][N_d] (output of precode)."""
+    _dev(X, torch.complex64, "X")
+    _dev(coef, torch.complex64, "coef")
+    n_sym, B, N_d = X.shape
+    if y is None:
+        y = torch.empty((n_sym, B, N_ifft), dtype=torch.complex64, device=X.device)
+    if XPA is None:
+        XPA = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=X.device)
+    _check(lib().chain_txrx_pre(_ptr(X), _ptr(coef), _ptr(y), _ptr(XPA), _ints(orders), len(orders), L, M, n_sym, B,
+                                N_d, N_ifft, C.byref(imp) if imp else None, _stream(X)))
+    return y, XPA
 
 
 def chain_txrx_ps(P_all, s_tilde, coef, orders, L, M, N_ifft, imp=None, y=None, XPA=None):
