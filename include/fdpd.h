@@ -63,7 +63,16 @@ void fd_shutdown(void);
  *  s_out     device complex64 [n_sym][U][N_d]; must not alias s_in.
  *  workspace device scratch of >= fdcnn_workspace_bytes(...) bytes (may be NULL
  *            when that returns 0).
+ *
+ * Implementation choice (process-wide, not thread-safe against concurrent calls):
+ * fd_set_cnn_path(FD_CNN_TENSOR or FD_CNN_AUTO) runs every layer as a tensor-core
+ * implicit GEMM (tcgen05 kind::tf32 with hi/lo operand splitting, FP32-accurate)
+ * when all hidden widths are 16, 32 or 64; FD_CNN_SIMT forces the FP32 SIMT kernels.
+ * The workspace size depends on the path: query it after choosing.  Returns
+ * FD_ERR_ARG for an unknown path.
  * ------------------------------------------------------------------------- */
+enum { FD_CNN_AUTO = 0, FD_CNN_SIMT = 1, FD_CNN_TENSOR = 2 };
+int fd_set_cnn_path(int path);
 size_t fdcnn_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d);
 int fdcnn_forward(const float* params, const int* chans, int n_layers,
                   const void* s_in, void* s_out, void* workspace, size_t workspace_bytes,

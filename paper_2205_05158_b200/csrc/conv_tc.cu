@@ -1,0 +1,448 @@
+// conv_tc.cu — FD-CNN 3x3 "same" convolutions on the 5th-generation tensor cores
+// (Eq. 15; BASELINE residual stack, readings A1-A6).
+//
+// A 3x3 convolution over an S x S image is an implicit GEMM
+//     D[q][co] = sum_{tap, ci} A[q + off(tap)][ci] * W[tap][ci][co],
+// q a pixel of the zero-haloed (S+2) x (S+2) image and off(tap) = (dy-1)(S+2) + (dx-1).
+// Activations live channels-last in the haloed layout act[img][q][C], so the A operand
+// of every tap is the SAME shared-memory tile shifted by off(tap) pixels: with the
+// K-major no-swizzle descriptor layout (pixel rows 16 B apart, 4 channels per 16 B row,
+// channel groups LBO apart) the shift is just the descriptor's start address — no
+// im2col copy.  One CTA computes M = 128 consecutive pixels x all output channels per
+// tile with tcgen05.mma kind::tf32 (M = 128, N = Cout padded to 16/32/64, K = 8 per
+// instruction) into a TMEM accumulator (two, double-buffered across tiles).
+//
+// FP32 accuracy with TF32 tensor cores (the 2e-5 parity bar): both operands are split
+// x = hi + lo with hi = rna_tf32(x), lo = rna_tf32(x - hi).  The weight halves sit side by
+// side in N (B = [W_hi | W_lo], N = 2 Cout) and each K step issues two MMAs, A_hi B and
+// A_lo B, into one accumulator: all four products, summed in the epilogue.  (An SS-mode
+// MMA at N <= 64 costs the same ~46 cycles as at N = 16 — it is bound by reading the
+// 4 KB A tile from shared memory — so doubling N is free where 3xTF32's third MMA is not.)  Weights are split once per call into a global image laid out exactly as
+// the shared-memory B operand, copied in with cp.async.bulk (TMA); activations are split
+// by the CTA while staging A.
+//
+// Layers: IN_MODE 1 reads the complex symbols (2 real channels, padded to K = 8);
+// OUT_MODE 0 writes tanh(D + b) channels-last with a zero halo; OUT_MODE 1 (Cout = 2,
+// N padded to 16) writes the residual s_out = s_in + D + b on the first N_d pixels.
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace fdpd {
+
+constexpr int TC_M = 128;
+
+struct TcConv {
+    int S, Wp, P, N_d;        // image side, haloed side, haloed pixels, symbols per image
+    int q_begin, q_end;       // computed pixel range [Wp, Wp + S Wp) (rows 1..S)
+    int n_tiles;              // tiles per image
+    int A_px, PL;             // staged pixels per tile, plane stride in bytes
+    int Cin, Cout;            // real channel counts
+    long long n_img;
+    int ws, na;               // weight ring slots (9 = all taps resident), A buffers
+    int off_a, off_bias, off_bar;   // smem byte offsets (weights at 0)
+    int tmem_cols;
+};
+
+// Weights W[co][ci][3][3] -> per tap [ci/4][n][4] with n < 2 NP: rows n < NP hold hi(W[n]),
+// rows NP + co hold lo(W[co]); zero padded to CINP x NP.  This is exactly the shared-memory
+// B operand (K-major, core matrices 8 rows x 4 ci) of one MMA with N = 2 NP, so
+//     D[:, co] + D[:, NP + co] = A (W_hi + W_lo)[co].
+__global__ void k_tc_weights(const float* __restrict__ W, float* __restrict__ Wg, int Cin, int Cout, int CINP, int NP) {
+    const int per_tap = 2 * CINP * NP;
+    const int n = 9 * per_tap;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const int tap = e / per_tap;
+        int r = e - tap * per_tap;
+        const int gq = r / (2 * NP * 4);
+        r -= gq * 2 * NP * 4;
+        const int row = r >> 2, ci = 4 * gq + (r & 3);
+        const int hl = row >= NP, co = row - hl * NP;
+        const float w = (co < Cout && ci < Cin) ? W[((size_t)co * Cin + ci) * 9 + tap] : 0.f;
+        const float hi = tf32_rna(w);
+        Wg[e] = hl ? tf32_rna(w - hi) : hi;
+    }
+}
+
+// Warp roles (no CTA-wide barrier inside the tile loop; mbarrier pipelines between roles):
+//   warps 0-3   epilogue: TMEM lane quadrant w (pixels 32w..32w+31) x all columns
+//   warps 4-11  A producers: load, split hi/lo, store the tile's A planes
+//   warp 12     one thread: weight TMA (resident or a ring of per-tap slots) + MMA issue
+// Rings: A buffers (na) with a_full (256 arrivals) / a_empty (tcgen05.commit), two TMEM
+// accumulators with acc_full (commit) / acc_empty (128 arrivals).
+constexpr int TC_EPI_WARPS = 4, TC_LOAD_WARPS = 8;
+constexpr int TC_THREADS = 32 * (TC_EPI_WARPS + TC_LOAD_WARPS + 1);
+constexpr int TC_LOAD_THREADS = 32 * TC_LOAD_WARPS;
+
+template <int CINP, int NP, int IN_MODE, int OUT_MODE>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const float* __restrict__ Wg,
+              const float* __restrict__ bias, float* __restrict__ act_out, float2* __restrict__ s_out, TcConv g) {
+    constexpr int G = CINP / 4;           // 16-byte channel groups (planes) per hi / lo
+    constexpr int KSTEPS = CINP / 8;      // MMAs of K = 8 per tap and product
+    constexpr uint32_t WBYTES = 2u * CINP * NP * 4u;
+    constexpr uint32_t IDESC = idesc_tf32_m128(2 * NP);
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + g.off_bar);
+    uint64_t* acc_full = bars;                 // [2]
+    uint64_t* acc_empty = bars + 2;            // [2]
+    uint64_t* a_full = bars + 4;               // [na]
+    uint64_t* a_empty = a_full + g.na;         // [na]
+    uint64_t* wfull = a_empty + g.na;          // [ws]
+    uint64_t* wempty = wfull + g.ws;           // [ws]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + g.ws);
+    float* bsm = reinterpret_cast<float*>(sm + g.off_bias);
+    const uint32_t sm_base = smem_u32(sm);
+    const uint32_t abytes = 2u * G * g.PL;
+
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 32 * TC_EPI_WARPS);
+        }
+        for (int i = 0; i < g.na; ++i) {
+            mbar_init(&a_full[i], TC_LOAD_THREADS);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < g.ws; ++i) {
+            mbar_init(&wfull[i], 1);
+            mbar_init(&wempty[i], 1);
+        }
+    }
+    if (tid < NP) bsm[tid] = tid < g.Cout ? bias[tid] : 0.f;
+    if (warp == 0) tmem_alloc(tmem_slot, g.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // 32-bit tile bookkeeping (the host guarantees n_img * n_tiles < 2^31); ring slots and
+    // phases advance incrementally (no divisions in the role loops)
+    const int total = (int)(g.n_img * g.n_tiles);
+    const int my_tiles = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+    if (warp >= TC_EPI_WARPS && warp < TC_EPI_WARPS + TC_LOAD_WARPS) {
+        // ------------------------------------------------------------ A producers
+        const int lt = tid - 32 * TC_EPI_WARPS;
+        int buf = 0;
+        uint32_t ph = 0;
+        int img = (int)blockIdx.x / g.n_tiles, t = (int)blockIdx.x - img * g.n_tiles;
+        const int dimg = (int)gridDim.x / g.n_tiles, dt = (int)gridDim.x - dimg * g.n_tiles;
+        for (int i = 0; i < my_tiles; ++i) {
+            if (i >= g.na) mbar_wait(&a_empty[buf], ph ^ 1u);
+            const int q0 = g.q_begin + t * TC_M;
+            const int qa = q0 - g.Wp - 1;
+            unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
+            if constexpr (IN_MODE == 0) {
+                const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP);
+                for (int e = lt; e < g.A_px * G; e += TC_LOAD_THREADS) {
+                    const int p = e / G, gq = e - p * G;
+                    const int pos = qa + p;
+                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (pos >= 0 && pos < g.P) x = __ldg(src + (size_t)pos * G + gq);
+                    float4 hi, lo;
+                    hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
+                    hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
+                    hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
+                    hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
+                    *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
+                    *reinterpret_cast<float4*>(ab + (size_t)(G + gq) * g.PL + p * 16) = lo;
+                }
+            } else {
+                // symbols: channel 0 = Re, 1 = Im of s[y S + x] (zero beyond N_d and on the halo)
+                const float2* simg = s_in + (size_t)img * g.N_d;
+                const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int p = lt; p < g.A_px; p += TC_LOAD_THREADS) {
+                    const int pos = qa + p;
+                    float2 z = make_float2(0.f, 0.f);
+                    if (pos >= 0 && pos < g.P) {
+                        const int row = pos / g.Wp;
+                        const int y = row - 1, x = pos - row * g.Wp - 1;
+                        const int k = y * g.S + x;
+                        if (y >= 0 && y < g.S && x >= 0 && x < g.S && k < g.N_d) z = __ldg(simg + k);
+                    }
+                    const float hx = tf32_rna(z.x), hy = tf32_rna(z.y);
+                    *reinterpret_cast<float4*>(ab + p * 16) = make_float4(hx, hy, 0.f, 0.f);
+                    *reinterpret_cast<float4*>(ab + (size_t)G * g.PL + p * 16) =
+                        make_float4(tf32_rna(z.x - hx), tf32_rna(z.y - hy), 0.f, 0.f);
+#pragma unroll
+                    for (int gq = 1; gq < G; ++gq) {
+                        *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = z4;
+                        *reinterpret_cast<float4*>(ab + (size_t)(G + gq) * g.PL + p * 16) = z4;
+                    }
+                }
+            }
+            fence_proxy_async();                 // generic smem writes -> tensor-core reads
+            mbar_arrive(&a_full[buf]);
+            if (++buf == g.na) { buf = 0; ph ^= 1u; }
+            img += dimg;
+            t += dt;
+            if (t >= g.n_tiles) { t -= g.n_tiles; ++img; }
+        }
+    } else if (warp == TC_EPI_WARPS + TC_LOAD_WARPS) {
+        // ------------------------------------------------------------ weights + MMA issue
+        // The whole warp walks the loop with identical (warp-uniform) values, so the
+        // descriptors live in uniform registers; one elected lane issues each instruction.
+        const int my_taps = 9 * my_tiles;
+        // weight ring: producer (TMA) and consumer (MMA) slot / phase
+        int lslot = 0, cslot = 0, w_loaded = 0;
+        uint32_t lph = 0, cph = 0;
+        auto load_w = [&](int idx) {
+            if (idx >= g.ws) mbar_wait(&wempty[lslot], lph ^ 1u);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&wfull[lslot], WBYTES);
+                tma_bulk_g2s(sm + (size_t)lslot * WBYTES, Wg + (size_t)(idx % 9) * (WBYTES / 4), WBYTES,
+                             &wfull[lslot]);
+            }
+            __syncwarp();
+            if (++lslot == g.ws) { lslot = 0; lph ^= 1u; }
+        };
+        const bool resident = g.ws == 9;
+        const int first = resident ? (my_taps > 0 ? 9 : 0) : (my_taps < g.ws ? my_taps : g.ws);
+        for (; w_loaded < first; ++w_loaded) load_w(w_loaded);
+        const uint32_t PL = (uint32_t)g.PL;
+        int buf = 0;
+        uint32_t aph = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            const int acc = i & 1;
+            mbar_wait(&a_full[buf], aph);
+            if (i >= 2) mbar_wait(&acc_empty[acc], (uint32_t)(((i >> 1) - 1) & 1));
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)acc * (2 * NP);
+            const uint32_t ab = sm_base + g.off_a + (uint32_t)buf * abytes;
+            for (int tap = 0; tap < 9; ++tap) {
+                // resident weights (ws = 9) are waited for once, before the first tile
+                if (!resident || i == 0) {
+                    mbar_wait(&wfull[cslot], cph);
+                    tc_fence_after();
+                }
+                const uint32_t wb = sm_base + (uint32_t)cslot * WBYTES;
+                const uint32_t at = ab + (uint32_t)(((tap / 3) * g.Wp + (tap % 3)) * 16);
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < KSTEPS; ++k) {
+                        const uint64_t ahi = umma_desc(at + 2u * k * PL, PL, 128);
+                        const uint64_t alo = umma_desc(at + (uint32_t)(G + 2 * k) * PL, PL, 128);
+                        const uint64_t b = umma_desc(wb + 2u * k * (2 * NP) * 16, 2 * NP * 16, 128);
+                        mma_tf32(d, ahi, b, IDESC, (tap | k) ? 1u : 0u);
+                        mma_tf32(d, alo, b, IDESC, 1u);
+                    }
+                    if (!resident) umma_commit(&wempty[cslot]);
+                }
+                __syncwarp();
+                if (++cslot == g.ws) { cslot = 0; cph ^= 1u; }
+                // streamed weights: refill the previous tap's slot (its MMAs finish as these start)
+                if (!resident && w_loaded < my_taps && w_loaded < i * 9 + tap + g.ws) load_w(w_loaded++);
+            }
+            if (elect_one()) {
+                umma_commit(&a_empty[buf]);
+                umma_commit(&acc_full[acc]);
+            }
+            __syncwarp();
+            if (++buf == g.na) { buf = 0; aph ^= 1u; }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 0-3)
+        int img = (int)blockIdx.x / g.n_tiles, t = (int)blockIdx.x - img * g.n_tiles;
+        const int dimg = (int)gridDim.x / g.n_tiles, dt = (int)gridDim.x - dimg * g.n_tiles;
+        for (int i = 0; i < my_tiles; ++i, img += dimg, t += dt) {
+            if (t >= g.n_tiles) { t -= g.n_tiles; ++img; }
+            const int acc = i & 1;
+            mbar_wait(&acc_full[acc], (uint32_t)((i >> 1) & 1));
+            tc_fence_after();
+            const int pos = g.q_begin + t * TC_M + warp * 32 + lane;
+            const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)acc * (2 * NP);
+            const int prow = pos / g.Wp, pcol = pos - prow * g.Wp;
+            const bool interior = pos < g.q_end && pcol >= 1 && pcol <= g.S;
+            if constexpr (OUT_MODE == 0) {
+                float* o = act_out + ((size_t)img * g.P + pos) * NP;
+#pragma unroll
+                for (int c0 = 0; c0 < NP; c0 += 8) {
+                    float v[8], w[8];
+                    tmem_ld8(tbase + c0, v);          // A W_hi
+                    tmem_ld8(tbase + NP + c0, w);     // A W_lo
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[j] = interior ? tanhf((v[j] + w[j]) + bsm[c0 + j]) : 0.f;
+                    if (pos < g.q_end) {
+                        reinterpret_cast<float4*>(o + c0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        reinterpret_cast<float4*>(o + c0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&acc_empty[acc]);
+                // the halo rows 0 and S+1 are never computed: zero them from the first / last tile
+                for (int side = 0; side < 2; ++side) {
+                    if (t != (side ? g.n_tiles - 1 : 0)) continue;
+                    float4* z = reinterpret_cast<float4*>(act_out + ((size_t)img * g.P + (side ? g.q_end : 0)) * NP);
+                    for (int e = tid; e < g.Wp * NP / 4; e += 32 * TC_EPI_WARPS) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            } else {
+                float v[8], w[8];
+                tmem_ld8(tbase, v);
+                tmem_ld8(tbase + NP, w);
+                v[0] += w[0];
+                v[1] += w[1];
+                tc_fence_before();
+                mbar_arrive(&acc_empty[acc]);
+                const int k = (prow - 1) * g.S + (pcol - 1);
+                if (interior && k < g.N_d) {
+                    const size_t o = (size_t)img * g.N_d + k;
+                    const float2 z = __ldg(s_in + o);
+                    s_out[o] = make_float2(z.x + (v[0] + bsm[0]), z.y + (v[1] + bsm[1]));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, g.tmem_cols);
+    }
+}
+
+// ============================================================================ host side
+static int pad_ch(int c) { return c <= 8 ? 8 : (c <= 16 ? 16 : (c <= 32 ? 32 : 64)); }
+static int pad_n(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : 64); }
+
+// Whether every layer of chans maps onto k_conv_tc (first 2 -> C, middle C -> C', last C -> 2,
+// C in {16, 32, 64}).
+bool tc_supported(const int* chans, int n_layers) {
+    if (n_layers < 2 || chans[0] != 2 || chans[n_layers] != 2) return false;
+    for (int l = 1; l < n_layers; ++l)
+        if (chans[l] != 16 && chans[l] != 32 && chans[l] != 64) return false;
+    return true;
+}
+
+static TcConv tc_geom(int S, int N_d, int Cin, int Cout, long long n_img) {
+    TcConv g{};
+    g.S = S;
+    g.Wp = S + 2;
+    g.P = g.Wp * g.Wp;
+    g.N_d = N_d;
+    g.q_begin = g.Wp;
+    g.q_end = g.Wp + S * g.Wp;
+    g.n_tiles = (S * g.Wp + TC_M - 1) / TC_M;
+    g.A_px = (TC_M + 2 * g.Wp + 2 + 7) & ~7;
+    g.PL = (g.A_px + 1) * 16;   // one spare row: the 4-channel groups of a pixel hit distinct banks
+    g.Cin = Cin;
+    g.Cout = Cout;
+    g.n_img = n_img;
+    return g;
+}
+
+// smem plan: weights (ws slots) | A ring (na buffers) | bias | barriers.  Deepest A ring
+// first (up to 4), resident weights preferred at equal depth.  Returns bytes or 0.
+static size_t tc_plan(TcConv& g, int CINP, int NP) {
+    const size_t wtap = 2ull * CINP * NP * 4, abuf = 2ull * (CINP / 4) * g.PL;
+    const size_t limit = 227 * 1024;
+    for (int na = 4; na >= 1; --na)
+        for (int ws : {9, 2}) {
+            const size_t off_a = ws * wtap;
+            const size_t off_bias = off_a + na * abuf;
+            const size_t off_bar = (off_bias + NP * 4 + 15) & ~(size_t)15;
+            const size_t bytes = off_bar + 8 * (4 + 2 * na + 2 * ws) + 16;
+            if (bytes > limit) continue;
+            g.ws = ws;
+            g.na = na;
+            g.off_a = (int)off_a;
+            g.off_bias = (int)off_bias;
+            g.off_bar = (int)off_bar;
+            int cols = 32;
+            while (cols < 4 * NP) cols <<= 1;   // two accumulators of N = 2 NP
+            g.tmem_cols = cols;
+            return bytes;
+        }
+    return 0;
+}
+
+template <int CINP, int NP, int IN_MODE, int OUT_MODE>
+static int launch_tc_na(const TcConv& g, size_t smem, const float* act_in, const float2* s_in, const float* Wg,
+                        const float* bias, float* act_out, float2* s_out, cudaStream_t st) {
+    auto kern = k_conv_tc<CINP, NP, IN_MODE, OUT_MODE>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0, dev = 0, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long tiles = g.n_img * g.n_tiles;
+    const long long grid = std::min<long long>(tiles, (long long)nsm * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, TC_THREADS, smem, st>>>(act_in, s_in, Wg, bias, act_out, s_out, g);
+    return check_launch("fdcnn_forward (tensor-core conv)");
+}
+
+template <int IN_MODE, int OUT_MODE, int CINP>
+static int launch_tc_n(int NP, const TcConv& g, size_t smem, const float* act_in, const float2* s_in, const float* Wg,
+                       const float* bias, float* act_out, float2* s_out, cudaStream_t st) {
+    switch (NP) {
+        case 16: return launch_tc_na<CINP, 16, IN_MODE, OUT_MODE>(g, smem, act_in, s_in, Wg, bias, act_out, s_out, st);
+        case 32: return launch_tc_na<CINP, 32, IN_MODE, OUT_MODE>(g, smem, act_in, s_in, Wg, bias, act_out, s_out, st);
+        default: return launch_tc_na<CINP, 64, IN_MODE, OUT_MODE>(g, smem, act_in, s_in, Wg, bias, act_out, s_out, st);
+    }
+}
+
+// Workspace: two channels-last haloed activation buffers + the split weights of every layer.
+size_t fdcnn_tc_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d) {
+    int S = 1;
+    while (S * S < N_d) ++S;
+    const size_t P = (size_t)(S + 2) * (S + 2);
+    int cmax = 0;
+    for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
+    const size_t one = (((size_t)n_sym * U * P * cmax * 4) + 255) & ~(size_t)255;
+    size_t bytes = (n_layers > 2 ? 2 : 1) * one;
+    for (int l = 0; l < n_layers; ++l)
+        bytes += ((size_t)9 * 2 * pad_ch(chans[l]) * pad_n(chans[l + 1]) * 4 + 255) & ~(size_t)255;
+    return bytes;
+}
+
+int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const float2* s_in, float2* s_out,
+                     void* workspace, long long n_sym, int U, int N_d, cudaStream_t stream) {
+    int S = 1;
+    while (S * S < N_d) ++S;
+    const long long n_img = n_sym * U;
+    const size_t P = (size_t)(S + 2) * (S + 2);
+    int cmax = 0;
+    for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
+    const size_t one = (((size_t)n_img * P * cmax * 4) + 255) & ~(size_t)255;
+    char* ws = static_cast<char*>(workspace);
+    float* act[2] = {reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws + (n_layers > 2 ? one : 0))};
+    char* wptr = ws + (n_layers > 2 ? 2 : 1) * one;
+    size_t off = 0;
+    int rc = FD_OK;
+    for (int l = 0; l < n_layers; ++l) {
+        const int ci = chans[l], co = chans[l + 1];
+        const int CINP = pad_ch(ci), NP = pad_n(co);
+        const float* W = params + off;
+        const float* b = W + (size_t)co * ci * 9;
+        off += (size_t)co * ci * 9 + co;
+        float* Wg = reinterpret_cast<float*>(wptr);
+        const int nw = 9 * 2 * CINP * NP;
+        wptr += ((size_t)nw * 4 + 255) & ~(size_t)255;
+        k_tc_weights<<<(nw + 255) / 256, 256, 0, stream>>>(W, Wg, ci, co, CINP, NP);
+        if ((rc = check_launch("fdcnn_forward (weight split)"))) return rc;
+        TcConv g = tc_geom(S, N_d, ci, co, n_img);
+        FD_REQUIRE(n_img * g.n_tiles < (1LL << 31), "fdcnn_forward: too many images per call for the tensor-core path");
+        const size_t smem = tc_plan(g, CINP, NP);
+        if (!smem) return fail_arg("fdcnn_forward: tensor-core plan does not fit shared memory");
+        const bool first = l == 0, last = l == n_layers - 1;
+        const float* in = first ? nullptr : act[(l - 1) & 1];
+        float* out = last ? nullptr : act[l & 1];
+        if (first) rc = launch_tc_n<1, 0, 8>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream);
+        else if (last) {
+            switch (CINP) {
+                case 16: rc = launch_tc_n<0, 1, 16>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+                case 32: rc = launch_tc_n<0, 1, 32>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+                default: rc = launch_tc_n<0, 1, 64>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+            }
+        } else {
+            switch (CINP) {
+                case 16: rc = launch_tc_n<0, 0, 16>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+                case 32: rc = launch_tc_n<0, 0, 32>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+                default: rc = launch_tc_n<0, 0, 64>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+            }
+        }
+        if (rc) return rc;
+    }
+    return FD_OK;
+}
+
+}  // namespace fdpd

@@ -47,6 +47,7 @@ SIGNATURES = {
     "fd_last_error": (C.c_char_p, []),
     "fd_version": (_i, []),
     "fd_shutdown": (None, []),
+    "fd_set_cnn_path": (_i, [_i]),
     "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
     "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
     "fdcnn_paper_workspace_bytes": (_sz, [_i, _ll, _i, _i]),
@@ -139,6 +140,15 @@ def _ws(nbytes, like):
 
 
 # ----------------------------------------------------------------------------- a1
+CNN_AUTO, CNN_SIMT, CNN_TENSOR = 0, 1, 2
+
+
+def set_cnn_path(path: int):
+    """Choose the FD-CNN implementation (include/fdpd.h fd_set_cnn_path): CNN_AUTO (tensor
+    cores where every hidden width is 16/32/64), CNN_SIMT or CNN_TENSOR.  Process-wide."""
+    _check(lib().fd_set_cnn_path(int(path)))
+
+
 def fdcnn_forward(params, chans, s_in, out=None, workspace=None):
     """s_tilde = s + CNN(s)  (include/fdpd.h fdcnn_forward).  s_in complex64 [n_sym][U][N_d]."""
     _dev(params, torch.float32, "params")

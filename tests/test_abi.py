@@ -78,8 +78,19 @@ def test_workspace_queries(lib):
     lib.fdcnn_workspace_bytes.restype = ctypes.c_size_t
     lib.fdcnn_workspace_bytes.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_longlong,
                                           ctypes.c_int, ctypes.c_int]
-    ch = (ctypes.c_int * 4)(2, 16, 16, 2)
-    assert lib.fdcnn_workspace_bytes(ch, 3, 1024, 4, 600) == 0          # C2: whole network in shared memory
-    ch = (ctypes.c_int * 5)(2, 32, 32, 32, 2)
-    act = 2 * 4 * 16 * 8 * 32 * 35 * 35                      # C3: per-layer, two activation buffers
-    assert act < lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) < act + (1 << 20)   # + transposed weights
+    lib.fd_set_cnn_path.restype = ctypes.c_int
+    lib.fd_set_cnn_path.argtypes = [ctypes.c_int]
+    assert lib.fd_set_cnn_path(7) == 2                                   # unknown path: FD_ERR_ARG
+    try:
+        assert lib.fd_set_cnn_path(1) == 0                               # SIMT kernels
+        ch = (ctypes.c_int * 4)(2, 16, 16, 2)
+        assert lib.fdcnn_workspace_bytes(ch, 3, 1024, 4, 600) == 0      # C2: whole network in shared memory
+        ch = (ctypes.c_int * 5)(2, 32, 32, 32, 2)
+        act = 2 * 4 * 16 * 8 * 32 * 35 * 35                  # C3: per-layer, two activation buffers
+        assert act < lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) < act + (1 << 20)   # + transposed weights
+        assert lib.fd_set_cnn_path(2) == 0                               # tensor cores
+        act = 2 * 4 * 16 * 8 * 32 * 37 * 37                  # channels-last, zero halo (S + 2)^2
+        wsplit = 4 * 9 * 2 * (8 * 32 + 32 * 32 * 2 + 32 * 16)   # hi/lo weight images, padded
+        assert act + wsplit <= lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) < act + wsplit + 4096
+    finally:
+        lib.fd_set_cnn_path(0)

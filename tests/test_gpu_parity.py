@@ -102,6 +102,44 @@ def test_fdcnn_forward(F, name, nsym):
     assert rel(got - inp["s"], want - inp["s"]) < 1e-4       # the residual itself
 
 
+@pytest.fixture
+def cnn_path(F):
+    yield F.set_cnn_path
+    F.set_cnn_path(F.CNN_AUTO)
+
+
+@pytest.mark.parametrize("path", ["simt", "tensor"])
+@pytest.mark.parametrize("chans,N_d,nsym,U", [((2, 16, 16, 2), 600, 37, 4),      # C2 shape, many tiles / CTA
+                                             ((2, 32, 32, 32, 2), 1200, 3, 8),  # C3
+                                             ((2, 64, 64, 64, 64, 2), 3300, 1, 4),  # C5 widths (streamed W)
+                                             ((2, 16, 32, 64, 2), 500, 5, 3),    # mixed widths, ragged S
+                                             ((2, 16, 2), 37, 9, 2),             # no hidden-to-hidden layer, S = 7
+                                             ((2, 32, 2), 2, 4, 1)])             # S = 2: one partial tile
+def test_fdcnn_paths(F, cnn_path, path, chans, N_d, nsym, U):
+    """Tensor-core (3xTF32 tcgen05) and SIMT FD-CNN paths against the fp64 oracle."""
+    cnn_path(F.CNN_SIMT if path == "simt" else F.CNN_TENSOR)
+    rng = np.random.default_rng(len(chans) * 1000 + N_d)
+    s = crandn(rng, nsym, U, N_d, scale=0.7)
+    n_par = sum(co * ci * 9 + co for ci, co in zip(chans[:-1], chans[1:]))
+    params = (0.05 * rng.standard_normal(n_par)).astype(np.float32)
+    got = host(F.fdcnn_forward(dev(params, torch.float32), chans, dev(s)))
+    want = O.fdcnn_forward(s, params, chans, N_d)
+    assert rel(got, want) < TOL
+    assert rel(got - s, want - s) < 1e-4
+
+
+def test_fdcnn_tensor_full_batch_sampled(F, cnn_path):
+    """C2 at the bench batch (1024 symbols) on the tensor-core path; the oracle checks
+    sampled symbols one by one (the CNN acts per symbol image)."""
+    cfg = configs.C2
+    cnn_path(F.CNN_TENSOR)
+    inp = gen.make_inputs(cfg, range(cfg.n_sym))
+    got = host(F.fdcnn_forward(dev(inp["params"], torch.float32), cfg.chans, dev(inp["s"])))
+    for n in (0, 1, 511, 1023):
+        want = O.fdcnn_forward(inp["s"][n:n + 1], inp["params"], cfg.chans, cfg.N_d)
+        assert rel(got[n:n + 1], want) < TOL
+
+
 @pytest.mark.parametrize("nsym", [1, 3, 40])
 def test_fdcnn_paper_forward(F, nsym):
     """Paper FD-CNN head (NEXT f2): conv + ReLU + FC GEMM vs the oracle; ragged M, N tails."""
