@@ -78,8 +78,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const float* __restrict__ Wg,
               const float* __restrict__ bias, float* __restrict__ act_out, float2* __restrict__ s_out, TcConv g) {
     constexpr int G = CINP / 4;           // 16-byte channel groups (planes) per hi / lo
-    constexpr int KSTEPS = CINP / 8;      // MMAs of K = 8 per tap and product
-    constexpr uint32_t WBYTES = 2u * CINP * NP * 4u;
+    constexpr int KSTEPS = CINP / 8;      // K = 8 steps per tap (two MMAs each: A_hi, A_lo)
+    constexpr int KS = CINP == 64 ? 2 : 1;   // weight chunks per tap
+    constexpr uint32_t CBYTES = 2u * CINP * NP * 4u / KS;
     constexpr uint32_t IDESC = idesc_tf32_m128(2 * NP);
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -183,25 +184,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ------------------------------------------------------------ weights + MMA issue
         // The whole warp walks the loop with identical (warp-uniform) values, so the
         // descriptors live in uniform registers; one elected lane issues each instruction.
-        const int my_taps = 9 * my_tiles;
-        // weight ring: producer (TMA) and consumer (MMA) slot / phase
+        // weight chunks: KS per tap (K halves for CINP = 64), CBYTES each; either all 9 KS
+        // chunks resident (loaded once) or a ring of ws slots refilled ws - 1 chunks ahead
+        const int my_chunks = 9 * KS * my_tiles;
         int lslot = 0, cslot = 0, w_loaded = 0;
         uint32_t lph = 0, cph = 0;
         auto load_w = [&](int idx) {
             if (idx >= g.ws) mbar_wait(&wempty[lslot], lph ^ 1u);
             if (elect_one()) {
-                mbar_arrive_expect_tx(&wfull[lslot], WBYTES);
-                tma_bulk_g2s(sm + (size_t)lslot * WBYTES, Wg + (size_t)(idx % 9) * (WBYTES / 4), WBYTES,
+                mbar_arrive_expect_tx(&wfull[lslot], CBYTES);
+                tma_bulk_g2s(sm + (size_t)lslot * CBYTES, Wg + (size_t)(idx % (9 * KS)) * (CBYTES / 4), CBYTES,
                              &wfull[lslot]);
             }
             __syncwarp();
             if (++lslot == g.ws) { lslot = 0; lph ^= 1u; }
         };
-        const bool resident = g.ws == 9;
-        const int first = resident ? (my_taps > 0 ? 9 : 0) : (my_taps < g.ws ? my_taps : g.ws);
+        const bool resident = g.ws == 9 * KS;
+        const int first = resident ? (my_chunks > 0 ? 9 * KS : 0) : (my_chunks < g.ws ? my_chunks : g.ws);
         for (; w_loaded < first; ++w_loaded) load_w(w_loaded);
         const uint32_t PL = (uint32_t)g.PL;
-        int buf = 0;
+        int buf = 0, used = 0;
         uint32_t aph = 0;
         for (int i = 0; i < my_tiles; ++i) {
             const int acc = i & 1;
@@ -211,28 +213,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t d = tmem + (uint32_t)acc * (2 * NP);
             const uint32_t ab = sm_base + g.off_a + (uint32_t)buf * abytes;
             for (int tap = 0; tap < 9; ++tap) {
-                // resident weights (ws = 9) are waited for once, before the first tile
-                if (!resident || i == 0) {
-                    mbar_wait(&wfull[cslot], cph);
-                    tc_fence_after();
-                }
-                const uint32_t wb = sm_base + (uint32_t)cslot * WBYTES;
                 const uint32_t at = ab + (uint32_t)(((tap / 3) * g.Wp + (tap % 3)) * 16);
-                if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < KSTEPS; ++k) {
-                        const uint64_t ahi = umma_desc(at + 2u * k * PL, PL, 128);
-                        const uint64_t alo = umma_desc(at + (uint32_t)(G + 2 * k) * PL, PL, 128);
-                        const uint64_t b = umma_desc(wb + 2u * k * (2 * NP) * 16, 2 * NP * 16, 128);
-                        mma_tf32(d, ahi, b, IDESC, (tap | k) ? 1u : 0u);
-                        mma_tf32(d, alo, b, IDESC, 1u);
+                for (int h = 0; h < KS; ++h) {
+                    // resident weights are waited for once, before the first tile
+                    if (!resident || i == 0) {
+                        mbar_wait(&wfull[cslot], cph);
+                        tc_fence_after();
                     }
-                    if (!resident) umma_commit(&wempty[cslot]);
+                    const uint32_t wb = sm_base + (uint32_t)cslot * CBYTES;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < KSTEPS / KS; ++kk) {
+                            const int k = h * (KSTEPS / KS) + kk;
+                            const uint64_t ahi = umma_desc(at + 2u * k * PL, PL, 128);
+                            const uint64_t alo = umma_desc(at + (uint32_t)(G + 2 * k) * PL, PL, 128);
+                            const uint64_t b = umma_desc(wb + 2u * kk * (2 * NP) * 16, 2 * NP * 16, 128);
+                            mma_tf32(d, ahi, b, IDESC, (tap | k) ? 1u : 0u);
+                            mma_tf32(d, alo, b, IDESC, 1u);
+                        }
+                        if (!resident) umma_commit(&wempty[cslot]);
+                    }
+                    __syncwarp();
+                    if (++cslot == g.ws) { cslot = 0; cph ^= 1u; }
+                    ++used;
+                    // streamed weights: refill the slot of the previous chunk (its MMAs finish as
+                    // these start), keeping ws - 1 chunks in flight
+                    if (!resident && w_loaded < my_chunks && w_loaded < used + g.ws - 1) load_w(w_loaded++);
                 }
-                __syncwarp();
-                if (++cslot == g.ws) { cslot = 0; cph ^= 1u; }
-                // streamed weights: refill the previous tap's slot (its MMAs finish as these start)
-                if (!resident && w_loaded < my_taps && w_loaded < i * 9 + tap + g.ws) load_w(w_loaded++);
             }
             if (elect_one()) {
                 umma_commit(&a_empty[buf]);
@@ -330,28 +338,42 @@ static TcConv tc_geom(int S, int N_d, int Cin, int Cout, long long n_img) {
     return g;
 }
 
-// smem plan: weights (ws slots) | A ring (na buffers) | bias | barriers.  Deepest A ring
-// first (up to 4), resident weights preferred at equal depth.  Returns bytes or 0.
+// smem plan: weight chunks (ws slots) | A ring (na buffers) | bias | barriers.  Order of
+// preference: resident weights with a double-buffered (or deeper) A ring; streamed weights
+// (>= 4 slots) with >= 2 A buffers; resident with one A buffer; streamed with one.
 static size_t tc_plan(TcConv& g, int CINP, int NP) {
-    const size_t wtap = 2ull * CINP * NP * 4, abuf = 2ull * (CINP / 4) * g.PL;
+    const int KS = CINP == 64 ? 2 : 1;
+    const size_t chunk = 2ull * CINP * NP * 4 / KS, abuf = 2ull * (CINP / 4) * g.PL;
     const size_t limit = 227 * 1024;
-    for (int na = 4; na >= 1; --na)
-        for (int ws : {9, 2}) {
-            const size_t off_a = ws * wtap;
-            const size_t off_bias = off_a + na * abuf;
-            const size_t off_bar = (off_bias + NP * 4 + 15) & ~(size_t)15;
-            const size_t bytes = off_bar + 8 * (4 + 2 * na + 2 * ws) + 16;
-            if (bytes > limit) continue;
-            g.ws = ws;
-            g.na = na;
-            g.off_a = (int)off_a;
-            g.off_bias = (int)off_bias;
-            g.off_bar = (int)off_bar;
-            int cols = 32;
-            while (cols < 4 * NP) cols <<= 1;   // two accumulators of N = 2 NP
-            g.tmem_cols = cols;
-            return bytes;
-        }
+    auto bytes_of = [&](int ws, int na, size_t& off_a, size_t& off_bias, size_t& off_bar) {
+        off_a = ws * chunk;
+        off_bias = off_a + na * abuf;
+        off_bar = (off_bias + NP * 4 + 15) & ~(size_t)15;
+        return off_bar + 8 * (4 + 2 * na + 2 * ws) + 16;
+    };
+    auto take = [&](int ws, int na) -> size_t {
+        size_t oa, ob, obar;
+        const size_t bytes = bytes_of(ws, na, oa, ob, obar);
+        if (bytes > limit) return 0;
+        g.ws = ws;
+        g.na = na;
+        g.off_a = (int)oa;
+        g.off_bias = (int)ob;
+        g.off_bar = (int)obar;
+        int cols = 32;
+        while (cols < 4 * NP) cols <<= 1;   // two accumulators of N = 2 NP
+        g.tmem_cols = cols;
+        return bytes;
+    };
+    size_t r;
+    for (int na = 4; na >= 2; --na)
+        if ((r = take(9 * KS, na))) return r;
+    for (int na = 4; na >= 2; --na)
+        for (int ws = 8; ws >= 4; --ws)
+            if ((r = take(ws, na))) return r;
+    if ((r = take(9 * KS, 1))) return r;
+    for (int ws = 8; ws >= 2; --ws)
+        if ((r = take(ws, 1))) return r;
     return 0;
 }
 

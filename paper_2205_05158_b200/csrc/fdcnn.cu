@@ -3,9 +3,9 @@
 // with tanh, residual output.
 //
 // Three implementations (FP32 results, accurate tanhf, no fast-math):
-//  * k_conv_tc   — tensor-core implicit GEMM per layer, 3xTF32 (conv_tc.cu), used when
-//                  every hidden width is 16, 32 or 64 (C2-C5);
-//  * k_cnn_fused — SIMT, the whole network per image in shared memory (C1);
+//  * k_conv_tc   — tensor-core implicit GEMM per layer, hi/lo-split TF32 (conv_tc.cu),
+//                  used when every hidden width is 16, 32 or 64 and one is >= 32 (C3-C5);
+//  * k_cnn_fused — SIMT, the whole network per image in shared memory (C1, C2);
 //  * k_conv      — SIMT, one layer per launch through HBM activations (other shapes).
 // Plain TF32 would miss the 2e-5 parity bar (the residual is not small against s at
 // C4/C5), hence the hi/lo operand split, see DESIGN.md §6.
@@ -18,10 +18,17 @@ size_t fdcnn_tc_workspace_bytes(const int* chans, int n_layers, long long n_sym,
 int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const float2* s_in, float2* s_out,
                      void* workspace, long long n_sym, int U, int N_d, cudaStream_t stream);
 
-// FD_CNN_AUTO picks the tensor-core path where it applies, else the SIMT kernels.
+// FD_CNN_AUTO picks the tensor-core path where it applies and some hidden width is >= 32
+// (C3-C5); at width 16 (C2) the whole-network SIMT kernel is faster (measured 0.51 vs 1.02 ms
+// per 1024 symbols: an SS-mode MMA costs the same at N = 32 as at N = 128, and the per-layer
+// tensor path pays an HBM round trip per layer).
 static int g_cnn_path = FD_CNN_AUTO;
 static bool use_tc(const int* chans, int n_layers) {
-    return g_cnn_path != FD_CNN_SIMT && tc_supported(chans, n_layers);
+    if (g_cnn_path == FD_CNN_SIMT || !tc_supported(chans, n_layers)) return false;
+    if (g_cnn_path == FD_CNN_TENSOR) return true;
+    int cmax = 0;
+    for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
+    return cmax >= 32;
 }
 
 constexpr int CNN_THREADS = 256;

@@ -140,6 +140,26 @@ __device__ __forceinline__ void pass_load_smem(const float2* sm, float2 (&v)[VPT
         for (int r = 0; r < R; ++r) v[q * R + r] = sm[pidx(pass_pos<R, VPT, T, N>(tid, q, r))];
 }
 
+// Multiplies v[off + r], r = 1..R-1, by the pass twiddle W^{r step}: the power-of-two
+// exponents come from the fp64-derived table (log2 R scattered loads instead of R-1) and
+// the rest from at most three complex products (~3 ulp), e.g. W^7 = (W^1 W^2) W^4.
+template <int R, int DIR, int VPT>
+__device__ __forceinline__ void pass_twiddle(float2 (&v)[VPT], int off, int step, const float2* __restrict__ tw) {
+    float2 wp[R];
+    wp[0] = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int p = 1; p < R; p <<= 1) {
+        float2 w = __ldg(tw + p * step);
+        if (DIR > 0) w.y = -w.y;
+        wp[p] = w;
+    }
+#pragma unroll
+    for (int r = 3; r < R; ++r)
+        if (r & (r - 1)) wp[r] = cmul(wp[r & (r - 1)], wp[r & -r]);   // r = (r without lowest bit) + lowest bit
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[off + r] = cmul(v[off + r], wp[r]);
+}
+
 template <int R, int DIR, int VPT, int T, int N>
 __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT], int Ns, const float2* __restrict__ tw,
                                                    int tid) {
@@ -147,25 +167,7 @@ __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT],
     for (int q = 0; q < VPT / R; ++q) {
         const int j = tid + q * T;
         const int k = j & (Ns - 1);
-        if (Ns > 1) {
-            // W^{r*step}, r = 1..R-1: load the power-of-two exponents from the fp64-derived
-            // table (log2 R scattered loads instead of R-1) and build the rest with at most
-            // three complex products (~3 ulp), e.g. W^7 = (W^1 W^2) W^4.
-            const int step = k * (N / (Ns * R));
-            float2 wp[R];
-            wp[0] = make_float2(1.f, 0.f);
-#pragma unroll
-            for (int p = 1; p < R; p <<= 1) {
-                float2 w = __ldg(tw + p * step);
-                if (DIR > 0) w.y = -w.y;
-                wp[p] = w;
-            }
-#pragma unroll
-            for (int r = 3; r < R; ++r)
-                if (r & (r - 1)) wp[r] = cmul(wp[r & (r - 1)], wp[r & -r]);   // r = (r without lowest bit) + lowest bit
-#pragma unroll
-            for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], wp[r]);
-        }
+        if (Ns > 1) pass_twiddle<R, DIR>(v, q * R, k * (N / (Ns * R)), tw);
         dftR<R, DIR>(v, q * R);
         const int d = (j - k) * R + k;
 #pragma unroll
@@ -173,10 +175,11 @@ __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT],
     }
 }
 
-// Runs passes [1, n_passes) after the caller has filled v with the pass-0 input
-// layout (pass_pos with R = pass_radix(0)).  Leaves the transform (unnormalised)
-// in sm in natural order; ends with __syncthreads().
-template <int LOG2N, int DIR, int P = 0>
+// Runs passes [P, PEND) — P = 0: after the caller has filled v with the pass-0 input
+// layout (pass_pos with R = pass_radix(0)); P > 0: reading the previous pass from sm.
+// With PEND = n_passes the transform (unnormalised) is left in sm in natural order.
+// Ends with __syncthreads().
+template <int LOG2N, int DIR, int P = 0, int PEND = n_passes<LOG2N>()>
 __device__ __forceinline__ void fft_run(float2* sm, float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
                                         const float2* __restrict__ tw, int tid) {
     constexpr int N = 1 << LOG2N;
@@ -189,7 +192,86 @@ __device__ __forceinline__ void fft_run(float2* sm, float2 (&v)[(1 << LOG2N) / f
     }
     pass_compute_store<R, DIR, VPT, T, N>(sm, v, pass_ns<LOG2N>(P), tw, tid);
     __syncthreads();
-    if constexpr (P + 1 < n_passes<LOG2N>()) fft_run<LOG2N, DIR, P + 1>(sm, v, tw, tid);
+    if constexpr (P + 1 < PEND) fft_run<LOG2N, DIR, P + 1, PEND>(sm, v, tw, tid);
+}
+
+// ---------------------------------------------------------------- pruned radix-16 passes
+// The data subcarriers occupy the first and last h = N_d / 2 bins (reading A7).  When
+// h <= N / 8, the radix-16 pass whose 16 points are N/16 apart sees data only in slots
+// r < NZ and r >= 16 - NZ, NZ = ceil(h / (N/16)) <= 2: the IDFT's first pass has at most
+// 4 non-zero inputs per butterfly and the receive DFT's last pass needs at most 4 of its
+// 16 outputs.  Both are computed without the zero / unused arithmetic.
+
+// x * W16^M, W16 = exp(DIR 2 pi i / 16); exact for multiples of 4
+template <int DIR, int M>
+__device__ __forceinline__ float2 cmul_w16(float2 x) {
+    constexpr int m = ((M % 16) + 16) % 16;
+    if constexpr (m == 0) return x;
+    else if constexpr (m == 4) return mul_i<DIR>(x);
+    else if constexpr (m == 8) return make_float2(-x.x, -x.y);
+    else if constexpr (m == 12) return mul_i<-DIR>(x);
+    else return cmul(x, w16(m, DIR));
+}
+
+// sum_{n2} a[n2] (DIR i)^{n2 K2}: one output of a 4-point DFT
+template <int DIR, int K2>
+__device__ __forceinline__ float2 dft4_out(float2 a0, float2 a1, float2 a2, float2 a3) {
+    constexpr int k = K2 & 3;
+    if constexpr (k == 0) return cadd(cadd(a0, a2), cadd(a1, a3));
+    else if constexpr (k == 2) return csub(cadd(a0, a2), cadd(a1, a3));
+    else if constexpr (k == 1) return cadd(csub(a0, a2), mul_i<DIR>(csub(a1, a3)));
+    else return csub(csub(a0, a2), mul_i<DIR>(csub(a1, a3)));
+}
+
+// 16-point DFT (natural order out) of inputs that are zero except x0 = x[0], x15 = x[15]
+// and, for NZ = 2, x1 = x[1], x14 = x[14].  With n = 4 n1 + n2 every n2 column holds one
+// non-zero input, so the first 4-point stage is a twiddle: B[n2](k1) = x W16^{n k1}.
+template <int DIR, int NZ>
+__device__ __forceinline__ void dft16_sparse_in(float2 x0, float2 x1, float2 x14, float2 x15, float2 (&X)[16]) {
+#define FDPD_SPARSE_K1(K1)                                                                     \
+    {                                                                                          \
+        const float2 b0 = x0, b3 = cmul_w16<DIR, 15 * K1>(x15);                               \
+        if constexpr (NZ == 2) {                                                               \
+            const float2 b1 = cmul_w16<DIR, K1>(x1), b2 = cmul_w16<DIR, 14 * K1>(x14);         \
+            X[K1] = dft4_out<DIR, 0>(b0, b1, b2, b3);                                          \
+            X[K1 + 4] = dft4_out<DIR, 1>(b0, b1, b2, b3);                                      \
+            X[K1 + 8] = dft4_out<DIR, 2>(b0, b1, b2, b3);                                      \
+            X[K1 + 12] = dft4_out<DIR, 3>(b0, b1, b2, b3);                                     \
+        } else {                                                                               \
+            const float2 t = mul_i<DIR>(b3);   /* (DIR i)^{3 k2} b3 for k2 = 1 is -t */          \
+            X[K1] = cadd(b0, b3);                                                              \
+            X[K1 + 4] = csub(b0, t);                                                           \
+            X[K1 + 8] = csub(b0, b3);                                                          \
+            X[K1 + 12] = cadd(b0, t);                                                          \
+        }                                                                                      \
+    }
+    FDPD_SPARSE_K1(0)
+    FDPD_SPARSE_K1(1)
+    FDPD_SPARSE_K1(2)
+    FDPD_SPARSE_K1(3)
+#undef FDPD_SPARSE_K1
+}
+
+// Outputs r < NZ and r >= 16 - NZ of the 16-point DFT of v[off .. off+16) (natural order
+// in); v is clobbered.  out[0..NZ) = X[0..NZ), out[NZ..2NZ) = X[16-NZ..16).
+template <int DIR, int NZ, int VPT>
+__device__ __forceinline__ void dft16_sparse_out(float2 (&v)[VPT], int off, float2 (&out)[2 * NZ]) {
+    // n = 4 n1 + n2: 4-point DFTs over n1 -> A[n2][k1] at v[off + 4 k1 + n2]
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<DIR>(v[off + n2], v[off + 4 + n2], v[off + 8 + n2], v[off + 12 + n2]);
+    // X[k1 + 4 k2] = sum_{n2} A[n2][k1] W16^{n2 k1} (DIR i)^{n2 k2}
+#define FDPD_OUT(K1, K2)                                                                        \
+    dft4_out<DIR, K2>(v[off + 4 * K1], cmul_w16<DIR, K1>(v[off + 4 * K1 + 1]),                  \
+                      cmul_w16<DIR, 2 * K1>(v[off + 4 * K1 + 2]), cmul_w16<DIR, 3 * K1>(v[off + 4 * K1 + 3]))
+    out[0] = FDPD_OUT(0, 0);                          // r = 0
+    if constexpr (NZ == 2) {
+        out[1] = FDPD_OUT(1, 0);                      // r = 1
+        out[2] = FDPD_OUT(2, 3);                      // r = 14
+        out[3] = FDPD_OUT(3, 3);                      // r = 15
+    } else {
+        out[1] = FDPD_OUT(3, 3);                      // r = 15
+    }
+#undef FDPD_OUT
 }
 
 // Data-subcarrier index of IDFT bin k (reading A7), or -1 for a guard bin.

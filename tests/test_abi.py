@@ -91,6 +91,10 @@ def test_workspace_queries(lib):
         assert lib.fd_set_cnn_path(2) == 0                               # tensor cores
         act = 2 * 4 * 16 * 8 * 32 * 37 * 37                  # channels-last, zero halo (S + 2)^2
         wsplit = 4 * 9 * 2 * (8 * 32 + 32 * 32 * 2 + 32 * 16)   # hi/lo weight images, padded
-        assert act + wsplit <= lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) < act + wsplit + 4096
+        tc_bytes = lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200)
+        assert act + wsplit <= tc_bytes < act + wsplit + 4096
+        assert lib.fd_set_cnn_path(0) == 0                               # auto: tensor cores from width 32
+        assert lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) == tc_bytes
+        assert lib.fdcnn_workspace_bytes((ctypes.c_int * 4)(2, 16, 16, 2), 3, 1024, 4, 600) == 0
     finally:
         lib.fd_set_cnn_path(0)

@@ -221,11 +221,38 @@ def test_chain_txrx_vs_unfused(F, name):
     s, coef = dev(inp["s"]), dev(inp["coef"])
     y, XPA = F.chain_txrx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
     y_ref = F.chain_tx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
-    assert torch.equal(y, y_ref)
+    # same arithmetic except the pruned first IDFT pass of chain_txrx (rounding-level)
+    assert rel(host(y), host(y_ref)) < 1e-6
     want = np.fft.fft(host(y).astype(np.complex128), axis=-1, norm="ortho")[..., O.data_bins(cfg.N_d, cfg.N_ifft)]
     assert rel(host(XPA), want) < 2e-6
     yhat = F.ue_combine(XPA, h_fd)
     assert rel(host(yhat), host(F.ue_receive(y, h_fd))) < 2e-6
+
+
+@pytest.mark.parametrize("N,N_d,orders,L,M", [
+    (4096, 512, (1, 3, 5, 7), 4, 2),      # h = N/16: one data slot per side (PZ = 1)
+    (4096, 514, (1, 3, 5, 7), 4, 2),      # h = N/16 + 1: second slot holds one bin (PZ = 2)
+    (4096, 1024, (1, 3, 5, 7), 3, 1),     # h = N/8: the largest pruned case
+    (4096, 1026, (1, 3, 5, 7), 4, 2),     # h > N/8: generic passes
+    (4096, 384, (1, 3, 5, 7), 3, 1),      # the paper's shape (PZ = 1)
+    (8192, 1200, (1, 3, 5, 7), 4, 2),     # N = 2 * 16^3: pruned IDFT pass only
+    (16384, 3300, (1, 3, 5, 7, 9), 6, 3)])
+def test_chain_txrx_pruned_fft(F, N, N_d, orders, L, M):
+    """Pruned radix-16 passes (first IDFT pass, last receive-DFT pass) against the oracle's
+    precode -> IDFT -> GMP and the fp64 FFT of the returned waveform at the data bins."""
+    rng = np.random.default_rng(N + N_d)
+    B, U, n = 3, 2, 2
+    Kp = len(orders)
+    ncoef = Kp * (L + 1) + 2 * (Kp - 1) * (L + 1) * M
+    P = crandn(rng, B, U, N_d, scale=0.5)
+    s = crandn(rng, n, U, N_d)
+    coef = crandn(rng, B, ncoef, scale=0.05)
+    coef[:, 0] = 1.0
+    y, XPA = F.chain_txrx(dev(P), dev(s), dev(coef), orders, L, M, N)
+    x = O.ofdm_modulate(O.precode(P.transpose(2, 0, 1), s), N)
+    assert rel(host(y), O.gmp_pa(x, coef, orders, L, M)) < TOL
+    want = np.fft.fft(host(y).astype(np.complex128), axis=-1, norm="ortho")[..., O.data_bins(N_d, N)]
+    assert rel(host(XPA), want) < 2e-6
 
 
 @pytest.mark.parametrize("orders,L,M", [((1, 5, 9), 3, 0), ((1, 3), 1, 1)])
