@@ -133,10 +133,93 @@ __global__ void __launch_bounds__(128) k_rx_combine(const float2* __restrict__ X
     if (SER) add_counts(counts, err, near, cnt);
 }
 
+// Register-blocked variant for a single channel realisation: a thread owns subcarrier j of
+// NS consecutive symbols and UC users at a time, so each h_fd value fetched from L2 feeds NS
+// symbols and each XPA value UC users (the simple kernel above re-reads XPA per user and
+// h_fd per symbol: ~4x the L2 traffic).  Same summation order over b as k_rx_combine.
+template <bool SER, bool AWGN, int UC, int NS>
+__global__ void __launch_bounds__(128) k_rx_combine_blk(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
+                                                        float2* __restrict__ yhat, int B, int U, int N_d,
+                                                        long long n_sym, int accumulate,
+                                                        const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
+                                                        long long* counts, SliceParams sp, Impair imp) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n0 = (long long)blockIdx.y * NS;
+    int err = 0, near = 0, cnt = 0;
+    if (j < N_d) {
+        const float2* Xc[NS];
+        bool nok[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            nok[s] = n0 + s < n_sym;
+            Xc[s] = XPA + (size_t)(nok[s] ? n0 + s : n0) * B * N_d + j;
+        }
+        for (int u0 = 0; u0 < U; u0 += UC) {
+            float2 acc[NS][UC];
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+#pragma unroll
+                for (int c = 0; c < UC; ++c) acc[s][c] = make_float2(0.f, 0.f);
+            const float2* H = hfd + (size_t)u0 * B * N_d + j;
+#pragma unroll 2
+            for (int b = 0; b < B; ++b) {
+                float2 hv[UC], xv[NS];
+#pragma unroll
+                for (int c = 0; c < UC; ++c)
+                    hv[c] = (u0 + c < U) ? __ldg(H + ((size_t)c * B + b) * N_d) : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int s = 0; s < NS; ++s) xv[s] = __ldg(Xc[s] + (size_t)b * N_d);
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+#pragma unroll
+                    for (int c = 0; c < UC; ++c) acc[s][c] = cfma(hv[c], xv[s], acc[s][c]);
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (!nok[s]) continue;
+                const long long n = n0 + s;
+#pragma unroll
+                for (int c = 0; c < UC; ++c) {
+                    const int u = u0 + c;
+                    if (u >= U) continue;
+                    const size_t o = ((size_t)n * U + u) * N_d + j;
+                    float2 a = acc[s][c];
+                    if (accumulate) a = cadd(a, yhat[o]);
+                    if constexpr (AWGN)
+                        a = cadd(a, cgauss((unsigned long long)((imp.sym0 + n) * U + u) * N_d + j, STREAM_AWGN,
+                                           imp.key_lo, imp.key_hi, imp.awgn_std));
+                    yhat[o] = a;
+                    if constexpr (SER) {
+                        bool nr = false;
+                        const int di = slice_axis(a.x * sp.inv_ac, sp, nr);
+                        const int dq = slice_axis(a.y * sp.inv_ac, sp, nr);
+                        const int dd = di + sp.m * dq;
+                        if (dec) dec[o] = (uint16_t)dd;
+                        err += (dd != (int)idx[o]);
+                        near += nr;
+                        ++cnt;
+                    }
+                }
+            }
+        }
+    }
+    if (SER) add_counts(counts, err, near, cnt);
+}
+
 template <bool SER, bool AWGN>
 static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d, long long n_sym,
                            int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
                            const SliceParams& sp, const Impair& imp, cudaStream_t st) {
+    if (imp.h_stride == 0 && imp.alpha_dev == nullptr) {
+        auto go = [&](auto kern, int ns) {
+            dim3 g((N_d + 127) / 128, (unsigned)((n_sym + ns - 1) / ns));
+            kern<<<g, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, imp);
+        };
+        if (U <= 2) go(k_rx_combine_blk<SER, AWGN, 2, 4>, 4);
+        else if (U <= 4) go(k_rx_combine_blk<SER, AWGN, 4, 4>, 4);
+        else go(k_rx_combine_blk<SER, AWGN, 8, 2>, 2);
+        return;
+    }
     dim3 grid((N_d + 127) / 128, (unsigned)n_sym);
     if (imp.h_stride != 0 || imp.alpha_dev != nullptr)
         k_rx_combine<SER, AWGN, true><<<grid, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, accumulate, idx, dec, counts, sp,
