@@ -225,7 +225,8 @@ def run_ours(args, cfg):
                impair=impair)
     torch.cuda.synchronize()
     t_zf = time.perf_counter() - t_zf0
-    ch.split_precode = args.split_precode
+    if args.split_precode:
+        ch.split_precode = True
     native = fdpd.NativeChain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], max_batch=n,
                               device=dev)
 

@@ -188,6 +188,8 @@ int chain_txrx_ex(const void* P, const void* s_tilde, const void* coef, void* y,
 /* chain_txrx on an already precoded spectrum X [n_sym][B_loc][N_d] (the output of precode):
  * the split precode -> chain_txrx_pre moves the U-fold L2 gather of P_b and s_n out of the
  * fused kernel's prologue into one bandwidth-bound kernel.  imp nullable. */
+/* Native-runtime / binding policy: from this many users a step runs precode -> chain_txrx_pre. */
+#define FD_SPLIT_PRECODE_MIN_U 16
 int chain_txrx_pre(const void* X, const void* coef, void* y, void* XPA, const int* orders, int n_orders,
                    int L, int M, long long n_sym, int B_loc, int N_d, int N_ifft, const fd_impair* imp,
                    cudaStream_t stream);

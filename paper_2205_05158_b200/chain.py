@@ -53,6 +53,10 @@ class Chain:
         self.coef = torch.as_tensor(coef).to(dev, torch.complex64)[b0:b0 + self.B_loc].contiguous()
         self.params = torch.as_tensor(params).to(dev, torch.float32).contiguous()
         self.impair = dict(impair) if impair else None
+        # precode as its own tiled kernel (then chain_txrx_pre) from U >= 16: the fused prologue
+        # gathers U P_b and s_n rows per (symbol, antenna) CTA from L2, which dominates at
+        # C4/C5 (measured: C4 17.7 -> 13.8 ms, C5 11.5 -> 7.4 ms) but not at C2/C3 (U <= 8)
+        self.split_precode = shapes.U >= fdpd.SPLIT_PRECODE_MIN_U
         # a2, once per channel realisation
         if self.impair and self.impair.get("csi_eta", 0.0) > 0:
             h_err = torch.as_tensor(self.impair["h_err"]).to(dev, torch.complex64).contiguous()
@@ -109,7 +113,7 @@ class Chain:
         n = s_tilde.shape[0]
         sh = self.sh
         XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
-        if getattr(self, "split_precode", False):
+        if self.split_precode:
             # precode as its own bandwidth-bound kernel, then the fused chain on X
             if getattr(self, "X", None) is None or self.X.shape[0] < n:
                 self.X = torch.empty((max(n, self.cap), self.B_loc, sh.N_d), dtype=torch.complex64,

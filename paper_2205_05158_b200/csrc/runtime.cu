@@ -19,6 +19,7 @@ struct fd_chain {
     float2 *h_taps = nullptr, *coef = nullptr, *h_fd = nullptr, *P = nullptr;
     float* params = nullptr;
     float2 *s = nullptr, *s_tilde = nullptr, *y = nullptr, *XPA = nullptr, *yhat = nullptr;
+    float2* X = nullptr;   // precoded spectrum [cap][B][N_d] when U >= FD_SPLIT_PRECODE_MIN_U
     uint16_t* idx = nullptr;
     long long* counts = nullptr;
     void* ws_cnn = nullptr;
@@ -45,7 +46,7 @@ int dalloc(T** p, size_t n) {
 void release(fd_chain* c) {
     if (!c) return;
     void* ptrs[] = {c->h_taps, c->coef, c->h_fd, c->P, c->params, c->s, c->s_tilde, c->y,
-                    c->XPA, c->yhat, c->idx, c->counts, c->ws_cnn, c->ws_zf};
+                    c->XPA, c->yhat, c->idx, c->counts, c->ws_cnn, c->ws_zf, c->X};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_in)
@@ -58,10 +59,10 @@ void release(fd_chain* c) {
 int ensure_batch(fd_chain* c, long long n) {
     if (n <= c->cap) return FD_OK;
     const fd_chain_desc& d = c->d;
-    void* old[] = {c->s, c->s_tilde, c->y, c->XPA, c->yhat, c->idx, c->ws_cnn};
+    void* old[] = {c->s, c->s_tilde, c->y, c->XPA, c->yhat, c->idx, c->ws_cnn, c->X};
     for (void* p : old)
         if (p) cudaFree(p);
-    c->s = c->s_tilde = c->y = c->XPA = c->yhat = nullptr;
+    c->s = c->s_tilde = c->y = c->XPA = c->yhat = c->X = nullptr;
     c->idx = nullptr;
     c->ws_cnn = nullptr;
     int rc;
@@ -70,6 +71,7 @@ int ensure_batch(fd_chain* c, long long n) {
     if ((rc = dalloc(&c->y, (size_t)n * d.B * d.N_ifft))) return rc;
     if ((rc = dalloc(&c->XPA, (size_t)n * d.B * d.N_d))) return rc;
     if ((rc = dalloc(&c->yhat, (size_t)n * d.U * d.N_d))) return rc;
+    if (d.U >= FD_SPLIT_PRECODE_MIN_U && (rc = dalloc(&c->X, (size_t)n * d.B * d.N_d))) return rc;
     if ((rc = dalloc(&c->idx, (size_t)n * d.U * d.N_d))) return rc;
     c->ws_cnn_bytes = d.head == 1 ? fdcnn_paper_workspace_bytes(d.n_conv, n, d.U, d.N_d)
                                   : fdcnn_workspace_bytes(d.chans, d.n_layers, n, d.U, d.N_d);
@@ -91,8 +93,17 @@ int run_chunk(fd_chain* c, const void* s, const uint16_t* tx_idx, long long s0, 
                                          d.N_d, stream);
     if (rc) return rc;
     float2* XPA = c->XPA + s0 * pb;
-    rc = chain_txrx(c->P, st, c->coef, c->y + s0 * py, XPA, d.orders, d.n_orders, d.L, d.M, n, d.B, d.U, d.N_d,
-                    d.N_ifft, stream);
+    if (c->X) {
+        // many users: tiled precode kernel, then the chain on the precoded spectrum
+        float2* X = c->X + s0 * pb;
+        rc = precode(c->P, st, X, n, d.B, d.U, d.N_d, stream);
+        if (rc) return rc;
+        rc = chain_txrx_pre(X, c->coef, c->y + s0 * py, XPA, d.orders, d.n_orders, d.L, d.M, n, d.B, d.N_d, d.N_ifft,
+                            nullptr, stream);
+    } else {
+        rc = chain_txrx(c->P, st, c->coef, c->y + s0 * py, XPA, d.orders, d.n_orders, d.L, d.M, n, d.B, d.U, d.N_d,
+                        d.N_ifft, stream);
+    }
     if (rc) return rc;
     return ue_combine_ser(XPA, c->h_fd, yhat ? yhat : (void*)(c->yhat + s0 * pu), c->alpha, tx_idx, d.M_qam, nullptr,
                           counts, n, d.B, d.U, d.N_d, d.boundary_eps, stream);

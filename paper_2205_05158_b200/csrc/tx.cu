@@ -22,6 +22,63 @@ __global__ void k_precode(const float2* __restrict__ P, const float2* __restrict
     }
 }
 
+// Tiled form used by the product path.  Per data subcarrier j the contraction is a small
+// complex GEMM X_j[n][b] = sum_u s_j[n][u] P_j[b][u] (K = U); the naive kernel above re-reads
+// P_b for every symbol and s_n for every antenna (U-fold L2 gathers per output).  Here a CTA
+// owns 32 consecutive subcarriers (lane = j: coalesced 256-byte rows) x NT symbols x a range
+// of antennas: s_n for its NT symbols is staged once in shared memory ([NT][U][32], reused by
+// every antenna), and each thread accumulates NT x BPT outputs, so a P value fetched from L2
+// feeds NT symbols and an s value from shared memory BPT antennas.  The u summation order
+// (ascending, one complex FMA per term) is the same as k_precode and the fused chains.
+constexpr int PC_NT = 8, PC_BPT = 4, PC_WARPS = 8;
+template <int NT, int BPT>
+__global__ void __launch_bounds__(32 * PC_WARPS) k_precode_tile(const float2* __restrict__ P, const float2* __restrict__ s,
+                                                                float2* __restrict__ X, long long n_sym, int B, int U,
+                                                                int N_d, int b_per_cta) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* ssm = reinterpret_cast<float2*>(smem_raw);   // [NT][U][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + lane;
+    const bool jok = j < N_d;
+    const long long n0 = (long long)blockIdx.y * NT;
+    const int nt = (int)min((long long)NT, n_sym - n0);
+    for (int e = threadIdx.x; e < NT * U * 32; e += blockDim.x) {
+        const int l = e & 31, r = e >> 5, u = r % U, n = r / U;
+        const int jj = blockIdx.x * 32 + l;
+        ssm[e] = (n < nt && jj < N_d) ? __ldg(s + ((size_t)(n0 + n) * U + u) * N_d + jj) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    const int b_begin = blockIdx.z * b_per_cta, b_end = min(B, b_begin + b_per_cta);
+    for (int b0 = b_begin + warp * BPT; b0 < b_end; b0 += PC_WARPS * BPT) {
+        float2 acc[NT][BPT];
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int t = 0; t < BPT; ++t) acc[n][t] = make_float2(0.f, 0.f);
+        const float2* Pb = P + (size_t)b0 * U * N_d + (jok ? j : 0);
+#pragma unroll 2
+        for (int u = 0; u < U; ++u) {
+            float2 pv[BPT];
+#pragma unroll
+            for (int t = 0; t < BPT; ++t)
+                pv[t] = (b0 + t < b_end) ? __ldg(Pb + ((size_t)t * U + u) * N_d) : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const float2 sv = ssm[(n * U + u) * 32 + lane];
+#pragma unroll
+                for (int t = 0; t < BPT; ++t) acc[n][t] = cfma(pv[t], sv, acc[n][t]);
+            }
+        }
+        if (jok) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int t = 0; t < BPT; ++t)
+                    if (n < nt && b0 + t < b_end) X[((size_t)(n0 + n) * B + b0 + t) * N_d + j] = acc[n][t];
+        }
+    }
+}
+
 // ============================================================================ helpers
 // Fill the pass-0 registers with the precoded spectrum X = P_b s_n at data bins, 0 on guards.
 template <int LOG2N>
@@ -201,8 +258,18 @@ int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, i
     if (total == 0) return FD_OK;
     FD_REQUIRE(P && s && X, "precode: NULL pointer");
     FD_REQUIRE(aligned8(P) && aligned8(s) && aligned8(X), "precode: pointers must be 8-byte aligned");
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-    k_precode<<<blocks, 256, 0, stream>>>((const float2*)P, (const float2*)s, (float2*)X, n_sym, B_loc, U, N_d);
+    FD_REQUIRE(n_sym <= 65535LL * PC_NT, "precode: n_sym=%lld too large per call", n_sym);
+    const size_t smem = sizeof(float2) * PC_NT * U * 32;
+    FD_REQUIRE(smem <= 200 * 1024, "precode: U=%d too large for the staged tile", U);
+    // antenna split over grid.z so that even a short batch gives >= ~2 waves of CTAs
+    const long long xy = (long long)((N_d + 31) / 32) * ((n_sym + PC_NT - 1) / PC_NT);
+    int zc = 1;
+    while (xy * zc < 2 * 148 * 4 && B_loc / (zc * 2) >= PC_WARPS * PC_BPT) zc *= 2;
+    const int bpc = (B_loc + zc - 1) / zc;
+    set_smem(k_precode_tile<PC_NT, PC_BPT>, smem);
+    dim3 grid((N_d + 31) / 32, (unsigned)((n_sym + PC_NT - 1) / PC_NT), zc);
+    k_precode_tile<PC_NT, PC_BPT><<<grid, 32 * PC_WARPS, smem, stream>>>((const float2*)P, (const float2*)s,
+                                                                        (float2*)X, n_sym, B_loc, U, N_d, bpc);
     return check_launch("precode");
 }
 

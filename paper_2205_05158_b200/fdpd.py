@@ -141,6 +141,9 @@ def _ws(nbytes, like):
 
 # ----------------------------------------------------------------------------- a1
 CNN_AUTO, CNN_SIMT, CNN_TENSOR = 0, 1, 2
+# FD_SPLIT_PRECODE_MIN_U of include/fdpd.h: from this many users the chain runs precode ->
+# chain_txrx_pre instead of the fused-prologue chain_txrx (same policy as the native runtime)
+SPLIT_PRECODE_MIN_U = 16
 
 
 def set_cnn_path(path: int):

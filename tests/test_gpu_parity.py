@@ -196,6 +196,19 @@ def test_precode(F, name):
     assert rel(got, O.precode(P.transpose(2, 0, 1), s)) < TOL
 
 
+@pytest.mark.parametrize("n,B,U,Nd", [(11, 512, 32, 3300), (9, 37, 5, 70), (1, 8, 2, 36), (17, 256, 16, 3300),
+                                      (64, 64, 4, 600)])
+def test_precode_tiles_ragged(F, n, B, U, Nd):
+    """Tiled precode over ragged symbol / antenna / subcarrier tiles (NT = 8, 4 antennas per
+    thread, 32 subcarriers per CTA) against the oracle contraction."""
+    rng = np.random.default_rng(n * 7 + B)
+    P = crandn(rng, B, U, Nd)
+    s = crandn(rng, n, U, Nd)
+    got = host(F.precode(dev(P), dev(s)))
+    assert got.shape == (n, B, Nd)
+    assert rel(got, O.precode(P.transpose(2, 0, 1), s)) < TOL
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_chain_tx_vs_oracle_and_unfused(F, name):
     cfg = configs.get(name)
