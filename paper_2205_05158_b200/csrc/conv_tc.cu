@@ -136,18 +136,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
             if constexpr (IN_MODE == 0) {
                 const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP);
-                for (int e = lt; e < g.A_px * G; e += TC_LOAD_THREADS) {
-                    const int p = e / G, gq = e - p * G;
-                    const int pos = qa + p;
-                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (pos >= 0 && pos < g.P) x = __ldg(src + (size_t)pos * G + gq);
-                    float4 hi, lo;
-                    hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
-                    hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
-                    hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
-                    hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
-                    *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
-                    *reinterpret_cast<float4*>(ab + (size_t)(G + gq) * g.PL + p * 16) = lo;
+                // PB independent 16-byte loads in flight per thread before any split / store
+                // (one global round trip per PB elements instead of one per element)
+                constexpr int PB = 8;
+                const int ne = g.A_px * G;
+                for (int e0 = lt; e0 < ne; e0 += PB * TC_LOAD_THREADS) {
+                    float4 x[PB];
+#pragma unroll
+                    for (int k = 0; k < PB; ++k) {
+                        const int e = e0 + k * TC_LOAD_THREADS;
+                        const int p = e / G, gq = e - p * G;
+                        const int pos = qa + p;
+                        x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (e < ne && pos >= 0 && pos < g.P) x[k] = __ldg(src + (size_t)pos * G + gq);
+                    }
+#pragma unroll
+                    for (int k = 0; k < PB; ++k) {
+                        const int e = e0 + k * TC_LOAD_THREADS;
+                        if (e >= ne) break;
+                        const int p = e / G, gq = e - p * G;
+                        float4 hi, lo;
+                        hi.x = tf32_rna(x[k].x); lo.x = tf32_rna(x[k].x - hi.x);
+                        hi.y = tf32_rna(x[k].y); lo.y = tf32_rna(x[k].y - hi.y);
+                        hi.z = tf32_rna(x[k].z); lo.z = tf32_rna(x[k].z - hi.z);
+                        hi.w = tf32_rna(x[k].w); lo.w = tf32_rna(x[k].w - hi.w);
+                        *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
+                        *reinterpret_cast<float4*>(ab + (size_t)(G + gq) * g.PL + p * 16) = lo;
+                    }
                 }
             } else {
                 // symbols: channel 0 = Re, 1 = Im of s[y S + x] (zero beyond N_d and on the halo)
