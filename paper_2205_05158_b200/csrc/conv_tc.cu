@@ -64,23 +64,38 @@ __global__ void k_tc_weights(const float* __restrict__ W, float* __restrict__ Wg
 }
 
 // Warp roles (no CTA-wide barrier inside the tile loop; mbarrier pipelines between roles):
-//   warps 0-3   epilogue: TMEM lane quadrant w (pixels 32w..32w+31) x all columns
-//   warps 4-11  A producers: load, split hi/lo, store the tile's A planes
-//   warp 12     one thread: weight TMA (resident or a ring of per-tap slots) + MMA issue
-// Rings: A buffers (na) with a_full (256 arrivals) / a_empty (tcgen05.commit), two TMEM
-// accumulators with acc_full (commit) / acc_empty (128 arrivals).
-constexpr int TC_EPI_WARPS = 4, TC_LOAD_WARPS = 8;
-constexpr int TC_THREADS = 32 * (TC_EPI_WARPS + TC_LOAD_WARPS + 1);
+//   warps 0-7   epilogue: TMEM lane quadrant (w % 4) (pixels 32(w%4)..+31) x column half w / 4
+//   warps 8-15  A producers: load, split hi/lo, store one K chunk (CK input channels) of a tile
+//   warp 16     MMA issue (descriptors advanced by uniform adds; one elected lane issues)
+//   warp 17     weight TMA: all slices resident (loaded once) or a ring of (chunk, tap) slices
+// The A operand is staged per K chunk of CK = min(Cin, 32) channels (hi and lo planes), so a
+// 64-channel layer keeps two A chunks in flight next to a 5-slot weight ring, where the
+// whole-tile A staging (131 KB) left room for one A buffer and two weight slots.  The MMA
+// warp does nothing but wait, issue and commit: it is latency-bound on its own instruction
+// stream (measured: a ~100-instruction bookkeeping sequence per weight slice dominated the
+// MMA warp's samples), so weight loads live in their own warp and each slice carries 8 MMAs.
+// Rings: A chunks (na) with a_full (256 arrivals) / a_empty (tcgen05.commit), weight slices
+// (ws) with wfull (TMA bytes) / wempty (commit), two TMEM accumulators with acc_full
+// (commit) / acc_empty (256 arrivals).
+constexpr int TC_EPI_WARPS = 8, TC_LOAD_WARPS = 8;
+constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_LOAD_WARPS, TC_W_WARP = TC_MMA_WARP + 1;
+constexpr int TC_THREADS = 32 * (TC_W_WARP + 1);
 constexpr int TC_LOAD_THREADS = 32 * TC_LOAD_WARPS;
+constexpr int TC_EPI_THREADS = 32 * TC_EPI_WARPS;
+
+__host__ __device__ constexpr int tc_ck(int cinp) { return cinp >= 32 ? 32 : cinp; }
 
 template <int CINP, int NP, int IN_MODE, int OUT_MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const float* __restrict__ Wg,
               const float* __restrict__ bias, float* __restrict__ act_out, float2* __restrict__ s_out, TcConv g) {
-    constexpr int G = CINP / 4;           // 16-byte channel groups (planes) per hi / lo
-    constexpr int KSTEPS = CINP / 8;      // K = 8 steps per tap (two MMAs each: A_hi, A_lo)
-    constexpr int KS = CINP == 64 ? 2 : 1;   // weight chunks per tap
-    constexpr uint32_t CBYTES = 2u * CINP * NP * 4u / KS;
+    constexpr int G = CINP / 4;           // 16-byte channel groups of a pixel in global memory
+    constexpr int CK = tc_ck(CINP);       // input channels per K chunk
+    constexpr int NCH = CINP / CK;        // K chunks per tile
+    constexpr int GC = CK / 4;            // 16-byte planes per hi / lo of one chunk
+    constexpr int KSC = CK / 8;           // K = 8 steps per chunk (two MMAs each: A_hi, A_lo)
+    constexpr int NW = 9 * NCH;           // weight slices per tile, order (chunk, tap)
+    constexpr uint32_t WCB = (uint32_t)CK * 2 * NP * 4;   // bytes per weight slice
     constexpr uint32_t IDESC = idesc_tf32_m128(2 * NP);
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -94,12 +109,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + g.ws);
     float* bsm = reinterpret_cast<float*>(sm + g.off_bias);
     const uint32_t sm_base = smem_u32(sm);
-    const uint32_t abytes = 2u * G * g.PL;
+    const uint32_t abytes = 2u * GC * g.PL;
 
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 32 * TC_EPI_WARPS);
+            mbar_init(&acc_empty[i], TC_EPI_THREADS);
         }
         for (int i = 0; i < g.na; ++i) {
             mbar_init(&a_full[i], TC_LOAD_THREADS);
@@ -124,148 +139,148 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     if (warp >= TC_EPI_WARPS && warp < TC_EPI_WARPS + TC_LOAD_WARPS) {
         // ------------------------------------------------------------ A producers
-        const int lt = tid - 32 * TC_EPI_WARPS;
-        int buf = 0;
+        const int lt = tid - TC_EPI_THREADS;
+        int buf = 0, n_staged = 0;
         uint32_t ph = 0;
         int img = (int)blockIdx.x / g.n_tiles, t = (int)blockIdx.x - img * g.n_tiles;
         const int dimg = (int)gridDim.x / g.n_tiles, dt = (int)gridDim.x - dimg * g.n_tiles;
         for (int i = 0; i < my_tiles; ++i) {
-            if (i >= g.na) mbar_wait(&a_empty[buf], ph ^ 1u);
             const int q0 = g.q_begin + t * TC_M;
             const int qa = q0 - g.Wp - 1;
-            unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
-            if constexpr (IN_MODE == 0) {
-                const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP);
-                // PB independent 16-byte loads in flight per thread before any split / store
-                // (one global round trip per PB elements instead of one per element)
-                constexpr int PB = 8;
-                const int ne = g.A_px * G;
-                for (int e0 = lt; e0 < ne; e0 += PB * TC_LOAD_THREADS) {
-                    float4 x[PB];
+            for (int c = 0; c < NCH; ++c, ++n_staged) {
+                if (n_staged >= g.na) mbar_wait(&a_empty[buf], ph ^ 1u);
+                unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
+                if constexpr (IN_MODE == 0) {
+                    const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP) + c * GC;
+                    // PB independent 16-byte loads in flight per thread before any split / store
+                    constexpr int PB = 8;
+                    const int ne = g.A_px * GC;
+                    for (int e0 = lt; e0 < ne; e0 += PB * TC_LOAD_THREADS) {
+                        float4 x[PB];
 #pragma unroll
-                    for (int k = 0; k < PB; ++k) {
-                        const int e = e0 + k * TC_LOAD_THREADS;
-                        const int p = e / G, gq = e - p * G;
+                        for (int k = 0; k < PB; ++k) {
+                            const int e = e0 + k * TC_LOAD_THREADS;
+                            const int p = e / GC, gq = e - p * GC;
+                            const int pos = qa + p;
+                            x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (e < ne && pos >= 0 && pos < g.P) x[k] = __ldg(src + (size_t)pos * G + gq);
+                        }
+#pragma unroll
+                        for (int k = 0; k < PB; ++k) {
+                            const int e = e0 + k * TC_LOAD_THREADS;
+                            if (e >= ne) break;
+                            const int p = e / GC, gq = e - p * GC;
+                            float4 hi, lo;
+                            hi.x = tf32_rna(x[k].x); lo.x = tf32_rna(x[k].x - hi.x);
+                            hi.y = tf32_rna(x[k].y); lo.y = tf32_rna(x[k].y - hi.y);
+                            hi.z = tf32_rna(x[k].z); lo.z = tf32_rna(x[k].z - hi.z);
+                            hi.w = tf32_rna(x[k].w); lo.w = tf32_rna(x[k].w - hi.w);
+                            *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
+                            *reinterpret_cast<float4*>(ab + (size_t)(GC + gq) * g.PL + p * 16) = lo;
+                        }
+                    }
+                } else {
+                    // symbols: channel 0 = Re, 1 = Im of s[y S + x] (zero beyond N_d and on the halo)
+                    const float2* simg = s_in + (size_t)img * g.N_d;
+                    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int p = lt; p < g.A_px; p += TC_LOAD_THREADS) {
                         const int pos = qa + p;
-                        x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (e < ne && pos >= 0 && pos < g.P) x[k] = __ldg(src + (size_t)pos * G + gq);
-                    }
+                        float2 z = make_float2(0.f, 0.f);
+                        if (pos >= 0 && pos < g.P) {
+                            const int row = pos / g.Wp;
+                            const int y = row - 1, x = pos - row * g.Wp - 1;
+                            const int k = y * g.S + x;
+                            if (y >= 0 && y < g.S && x >= 0 && x < g.S && k < g.N_d) z = __ldg(simg + k);
+                        }
+                        const float hx = tf32_rna(z.x), hy = tf32_rna(z.y);
+                        *reinterpret_cast<float4*>(ab + p * 16) = make_float4(hx, hy, 0.f, 0.f);
+                        *reinterpret_cast<float4*>(ab + (size_t)GC * g.PL + p * 16) =
+                            make_float4(tf32_rna(z.x - hx), tf32_rna(z.y - hy), 0.f, 0.f);
 #pragma unroll
-                    for (int k = 0; k < PB; ++k) {
-                        const int e = e0 + k * TC_LOAD_THREADS;
-                        if (e >= ne) break;
-                        const int p = e / G, gq = e - p * G;
-                        float4 hi, lo;
-                        hi.x = tf32_rna(x[k].x); lo.x = tf32_rna(x[k].x - hi.x);
-                        hi.y = tf32_rna(x[k].y); lo.y = tf32_rna(x[k].y - hi.y);
-                        hi.z = tf32_rna(x[k].z); lo.z = tf32_rna(x[k].z - hi.z);
-                        hi.w = tf32_rna(x[k].w); lo.w = tf32_rna(x[k].w - hi.w);
-                        *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
-                        *reinterpret_cast<float4*>(ab + (size_t)(G + gq) * g.PL + p * 16) = lo;
+                        for (int gq = 1; gq < GC; ++gq) {
+                            *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = z4;
+                            *reinterpret_cast<float4*>(ab + (size_t)(GC + gq) * g.PL + p * 16) = z4;
+                        }
                     }
                 }
-            } else {
-                // symbols: channel 0 = Re, 1 = Im of s[y S + x] (zero beyond N_d and on the halo)
-                const float2* simg = s_in + (size_t)img * g.N_d;
-                const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (int p = lt; p < g.A_px; p += TC_LOAD_THREADS) {
-                    const int pos = qa + p;
-                    float2 z = make_float2(0.f, 0.f);
-                    if (pos >= 0 && pos < g.P) {
-                        const int row = pos / g.Wp;
-                        const int y = row - 1, x = pos - row * g.Wp - 1;
-                        const int k = y * g.S + x;
-                        if (y >= 0 && y < g.S && x >= 0 && x < g.S && k < g.N_d) z = __ldg(simg + k);
-                    }
-                    const float hx = tf32_rna(z.x), hy = tf32_rna(z.y);
-                    *reinterpret_cast<float4*>(ab + p * 16) = make_float4(hx, hy, 0.f, 0.f);
-                    *reinterpret_cast<float4*>(ab + (size_t)G * g.PL + p * 16) =
-                        make_float4(tf32_rna(z.x - hx), tf32_rna(z.y - hy), 0.f, 0.f);
-#pragma unroll
-                    for (int gq = 1; gq < G; ++gq) {
-                        *reinterpret_cast<float4*>(ab + (size_t)gq * g.PL + p * 16) = z4;
-                        *reinterpret_cast<float4*>(ab + (size_t)(G + gq) * g.PL + p * 16) = z4;
-                    }
-                }
+                fence_proxy_async();                 // generic smem writes -> tensor-core reads
+                mbar_arrive(&a_full[buf]);
+                if (++buf == g.na) { buf = 0; ph ^= 1u; }
             }
-            fence_proxy_async();                 // generic smem writes -> tensor-core reads
-            mbar_arrive(&a_full[buf]);
-            if (++buf == g.na) { buf = 0; ph ^= 1u; }
             img += dimg;
             t += dt;
             if (t >= g.n_tiles) { t -= g.n_tiles; ++img; }
         }
-    } else if (warp == TC_EPI_WARPS + TC_LOAD_WARPS) {
-        // ------------------------------------------------------------ weights + MMA issue
-        // The whole warp walks the loop with identical (warp-uniform) values, so the
-        // descriptors live in uniform registers; one elected lane issues each instruction.
-        // weight chunks: KS per tap (K halves for CINP = 64), CBYTES each; either all 9 KS
-        // chunks resident (loaded once) or a ring of ws slots refilled ws - 1 chunks ahead
-        const int my_chunks = 9 * KS * my_tiles;
-        int lslot = 0, cslot = 0, w_loaded = 0;
-        uint32_t lph = 0, cph = 0;
-        auto load_w = [&](int idx) {
+    } else if (warp == TC_W_WARP) {
+        // ------------------------------------------------------------ weight slices (TMA)
+        const int my_slices = NW * my_tiles;
+        const bool resident = g.ws == NW;
+        const int n_load = resident ? (my_slices > 0 ? NW : 0) : my_slices;
+        int lslot = 0, sl = 0;
+        uint32_t lph = 0;
+        for (int idx = 0; idx < n_load; ++idx) {
             if (idx >= g.ws) mbar_wait(&wempty[lslot], lph ^ 1u);
             if (elect_one()) {
-                mbar_arrive_expect_tx(&wfull[lslot], CBYTES);
-                tma_bulk_g2s(sm + (size_t)lslot * CBYTES, Wg + (size_t)(idx % (9 * KS)) * (CBYTES / 4), CBYTES,
+                const int c = sl / 9, tap = sl - 9 * c;
+                mbar_arrive_expect_tx(&wfull[lslot], WCB);
+                tma_bulk_g2s(sm + (size_t)lslot * WCB, Wg + (size_t)tap * CINP * 2 * NP + (size_t)c * CK * 2 * NP, WCB,
                              &wfull[lslot]);
             }
             __syncwarp();
             if (++lslot == g.ws) { lslot = 0; lph ^= 1u; }
-        };
-        const bool resident = g.ws == 9 * KS;
-        const int first = resident ? (my_chunks > 0 ? 9 * KS : 0) : (my_chunks < g.ws ? my_chunks : g.ws);
-        for (; w_loaded < first; ++w_loaded) load_w(w_loaded);
-        const uint32_t PL = (uint32_t)g.PL;
-        int buf = 0, used = 0;
-        uint32_t aph = 0;
+            if (++sl == NW) sl = 0;
+        }
+    } else if (warp == TC_MMA_WARP) {
+        // ------------------------------------------------------------ MMA issue
+        const bool resident = g.ws == NW;
+        const uint32_t PL16 = (uint32_t)g.PL >> 4, WP = (uint32_t)g.Wp;
+        const uint64_t adesc0 = umma_desc(sm_base + g.off_a, (uint32_t)g.PL, 128);
+        const uint64_t wdesc0 = umma_desc(sm_base, 2 * NP * 16, 128);
+        int cslot = 0, buf = 0;
+        uint32_t cph = 0, aph = 0;
         for (int i = 0; i < my_tiles; ++i) {
             const int acc = i & 1;
-            mbar_wait(&a_full[buf], aph);
             if (i >= 2) mbar_wait(&acc_empty[acc], (uint32_t)(((i >> 1) - 1) & 1));
-            tc_fence_after();
             const uint32_t d = tmem + (uint32_t)acc * (2 * NP);
-            const uint32_t ab = sm_base + g.off_a + (uint32_t)buf * abytes;
-            for (int tap = 0; tap < 9; ++tap) {
-                const uint32_t at = ab + (uint32_t)(((tap / 3) * g.Wp + (tap % 3)) * 16);
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) {
+                mbar_wait(&a_full[buf], aph);
+                tc_fence_after();
+                const uint64_t abase = adesc0 + (uint64_t)(((uint32_t)buf * abytes) >> 4);
 #pragma unroll
-                for (int h = 0; h < KS; ++h) {
-                    // resident weights are waited for once, before the first tile
-                    if (!resident || i == 0) {
-                        mbar_wait(&wfull[cslot], cph);
+                for (int tap = 0; tap < 9; ++tap) {
+                    const uint64_t at = abase + (uint64_t)((tap / 3) * WP + (tap % 3));
+                    const int slot = resident ? c * 9 + tap : cslot;
+                    if (!resident || i == 0) {   // resident weights: waited for once, at the first tile
+                        mbar_wait(&wfull[slot], resident ? 0u : cph);
                         tc_fence_after();
                     }
-                    const uint32_t wb = sm_base + (uint32_t)cslot * CBYTES;
+                    const uint64_t wb = wdesc0 + (uint64_t)(((uint32_t)slot * WCB) >> 4);
                     if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < KSTEPS / KS; ++kk) {
-                            const int k = h * (KSTEPS / KS) + kk;
-                            const uint64_t ahi = umma_desc(at + 2u * k * PL, PL, 128);
-                            const uint64_t alo = umma_desc(at + (uint32_t)(G + 2 * k) * PL, PL, 128);
-                            const uint64_t b = umma_desc(wb + 2u * kk * (2 * NP) * 16, 2 * NP * 16, 128);
-                            mma_tf32(d, ahi, b, IDESC, (tap | k) ? 1u : 0u);
+                        for (int k = 0; k < KSC; ++k) {
+                            const uint64_t ahi = at + (uint64_t)(2u * k * PL16);
+                            const uint64_t alo = ahi + (uint64_t)(GC * PL16);
+                            const uint64_t b = wb + (uint64_t)(2 * k * 2 * NP);
+                            mma_tf32(d, ahi, b, IDESC, (c | tap | k) ? 1u : 0u);
                             mma_tf32(d, alo, b, IDESC, 1u);
                         }
                         if (!resident) umma_commit(&wempty[cslot]);
                     }
                     __syncwarp();
-                    if (++cslot == g.ws) { cslot = 0; cph ^= 1u; }
-                    ++used;
-                    // streamed weights: refill the slot of the previous chunk (its MMAs finish as
-                    // these start), keeping ws - 1 chunks in flight
-                    if (!resident && w_loaded < my_chunks && w_loaded < used + g.ws - 1) load_w(w_loaded++);
+                    if (!resident && ++cslot == g.ws) { cslot = 0; cph ^= 1u; }
                 }
+                if (elect_one()) umma_commit(&a_empty[buf]);
+                __syncwarp();
+                if (++buf == g.na) { buf = 0; aph ^= 1u; }
             }
-            if (elect_one()) {
-                umma_commit(&a_empty[buf]);
-                umma_commit(&acc_full[acc]);
-            }
+            if (elect_one()) umma_commit(&acc_full[acc]);
             __syncwarp();
-            if (++buf == g.na) { buf = 0; aph ^= 1u; }
         }
     } else {
-        // ------------------------------------------------------------ epilogue (warps 0-3)
+        // ------------------------------------------------------------ epilogue (warps 0-7)
+        // warp w reads TMEM lanes 32 (w % 4) .. + 31 (its pixels) and the column half w / 4
+        const int quad = warp & 3, half = warp >> 2;
         int img = (int)blockIdx.x / g.n_tiles, t = (int)blockIdx.x - img * g.n_tiles;
         const int dimg = (int)gridDim.x / g.n_tiles, dt = (int)gridDim.x - dimg * g.n_tiles;
         for (int i = 0; i < my_tiles; ++i, img += dimg, t += dt) {
@@ -273,14 +288,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int acc = i & 1;
             mbar_wait(&acc_full[acc], (uint32_t)((i >> 1) & 1));
             tc_fence_after();
-            const int pos = g.q_begin + t * TC_M + warp * 32 + lane;
-            const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)acc * (2 * NP);
+            const int pos = g.q_begin + t * TC_M + quad * 32 + lane;
+            const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)acc * (2 * NP);
             const int prow = pos / g.Wp, pcol = pos - prow * g.Wp;
             const bool interior = pos < g.q_end && pcol >= 1 && pcol <= g.S;
             if constexpr (OUT_MODE == 0) {
                 float* o = act_out + ((size_t)img * g.P + pos) * NP;
+                constexpr int HC = NP / 2;            // columns per warp (>= 8)
 #pragma unroll
-                for (int c0 = 0; c0 < NP; c0 += 8) {
+                for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 8) {
                     float v[8], w[8];
                     tmem_ld8(tbase + c0, v);          // A W_hi
                     tmem_ld8(tbase + NP + c0, w);     // A W_lo
@@ -297,21 +313,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int side = 0; side < 2; ++side) {
                     if (t != (side ? g.n_tiles - 1 : 0)) continue;
                     float4* z = reinterpret_cast<float4*>(act_out + ((size_t)img * g.P + (side ? g.q_end : 0)) * NP);
-                    for (int e = tid; e < g.Wp * NP / 4; e += 32 * TC_EPI_WARPS) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int e = tid; e < g.Wp * NP / 4; e += TC_EPI_THREADS) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             } else {
                 float v[8], w[8];
-                tmem_ld8(tbase, v);
-                tmem_ld8(tbase + NP, w);
-                v[0] += w[0];
-                v[1] += w[1];
+                if (half == 0) {
+                    tmem_ld8(tbase, v);
+                    tmem_ld8(tbase + NP, w);
+                }
                 tc_fence_before();
                 mbar_arrive(&acc_empty[acc]);
                 const int k = (prow - 1) * g.S + (pcol - 1);
-                if (interior && k < g.N_d) {
+                if (half == 0 && interior && k < g.N_d) {
                     const size_t o = (size_t)img * g.N_d + k;
                     const float2 z = __ldg(s_in + o);
-                    s_out[o] = make_float2(z.x + (v[0] + bsm[0]), z.y + (v[1] + bsm[1]));
+                    s_out[o] = make_float2(z.x + ((v[0] + w[0]) + bsm[0]), z.y + ((v[1] + w[1]) + bsm[1]));
                 }
             }
         }
@@ -353,15 +369,15 @@ static TcConv tc_geom(int S, int N_d, int Cin, int Cout, long long n_img) {
     return g;
 }
 
-// smem plan: weight chunks (ws slots) | A ring (na buffers) | bias | barriers.  Order of
-// preference: resident weights with a double-buffered (or deeper) A ring; streamed weights
-// (>= 4 slots) with >= 2 A buffers; resident with one A buffer; streamed with one.
+// smem plan: weight slices (ws slots of CK x 2NP) | A chunk ring (na buffers) | bias |
+// barriers.  Order of preference: resident weights with >= 2 A chunks in flight; a weight
+// ring of >= 4 slices with >= 2 A chunks; then shallower variants.
 static size_t tc_plan(TcConv& g, int CINP, int NP) {
-    const int KS = CINP == 64 ? 2 : 1;
-    const size_t chunk = 2ull * CINP * NP * 4 / KS, abuf = 2ull * (CINP / 4) * g.PL;
+    const int CK = tc_ck(CINP), NW = 9 * (CINP / CK);
+    const size_t slice = (size_t)CK * 2 * NP * 4, abuf = 2ull * (CK / 4) * g.PL;
     const size_t limit = 227 * 1024;
     auto bytes_of = [&](int ws, int na, size_t& off_a, size_t& off_bias, size_t& off_bar) {
-        off_a = ws * chunk;
+        off_a = ws * slice;
         off_bias = off_a + na * abuf;
         off_bar = (off_bias + NP * 4 + 15) & ~(size_t)15;
         return off_bar + 8 * (4 + 2 * na + 2 * ws) + 16;
@@ -382,13 +398,15 @@ static size_t tc_plan(TcConv& g, int CINP, int NP) {
     };
     size_t r;
     for (int na = 4; na >= 2; --na)
-        if ((r = take(9 * KS, na))) return r;
+        if ((r = take(NW, na))) return r;
     for (int na = 4; na >= 2; --na)
-        for (int ws = 8; ws >= 4; --ws)
-            if ((r = take(ws, na))) return r;
-    if ((r = take(9 * KS, 1))) return r;
-    for (int ws = 8; ws >= 2; --ws)
-        if ((r = take(ws, 1))) return r;
+        for (int ws = 16; ws >= 4; --ws)
+            if (ws < NW && (r = take(ws, na))) return r;
+    for (int na = 2; na >= 1; --na) {
+        if ((r = take(NW, na))) return r;
+        for (int ws = 8; ws >= 2; --ws)
+            if (ws < NW && (r = take(ws, na))) return r;
+    }
     return 0;
 }
 
