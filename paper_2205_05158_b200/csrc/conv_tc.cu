@@ -14,8 +14,10 @@
 //
 // FP32 accuracy with TF32 tensor cores (the 2e-5 parity bar): both operands are split
 // x = hi + lo with hi = rna_tf32(x), lo = rna_tf32(x - hi).  The weight halves sit side by
-// side in N (B = [W_hi | W_lo], N = 2 Cout) and each K step issues two MMAs, A_hi B and
-// A_lo B, into one accumulator: all four products, summed in the epilogue.  (An SS-mode
+// side in N (B = [W_hi | W_lo], N = 2 Cout) and each K step issues two MMAs into one
+// accumulator, A_hi [W_hi | W_lo] (N = 2 Cout) and A_lo W_hi (N = Cout, the first half of
+// the same B tile): three of the four products (A_lo W_lo ~ 2^-22 relative is dropped),
+// summed in the epilogue.  (An SS-mode
 // MMA at N <= 64 costs the same ~46 cycles as at N = 16 — it is bound by reading the
 // 4 KB A tile from shared memory — so doubling N is free where 3xTF32's third MMA is not.)  Weights are split once per call into a global image laid out exactly as
 // the shared-memory B operand, copied in with cp.async.bulk (TMA); activations are split
@@ -97,6 +99,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int NW = 9 * NCH;           // weight slices per tile, order (chunk, tap)
     constexpr uint32_t WCB = (uint32_t)CK * 2 * NP * 4;   // bytes per weight slice
     constexpr uint32_t IDESC = idesc_tf32_m128(2 * NP);
+    // the A_lo MMA reads only the first NP rows of B (W_hi): A_lo W_lo (~2^-22 relative) is
+    // dropped and the MMA reads 25 % fewer shared-memory bytes
+    constexpr uint32_t IDESC_LO = idesc_tf32_m128(NP);
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + g.off_bar);
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             const uint64_t alo = ahi + (uint64_t)(GC * PL16);
                             const uint64_t b = wb + (uint64_t)(2 * k * 2 * NP);
                             mma_tf32(d, ahi, b, IDESC, (c | tap | k) ? 1u : 0u);
-                            mma_tf32(d, alo, b, IDESC, 1u);
+                            mma_tf32(d, alo, b, IDESC_LO, 1u);   // A_lo x W_hi only (N = NP)
                         }
                         if (!resident) umma_commit(&wempty[cslot]);
                     }
@@ -337,6 +342,95 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         tmem_dealloc(tmem, g.tmem_cols);
     }
+}
+
+// Last layer (C_out = 2) on the FP32 pipe.  On the tensor cores this layer paid the full A
+// operand read (9 taps x C_in x hi/lo per pixel) for an N = 16 tile of which 2 columns are
+// real (1.9 ms of the C5 CNN's 10.9 ms); as a direct convolution it is 2 x 9 x C_in FMAs per
+// pixel.  A group of G = C_in / 4 consecutive lanes owns a 4 x 4 block of output pixels, lane
+// gq its 4 input channels 4gq..4gq+3: the group's loads of one haloed pixel are G consecutive
+// float4 (coalesced; a 6 x 6 haloed window per 16 outputs), each lane accumulates its
+// channels' share of the 16 pixels x 2 outputs,
+// and the group reduces with shuffles.  Weights sit in shared memory as [j][tap][gq] float2
+// (both outputs), conflict-free across the group.  Writes s_out = s_in + out + b on the first
+// N_d pixels (A2-A5).
+template <int CINP>
+__global__ void __launch_bounds__(256) k_conv_out_cl(const float* __restrict__ act, const float* __restrict__ W,
+                                                     const float* __restrict__ bias, const float2* __restrict__ s_in,
+                                                     float2* __restrict__ s_out, int S, int Cin, int N_d,
+                                                     long long n_img) {
+    constexpr int G = CINP / 4;           // lanes per pixel block
+    __shared__ float2 wsm[4 * 9 * G];     // [j][tap][gq] -> (W[0][4gq+j][tap], W[1][4gq+j][tap])
+    for (int e = threadIdx.x; e < 4 * 9 * G; e += blockDim.x) {
+        const int gq = e % G, r = e / G, tap = r % 9, j = r / 9, ci = 4 * gq + j;
+        wsm[e] = ci < Cin ? make_float2(W[((size_t)0 * Cin + ci) * 9 + tap], W[((size_t)1 * Cin + ci) * 9 + tap])
+                          : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, gq = lane % G;
+    constexpr int BS = 4;                 // output block side
+    const int Wp = S + 2, nbx = (S + BS - 1) / BS, nblk = nbx * nbx;
+    const long long gi = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / G;   // pixel block
+    const bool active = gi < n_img * nblk;
+    const long long img = active ? gi / nblk : 0;
+    const int blk = active ? (int)(gi - img * nblk) : 0, by = blk / nbx, bx = blk - by * nbx;
+    const int y0 = BS * by, x0 = BS * bx;   // output pixel (y0, x0); haloed rows / cols y0 .. y0 + BS + 1
+    const float4* a4 = reinterpret_cast<const float4*>(act + (size_t)img * Wp * Wp * CINP) + gq;
+    float acc[BS][BS][2] = {};
+#pragma unroll
+    for (int r = 0; r < BS + 2; ++r) {
+        float4 nb[BS + 2];
+#pragma unroll
+        for (int c = 0; c < BS + 2; ++c) {
+            const int yy = y0 + r, xx = x0 + c;
+            nb[c] = (active && yy < Wp && xx < Wp) ? __ldg(a4 + ((size_t)yy * Wp + xx) * G)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int py = 0; py < BS; ++py) {
+            const int dy = r - py;
+            if (dy < 0 || dy > 2) continue;
+#pragma unroll
+            for (int px = 0; px < BS; ++px)
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    const float4 q = nb[px + dx];
+                    const int tap = dy * 3 + dx;
+                    const float2 w0 = wsm[(0 * 9 + tap) * G + gq], w1 = wsm[(1 * 9 + tap) * G + gq];
+                    const float2 w2 = wsm[(2 * 9 + tap) * G + gq], w3 = wsm[(3 * 9 + tap) * G + gq];
+                    float a0 = acc[py][px][0], a1 = acc[py][px][1];
+                    a0 = fmaf(w0.x, q.x, a0); a1 = fmaf(w0.y, q.x, a1);
+                    a0 = fmaf(w1.x, q.y, a0); a1 = fmaf(w1.y, q.y, a1);
+                    a0 = fmaf(w2.x, q.z, a0); a1 = fmaf(w2.y, q.z, a1);
+                    a0 = fmaf(w3.x, q.w, a0); a1 = fmaf(w3.y, q.w, a1);
+                    acc[py][px][0] = a0;
+                    acc[py][px][1] = a1;
+                }
+        }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int py = 0; py < BS; ++py)
+#pragma unroll
+            for (int px = 0; px < BS; ++px) {
+                acc[py][px][0] += __shfl_xor_sync(0xffffffffu, acc[py][px][0], o);
+                acc[py][px][1] += __shfl_xor_sync(0xffffffffu, acc[py][px][1], o);
+            }
+    if (!active || gq != 0) return;
+    const float b0 = bias[0], b1 = bias[1];
+#pragma unroll
+    for (int py = 0; py < BS; ++py)
+#pragma unroll
+        for (int px = 0; px < BS; ++px) {
+            const int y = y0 + py, x = x0 + px;
+            const int k = y * S + x;
+            if (y < S && x < S && k < N_d) {
+                const size_t o = (size_t)img * N_d + k;
+                const float2 z = __ldg(s_in + o);
+                s_out[o] = make_float2(z.x + (acc[py][px][0] + b0), z.y + (acc[py][px][1] + b1));
+            }
+        }
 }
 
 // ============================================================================ host side
@@ -483,11 +577,15 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
         float* out = last ? nullptr : act[l & 1];
         if (first) rc = launch_tc_n<1, 0, 8>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream);
         else if (last) {
+            // C_out = 2: direct FP32 convolution on the channels-last activations
+            const long long nth = n_img * (long long)(((S + 3) / 4) * ((S + 3) / 4)) * (CINP / 4);
+            const unsigned blocks = (unsigned)((nth + 255) / 256);
             switch (CINP) {
-                case 16: rc = launch_tc_n<0, 1, 16>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
-                case 32: rc = launch_tc_n<0, 1, 32>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
-                default: rc = launch_tc_n<0, 1, 64>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+                case 16: k_conv_out_cl<16><<<blocks, 256, 0, stream>>>(in, W, b, s_in, s_out, S, ci, N_d, n_img); break;
+                case 32: k_conv_out_cl<32><<<blocks, 256, 0, stream>>>(in, W, b, s_in, s_out, S, ci, N_d, n_img); break;
+                default: k_conv_out_cl<64><<<blocks, 256, 0, stream>>>(in, W, b, s_in, s_out, S, ci, N_d, n_img); break;
             }
+            rc = check_launch("fdcnn_forward (last layer)");
         } else {
             switch (CINP) {
                 case 16: rc = launch_tc_n<0, 0, 16>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
