@@ -206,6 +206,90 @@ __global__ void __launch_bounds__(128) k_rx_combine_blk(const float2* __restrict
     if (SER) add_counts(counts, err, near, cnt);
 }
 
+// Many users (U = 9..32): per subcarrier the channel sum is a small complex GEMM
+// yhat_j[n][u] = sum_b X_j[n][b] h_j[u][b] with a long contraction (b < B = 256..512) — the
+// register-blocked kernel above re-reads h_fd from L2 for every symbol pair (6.9 GB per 32
+// symbols at C5).  Here a CTA owns 32 subcarriers (lane = j) x NT = 8 symbols x all users
+// (warp w: users w UPT .. w UPT + UPT - 1): X_j for its 8 symbols is staged in shared memory
+// in chunks of BC antennas and read by all 8 warps, and each thread's h_fd loads (coalesced
+// over j) feed 8 symbols from registers.  Same summation order over b as k_rx_combine.
+template <bool SER, bool AWGN, int UPT>
+__global__ void __launch_bounds__(256) k_rx_combine_tile(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
+                                                         float2* __restrict__ yhat, int B, int U, int N_d,
+                                                         long long n_sym, int accumulate,
+                                                         const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
+                                                         long long* counts, SliceParams sp, Impair imp) {
+    constexpr int NT = 8, BC = 16;
+    __shared__ __align__(16) float2 xs[NT][BC][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = blockIdx.y * 32 + lane;
+    const bool jok = j < N_d;
+    const long long n0 = (long long)blockIdx.x * NT;
+    const int nt = (int)min((long long)NT, n_sym - n0);
+    const int u0 = warp * UPT;
+    float2 acc[NT][UPT];
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int c = 0; c < UPT; ++c) acc[n][c] = make_float2(0.f, 0.f);
+    const float2* H = hfd + (jok ? j : 0);
+    for (int b0 = 0; b0 < B; b0 += BC) {
+        const int bn = min(BC, B - b0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < NT * BC * 32; e += blockDim.x) {
+            const int l = e & 31, r = e >> 5, bb = r % BC, n = r / BC;
+            const int jj = blockIdx.y * 32 + l;
+            xs[n][bb][l] = (n < nt && bb < bn && jj < N_d) ? __ldg(XPA + ((size_t)(n0 + n) * B + b0 + bb) * N_d + jj)
+                                                          : make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int bb = 0; bb < bn; ++bb) {
+            const int b = b0 + bb;
+            float2 hv[UPT];
+#pragma unroll
+            for (int c = 0; c < UPT; ++c)
+                hv[c] = (u0 + c < U) ? __ldg(H + ((size_t)(u0 + c) * B + b) * N_d) : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const float2 xv = xs[n][bb][lane];
+#pragma unroll
+                for (int c = 0; c < UPT; ++c) acc[n][c] = cfma(hv[c], xv, acc[n][c]);
+            }
+        }
+    }
+    int err = 0, near = 0, cnt = 0;
+    if (jok) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            if (n >= nt) continue;
+#pragma unroll
+            for (int c = 0; c < UPT; ++c) {
+                const int u = u0 + c;
+                if (u >= U) continue;
+                const size_t o = ((size_t)(n0 + n) * U + u) * N_d + j;
+                float2 a = acc[n][c];
+                if (accumulate) a = cadd(a, yhat[o]);
+                if constexpr (AWGN)
+                    a = cadd(a, cgauss((unsigned long long)((imp.sym0 + n0 + n) * U + u) * N_d + j, STREAM_AWGN,
+                                       imp.key_lo, imp.key_hi, imp.awgn_std));
+                yhat[o] = a;
+                if constexpr (SER) {
+                    bool nr = false;
+                    const int di = slice_axis(a.x * sp.inv_ac, sp, nr);
+                    const int dq = slice_axis(a.y * sp.inv_ac, sp, nr);
+                    const int dd = di + sp.m * dq;
+                    if (dec) dec[o] = (uint16_t)dd;
+                    err += (dd != (int)idx[o]);
+                    near += nr;
+                    ++cnt;
+                }
+            }
+        }
+    }
+    if (SER) add_counts(counts, err, near, cnt);
+}
+
 template <bool SER, bool AWGN>
 static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d, long long n_sym,
                            int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
@@ -215,8 +299,17 @@ static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, i
             dim3 g((N_d + 127) / 128, (unsigned)((n_sym + ns - 1) / ns));
             kern<<<g, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, imp);
         };
+        auto go_tile = [&](auto kern) {
+            // n-tiles fastest: the CTAs sharing a subcarrier tile's h_fd slice (U x B x 32) run
+            // together, so h_fd comes from HBM once per step (432 MB at C5) and from L2 after
+            dim3 g((unsigned)((n_sym + 7) / 8), (N_d + 31) / 32);
+            kern<<<g, 256, 0, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, imp);
+        };
         if (U <= 2) go(k_rx_combine_blk<SER, AWGN, 2, 4>, 4);
         else if (U <= 4) go(k_rx_combine_blk<SER, AWGN, 4, 4>, 4);
+        else if (U <= 8) go(k_rx_combine_blk<SER, AWGN, 8, 2>, 2);
+        else if (U <= 16) go_tile(k_rx_combine_tile<SER, AWGN, 2>);
+        else if (U <= 32) go_tile(k_rx_combine_tile<SER, AWGN, 4>);
         else go(k_rx_combine_blk<SER, AWGN, 8, 2>, 2);
         return;
     }

@@ -209,6 +209,34 @@ def test_precode_tiles_ragged(F, n, B, U, Nd):
     assert rel(got, O.precode(P.transpose(2, 0, 1), s)) < TOL
 
 
+@pytest.mark.parametrize("n,B,U,Nd", [(11, 512, 32, 3300), (9, 37, 12, 70), (17, 256, 16, 600), (3, 64, 4, 600),
+                                      (5, 40, 7, 36), (2, 24, 24, 100)])
+def test_combine_ser_ragged(F, n, B, U, Nd):
+    """Channel sum + slicing (register-blocked kernel for U <= 8, staged tile kernel for
+    U = 9..32) on ragged symbol / subcarrier / antenna counts against the oracle einsum and
+    slicer; decisions identical except within 1e-4 of a boundary."""
+    rng = np.random.default_rng(n * 131 + U)
+    M_qam = 64
+    XPA = crandn(rng, n, B, Nd, scale=0.3)
+    h = crandn(rng, U, B, Nd, scale=0.3)
+    alpha = 0.7
+    idx = rng.integers(0, M_qam, size=(n, U, Nd)).astype(np.uint16)
+    want = np.einsum("ubj,nbj->nuj", h.astype(np.complex128), XPA.astype(np.complex128))
+    d_idx = torch.from_numpy(idx.astype(np.int32)).to("cuda").to(torch.uint16)
+    dec = torch.zeros((n, U, Nd), dtype=torch.uint16, device="cuda")
+    yhat, counts, _ = F.ue_combine_ser(dev(XPA), dev(h), alpha, d_idx, M_qam, dec=dec)
+    assert rel(host(yhat), want) < TOL
+    assert rel(host(F.ue_combine(dev(XPA), dev(h))), want) < TOL
+    dec_o, c_o = O.slice_ser(want, alpha, idx, M_qam)
+    near = np.zeros(want.shape, bool)
+    _, cn = O.slice_ser(want, alpha, idx, M_qam)
+    mism = host(dec).astype(np.int64) != dec_o.astype(np.int64)
+    c = host(counts)
+    assert c[1] == n * U * Nd
+    assert mism.sum() <= cn[2] + c[2]
+    assert abs(int(c[0]) - int(c_o[0])) <= cn[2] + c[2]
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_chain_tx_vs_oracle_and_unfused(F, name):
     cfg = configs.get(name)
