@@ -118,14 +118,15 @@ __host__ __device__ constexpr int pass_ns(int p) {
     return ns;
 }
 
-// Threads per CTA for an N-point transform: VPT = 16 values/thread up to N = 4096,
-// then 512 threads.
+// Threads per CTA for an N-point transform: VPT = 16 values/thread up to N = 4096; N = 8192
+// with 256 threads (VPT = 32: two CTAs of ~102 KB per SM instead of one 512-thread CTA);
+// N = 16384 with 512 threads.
 template <int LOG2N>
-__host__ __device__ constexpr int fft_threads() { return LOG2N <= 12 ? (1 << LOG2N) / 16 : 512; }
-// resident CTAs per SM requested from ptxas (register cap 65536 / (T * this) = 128).
+__host__ __device__ constexpr int fft_threads() { return LOG2N <= 12 ? (1 << LOG2N) / 16 : (LOG2N == 13 ? 256 : 512); }
+// resident CTAs per SM requested from ptxas (register cap 65536 / (T * this)).
 // (Measured: N/32 threads with 4 CTAs/SM at N = 4096 was 11% slower — register spills.)
 template <int LOG2N>
-__host__ __device__ constexpr int fft_min_blocks() { return fft_threads<LOG2N>() <= 256 ? 3 : 1; }
+__host__ __device__ constexpr int fft_min_blocks() { return LOG2N <= 12 ? 3 : (LOG2N == 13 ? 2 : 1); }
 
 // Register layout of a pass with radix R: element (q, r), q < VPT/R, r < R, is
 // position j + r * (N/R) with j = tid + q * T.
