@@ -188,6 +188,11 @@ int chain_txrx_ex(const void* P, const void* s_tilde, const void* coef, void* y,
 /* chain_txrx on an already precoded spectrum X [n_sym][B_loc][N_d] (the output of precode):
  * the split precode -> chain_txrx_pre moves the U-fold L2 gather of P_b and s_n out of the
  * fused kernel's prologue into one bandwidth-bound kernel.  imp nullable. */
+/* chain_txrx / chain_txrx_ex / _ps / _pre at N_ifft = 16384 (N_d % 4 == 0, GMP shapes of
+ * the configured workloads) split each (symbol, antenna) over a two-CTA cluster (one radix-2
+ * step across the pair, DSMEM exchange).  mode 0 = auto (default), 1 = never (single-CTA kernel).
+ * Process-wide; returns FD_ERR_ARG for other modes. */
+int fd_set_chain_split(int mode);
 /* Native-runtime / binding policy: from this many users a step runs precode -> chain_txrx_pre. */
 #define FD_SPLIT_PRECODE_MIN_U 16
 int chain_txrx_pre(const void* X, const void* coef, void* y, void* XPA, const int* orders, int n_orders,

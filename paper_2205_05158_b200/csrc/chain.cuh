@@ -237,6 +237,10 @@ inline int prune_slots(int N, int N_d) {
     const int nz = (h + w - 1) / w;
     return nz <= 2 ? nz : 0;
 }
+// Cluster-split chain_txrx for N = 8192 / 16384 (chain_cl.cu); returns -1 when it does not apply.
+int launch_chain_cluster(int log2n, int variant, const float2* P, const float2* s, const float2* coef, float2* y,
+                         float2* XPA, long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp,
+                         cudaStream_t st);
 // Pruned-FFT chain_txrx instantiations (tx_pruned.cu); returns -1 when none matches.
 int launch_chain_pruned(int log2n, int variant, int pz, const float2* P, const float2* s, const float2* coef,
                         float2* y, float2* XPA, long long n_sym, int B, int U, int N_d, const GmpDesc& d,

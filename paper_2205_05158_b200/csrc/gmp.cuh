@@ -279,9 +279,14 @@ struct RunLayout {
     __device__ static __forceinline__ int e_phys(int m) { return (e_chunk(m >> 2) << 2) | (m & 3); }
 };
 
-template <int KP, int L, int M, int R>
+// HALO (cluster-split symbols, chain_cl.cu): this CTA holds one half of the symbol's samples
+// (N local); window chunks left of 0 or right of N come from the partner CTA's buffers
+// (usw_r / esw_r, distributed shared memory), which hold the other half — for two halves the
+// partner is both the left and the right (circular) neighbour.
+template <int KP, int L, int M, int R, bool HALO = false>
 __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const float* __restrict__ esw,
-                                        const float2* __restrict__ cf, int N, int rho, float2 (&out)[R]) {
+                                        const float2* __restrict__ cf, int N, int rho, float2 (&out)[R],
+                                        const float2* usw_r = nullptr, const float* esw_r = nullptr) {
     static_assert(R % 4 == 0, "run length must be a multiple of 4");
     using Row = CoefRow<KP, M>;
     using Lay = RunLayout<R>;
@@ -299,7 +304,14 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
         const int xm = N / 4 - 1;
 #pragma unroll
         for (int c = 0; c < E_N / 4; ++c) {
-            const float4 t = e4[Lay::e_chunk(((m0 - E_LO) / 4 + c) & xm)];
+            float4 t;
+            if constexpr (HALO) {
+                const int q = (m0 - E_LO) / 4 + c;
+                const float4* src = (q < 0 || q > xm) ? reinterpret_cast<const float4*>(esw_r) : e4;
+                t = src[Lay::e_chunk(q & xm)];
+            } else {
+                t = e4[Lay::e_chunk(((m0 - E_LO) / 4 + c) & xm)];
+            }
             ew[0][4 * c + 0] = t.x;
             ew[0][4 * c + 1] = t.y;
             ew[0][4 * c + 2] = t.z;
@@ -316,7 +328,14 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
         const int xm = N / 2 - 1;
 #pragma unroll
         for (int c = 0; c < U_N / 2; ++c) {
-            const float4 t = u4[Lay::u_chunk(((m0 - U_LO) / 2 + c) & xm)];
+            float4 t;
+            if constexpr (HALO) {
+                const int q = (m0 - U_LO) / 2 + c;
+                const float4* src = (q < 0 || q > xm) ? reinterpret_cast<const float4*>(usw_r) : u4;
+                t = src[Lay::u_chunk(q & xm)];
+            } else {
+                t = u4[Lay::u_chunk(((m0 - U_LO) / 2 + c) & xm)];
+            }
             uw[2 * c] = make_float2(t.x, t.y);
             uw[2 * c + 1] = make_float2(t.z, t.w);
         }
@@ -359,17 +378,18 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
 // (pidx layout) into the swizzled u/e layouts, then all runs; y (global) gets R
 // contiguous complex per run via 128-bit stores.  usw aliases the FFT buffer.
 // ysm (optional): also store the outputs in shared memory in the FFT's pidx layout.
-template <int KP, int L, int M, int R, bool YS = false>
+template <int KP, int L, int M, int R, bool YS = false, bool HALO = false>
 __device__ __forceinline__ void gmp_runs_symbol(float2* __restrict__ buf, float* __restrict__ esw,
                                                 const float2* __restrict__ cf, int N, float2* __restrict__ y,
                                                 int tid, int T, float2* __restrict__ ysm = nullptr,
-                                                const Impair* im = nullptr, unsigned long long nbase = 0) {
+                                                const Impair* im = nullptr, unsigned long long nbase = 0,
+                                                const float2* buf_r = nullptr, const float* esw_r = nullptr) {
 #pragma unroll 1
     for (int rho = tid; rho < N / R; rho += T) {
         // keep the coefficient-row loads inside the loop (no hoisting into registers)
         asm volatile("" ::: "memory");
         float2 out[R];
-        gmp_run<KP, L, M, R>(buf, esw, cf, N, rho, out);
+        gmp_run<KP, L, M, R, HALO>(buf, esw, cf, N, rho, out, buf_r, esw_r);
         if (im) {
 #pragma unroll
             for (int i = 0; i < R; ++i) out[i] = pa_impair(out[i], nbase + (unsigned long long)(R * rho + i), *im);

@@ -215,6 +215,8 @@ static int launch_chain(int variant, const float2* P, const float2* s, const flo
                         long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp,
                         cudaStream_t st) {
     if (RX) {
+        const int rcl = launch_chain_cluster(LOG2N, variant, P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+        if (rcl >= 0) return rcl;
         const int pz = prune_slots(1 << LOG2N, N_d);
         if (pz > 0) {
             const int rc = launch_chain_pruned(LOG2N, variant, pz, P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);

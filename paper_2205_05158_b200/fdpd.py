@@ -152,6 +152,12 @@ def set_cnn_path(path: int):
     _check(lib().fd_set_cnn_path(int(path)))
 
 
+def set_chain_split(mode: int):
+    """Cluster split of the N = 8192 / 16384 chain kernels (include/fdpd.h fd_set_chain_split):
+    0 = auto (default), 1 = never.  Process-wide."""
+    _check(lib().fd_set_chain_split(int(mode)))
+
+
 def fdcnn_forward(params, chans, s_in, out=None, workspace=None):
     """s_tilde = s + CNN(s)  (include/fdpd.h fdcnn_forward).  s_in complex64 [n_sym][U][N_d]."""
     _dev(params, torch.float32, "params")

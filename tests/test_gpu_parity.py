@@ -253,6 +253,36 @@ def test_chain_tx_vs_oracle_and_unfused(F, name):
     assert rel(host(y), want) < TOL
 
 
+@pytest.mark.parametrize("name,impair", [("C4", False), ("C5", False), ("C4", True)])
+def test_chain_cluster_split_vs_single(F, name, impair):
+    """The two-CTA cluster split (N = 16384) against the single-CTA kernel on the same
+    inputs: one extra radix-2 step, so rounding-level differences only; per-stage oracle
+    parity is covered by the other chain tests (which run the split by default)."""
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg, range(2))
+    h_fd, P, alpha = F.zf_precoder_build(dev(inp["h_taps"]), cfg.N_ifft, cfg.N_d, cfg.rho)
+    s, coef = dev(inp["s"]), dev(inp["coef"])
+    imp = F.make_impairments(0.8, 1e-3, 0.0, 0.0, 77, 0, 0, cfg.B) if impair else None
+
+    def run():
+        if imp is None:
+            return F.chain_txrx(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+        return F.chain_txrx_ex(P, s, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft, imp)
+
+    y_cl, X_cl = run()
+    F.set_chain_split(1)
+    try:
+        y_1, X_1 = run()
+    finally:
+        F.set_chain_split(0)
+    assert rel(host(y_cl), host(y_1)) < 1e-6
+    assert rel(host(X_cl), host(X_1)) < 1e-6
+    if not impair:
+        Po = host(P).transpose(2, 0, 1)
+        want = O.gmp_pa(O.ofdm_modulate(O.precode(Po, inp["s"]), cfg.N_ifft), inp["coef"], cfg.orders, cfg.L, cfg.M)
+        assert rel(host(y_cl), want) < TOL
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_chain_txrx_vs_unfused(F, name):
     """chain_txrx = chain_tx + the receive FFT of ue_receive, in one kernel; XPA feeds ue_combine."""
