@@ -236,15 +236,42 @@ __global__ void __launch_bounds__(256) k_rx_combine_tile(const float2* __restric
     for (int b0 = 0; b0 < B; b0 += BC) {
         const int bn = min(BC, B - b0);
         __syncthreads();
-        for (int e = threadIdx.x; e < NT * BC * 32; e += blockDim.x) {
-            const int l = e & 31, r = e >> 5, bb = r % BC, n = r / BC;
-            const int jj = blockIdx.y * 32 + l;
-            xs[n][bb][l] = (n < nt && bb < bn && jj < N_d) ? __ldg(XPA + ((size_t)(n0 + n) * B + b0 + bb) * N_d + jj)
-                                                          : make_float2(0.f, 0.f);
+        {
+            // all of this thread's staging loads in flight before the shared-memory stores
+            constexpr int PER = NT * BC * 32 / 256;
+            float2 t[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int e = threadIdx.x + 256 * k;
+                const int l = e & 31, r = e >> 5, bb = r % BC, n = r / BC;
+                const int jj = blockIdx.y * 32 + l;
+                t[k] = (n < nt && bb < bn && jj < N_d) ? __ldg(XPA + ((size_t)(n0 + n) * B + b0 + bb) * N_d + jj)
+                                                      : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) (&xs[0][0][0])[threadIdx.x + 256 * k] = t[k];
         }
         __syncthreads();
-#pragma unroll 2
-        for (int bb = 0; bb < bn; ++bb) {
+        // h_fd for 4 antennas (4 UPT loads) in flight per step
+        int bb = 0;
+        for (; bb + 4 <= bn; bb += 4) {
+            float2 hv[4][UPT];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < UPT; ++c)
+                    hv[q][c] = (u0 + c < U) ? __ldg(H + ((size_t)(u0 + c) * B + b0 + bb + q) * N_d)
+                                            : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const float2 xv = xs[n][bb + q][lane];
+#pragma unroll
+                    for (int c = 0; c < UPT; ++c) acc[n][c] = cfma(hv[q][c], xv, acc[n][c]);
+                }
+        }
+        for (; bb < bn; ++bb) {
             const int b = b0 + bb;
             float2 hv[UPT];
 #pragma unroll

@@ -38,13 +38,13 @@ __global__ void __launch_bounds__(32 * PC_WARPS) k_precode_tile(const float2* __
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* ssm = reinterpret_cast<float2*>(smem_raw);   // [NT][U][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = blockIdx.x * 32 + lane;
+    const int j = blockIdx.y * 32 + lane;
     const bool jok = j < N_d;
-    const long long n0 = (long long)blockIdx.y * NT;
+    const long long n0 = (long long)blockIdx.x * NT;
     const int nt = (int)min((long long)NT, n_sym - n0);
     for (int e = threadIdx.x; e < NT * U * 32; e += blockDim.x) {
         const int l = e & 31, r = e >> 5, u = r % U, n = r / U;
-        const int jj = blockIdx.x * 32 + l;
+        const int jj = blockIdx.y * 32 + l;
         ssm[e] = (n < nt && jj < N_d) ? __ldg(s + ((size_t)(n0 + n) * U + u) * N_d + jj) : make_float2(0.f, 0.f);
     }
     __syncthreads();
@@ -260,7 +260,7 @@ int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, i
     if (total == 0) return FD_OK;
     FD_REQUIRE(P && s && X, "precode: NULL pointer");
     FD_REQUIRE(aligned8(P) && aligned8(s) && aligned8(X), "precode: pointers must be 8-byte aligned");
-    FD_REQUIRE(n_sym <= 65535LL * PC_NT, "precode: n_sym=%lld too large per call", n_sym);
+    FD_REQUIRE(N_d <= 65535 * 32, "precode: N_d=%d too large", N_d);
     const size_t smem = sizeof(float2) * PC_NT * U * 32;
     FD_REQUIRE(smem <= 200 * 1024, "precode: U=%d too large for the staged tile", U);
     // antenna split over grid.z so that even a short batch gives >= ~2 waves of CTAs
@@ -269,7 +269,9 @@ int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, i
     while (xy * zc < 2 * 148 * 4 && B_loc / (zc * 2) >= PC_WARPS * PC_BPT) zc *= 2;
     const int bpc = (B_loc + zc - 1) / zc;
     set_smem(k_precode_tile<PC_NT, PC_BPT>, smem);
-    dim3 grid((N_d + 31) / 32, (unsigned)((n_sym + PC_NT - 1) / PC_NT), zc);
+    // symbol tiles fastest: the CTAs that share a (subcarrier tile, antenna range) slice of P run
+    // together, so P streams from HBM once per call (432 MB at C5) instead of once per symbol tile
+    dim3 grid((unsigned)((n_sym + PC_NT - 1) / PC_NT), (N_d + 31) / 32, zc);
     k_precode_tile<PC_NT, PC_BPT><<<grid, 32 * PC_WARPS, smem, stream>>>((const float2*)P, (const float2*)s,
                                                                         (float2*)X, n_sym, B_loc, U, N_d, bpc);
     return check_launch("precode");

@@ -48,6 +48,7 @@ SIGNATURES = {
     "fd_version": (_i, []),
     "fd_shutdown": (None, []),
     "fd_set_cnn_path": (_i, [_i]),
+    "fd_set_chain_split": (_i, [_i]),
     "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
     "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
     "fdcnn_paper_workspace_bytes": (_sz, [_i, _ll, _i, _i]),
