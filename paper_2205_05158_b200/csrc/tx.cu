@@ -56,8 +56,25 @@ __global__ void __launch_bounds__(32 * PC_WARPS) k_precode_tile(const float2* __
 #pragma unroll
             for (int t = 0; t < BPT; ++t) acc[n][t] = make_float2(0.f, 0.f);
         const float2* Pb = P + (size_t)b0 * U * N_d + (jok ? j : 0);
-#pragma unroll 2
-        for (int u = 0; u < U; ++u) {
+        int u = 0;
+        // 4 users x BPT antennas of P in flight per step (the loop is latency-bound otherwise)
+        for (; u + 4 <= U; u += 4) {
+            float2 pv[4][BPT];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int t = 0; t < BPT; ++t)
+                    pv[q][t] = (b0 + t < b_end) ? __ldg(Pb + ((size_t)t * U + u + q) * N_d) : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const float2 sv = ssm[(n * U + u + q) * 32 + lane];
+#pragma unroll
+                    for (int t = 0; t < BPT; ++t) acc[n][t] = cfma(pv[q][t], sv, acc[n][t]);
+                }
+        }
+        for (; u < U; ++u) {
             float2 pv[BPT];
 #pragma unroll
             for (int t = 0; t < BPT; ++t)
