@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
 #pragma unroll
                 for (int q = 0; q < VPT / 16; ++q) {
                     const int j = tid + q * T;         // < N/16 = Ns: twiddle step j, outputs j + r N/16
-                    pass_twiddle<16, -1>(v, q * 16, j, tw);
+                    pass_twiddle_tab16<-1>(v, q * 16, j, N / 16, tw + tw_pass_off(N, NPS - 1));
                     float2 out[2 * PZ];
                     dft16_sparse_out<-1, PZ>(v, q * 16, out);
 #pragma unroll

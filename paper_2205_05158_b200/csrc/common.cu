@@ -1,5 +1,5 @@
 // common.cu — status handling and the twiddle-table plan cache.
-#include "common.cuh"
+#include "fft.cuh"
 
 #include <mutex>
 #include <map>
@@ -45,6 +45,24 @@ __global__ void k_twiddles(float2* w, int N) {
     }
 }
 
+// per-pass radix-16 tables behind the N-entry table (fft.cuh tw_pass_off)
+__global__ void k_twiddles_pass(float2* w, int N) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    int off = N;
+    for (long long ns = 16; ns * 16 <= N; ns *= 16) {
+        const int len = 15 * (int)ns;
+        if (e < len) {
+            const int r = e / (int)ns + 1, k = e % (int)ns;
+            double s, c;
+            sincospi(-2.0 * (double)(r * k) / (double)(16 * ns), &s, &c);
+            w[off + e] = make_float2((float)c, (float)s);
+            return;
+        }
+        e -= len;
+        off += len;
+    }
+}
+
 namespace {
 struct TwKey { int dev; int N; bool operator<(const TwKey& o) const { return dev != o.dev ? dev < o.dev : N < o.N; } };
 std::mutex g_mu;
@@ -58,8 +76,10 @@ const float2* twiddle_table(int N, cudaStream_t stream) {
     auto it = g_tw.find({dev, N});
     if (it != g_tw.end()) return it->second;
     float2* w = nullptr;
-    if (cudaMalloc(&w, sizeof(float2) * (size_t)N) != cudaSuccess) return nullptr;
+    const int len = tw_table_len(N);
+    if (cudaMalloc(&w, sizeof(float2) * (size_t)len) != cudaSuccess) return nullptr;
     k_twiddles<<<(N + 255) / 256, 256, 0, stream>>>(w, N);
+    if (len > N) k_twiddles_pass<<<(len - N + 255) / 256, 256, 0, stream>>>(w, N);
     // the table is plan data: make it visible to every stream before first use
     if (cudaStreamSynchronize(stream) != cudaSuccess) { cudaFree(w); return nullptr; }
     g_tw[{dev, N}] = w;

@@ -161,14 +161,43 @@ __device__ __forceinline__ void pass_twiddle(float2 (&v)[VPT], int off, int step
     for (int r = 1; r < R; ++r) v[off + r] = cmul(v[off + r], wp[r]);
 }
 
-template <int R, int DIR, int VPT, int T, int N>
+// Radix-16 pass twiddles from the per-pass table that follows the N-entry table
+// (twiddle_table): entry [(r - 1) Ns + k] = exp(-2 pi i r k / (16 Ns)), fp64-derived.  A
+// thread's 15 loads are coalesced across the warp (k = j mod Ns runs over consecutive j) and
+// replace 4 loads + 11 derivation products of pass_twiddle.
+template <int DIR, int VPT>
+__device__ __forceinline__ void pass_twiddle_tab16(float2 (&v)[VPT], int off, int k, int Ns,
+                                                   const float2* __restrict__ tab) {
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+        float2 w = __ldg(tab + (r - 1) * Ns + k);
+        if (DIR > 0) w.y = -w.y;
+        v[off + r] = cmul(v[off + r], w);
+    }
+}
+
+// Offset (in complex entries) of pass P's radix-16 table behind the N-entry table: tables for
+// passes p = 1 .. LOG2N/4 - 1 (Ns = 16^p), 15 Ns entries each.
+__host__ __device__ constexpr int tw_pass_off(int N, int P) {
+    int off = N, ns = 16;
+    for (int p = 1; p < P; ++p, ns *= 16) off += 15 * ns;
+    return off;
+}
+__host__ __device__ constexpr int tw_table_len(int N) {
+    int len = N, ns = 16;
+    while (ns * 16 <= N) { len += 15 * ns; ns *= 16; }   // radix-16 passes with Ns >= 16
+    return len;
+}
+
+template <int R, int DIR, int VPT, int T, int N, int TWOFF = 0>
 __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT], int Ns, const float2* __restrict__ tw,
                                                    int tid) {
 #pragma unroll
     for (int q = 0; q < VPT / R; ++q) {
         const int j = tid + q * T;
         const int k = j & (Ns - 1);
-        if (Ns > 1) pass_twiddle<R, DIR>(v, q * R, k * (N / (Ns * R)), tw);
+        if (R == 16 && TWOFF > 0 && Ns > 1) pass_twiddle_tab16<DIR>(v, q * R, k, Ns, tw + TWOFF);
+        else if (Ns > 1) pass_twiddle<R, DIR>(v, q * R, k * (N / (Ns * R)), tw);
         dftR<R, DIR>(v, q * R);
         const int d = (j - k) * R + k;
 #pragma unroll
@@ -191,7 +220,8 @@ __device__ __forceinline__ void fft_run(float2* sm, float2 (&v)[(1 << LOG2N) / f
         pass_load_smem<R, VPT, T, N>(sm, v, tid);
         __syncthreads();
     }
-    pass_compute_store<R, DIR, VPT, T, N>(sm, v, pass_ns<LOG2N>(P), tw, tid);
+    constexpr int TWOFF = (R == 16 && P > 0) ? tw_pass_off(N, P) : 0;
+    pass_compute_store<R, DIR, VPT, T, N, TWOFF>(sm, v, pass_ns<LOG2N>(P), tw, tid);
     __syncthreads();
     if constexpr (P + 1 < PEND) fft_run<LOG2N, DIR, P + 1, PEND>(sm, v, tw, tid);
 }
