@@ -85,10 +85,14 @@ __device__ __forceinline__ float2 cmul2(float2 a, float2 b) {
 }
 // complex coefficient times real feature, accumulated: acc += a * w
 __device__ __forceinline__ float2 cfma_real(float2 a, float w, float2 acc) { return ffma2(a, make_float2(w, w), acc); }
-// acc += a * b (complex), as two FFMA2: (a.x, a.x)*(b.x, b.y) + (-a.y, a.y)*(b.y, b.x)
+// acc += a * b (complex), as two FFMA2: (a.x, a.x)*(b.x, b.y) + (-b.y, b.x)*(a.y, a.y).
+// Written with the broadcast scalar in the second operand of both, so ptxas uses the
+// FFMA2 scalar-operand form and the swap / negate-half modifiers on b, with no register-pair
+// duplication (the (-a.y, a.y) form cost two MOVs per complex MAC in the GMP loop);
+// products and rounding are identical.
 __device__ __forceinline__ float2 cfma2(float2 a, float2 b, float2 acc) {
-    acc = ffma2(make_float2(a.x, a.x), b, acc);
-    return ffma2(make_float2(-a.y, a.y), make_float2(b.y, b.x), acc);
+    acc = ffma2(b, make_float2(a.x, a.x), acc);
+    return ffma2(make_float2(-b.y, b.x), make_float2(a.y, a.y), acc);
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
