@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
                float2* __restrict__ y, float2* __restrict__ XPA, const float2* __restrict__ tw, int B, int U,
                int N_d, float sc, GmpDesc d, Impair imp) {
     constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T;
+    static_assert(PZ == 0 || n_passes<LOG2N>() >= 2, "pruned first pass needs a later pass");
     constexpr bool YSM = RX && KP > 0 && chain_ysm<LOG2N>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const ChainSmem lay = chain_smem(N, N_d, d, YSM);
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
         // P holds the precoded spectrum X [n_sym][B][N_d] (chain_txrx_pre): one coalesced
         // pass over the symbol-antenna row into xs
         const float2* Xr = P + nb * N_d;
-        for (int j = tid; j < N_d; j += T) xs[j] = __ldg(Xr + j);
+        for (int j = tid; j < N_d; j += T) xs[j] = cscale(__ldg(Xr + j), sc);
     } else {
         const float2* Pb = P + (size_t)n * imp.p_stride + (size_t)b * U * N_d;
         const float2* sn = s + n * U * N_d;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
                 sp += 4 * N_d;
             }
             for (; u < U; ++u, pp += N_d, sp += N_d) acc = cfma(__ldg(pp), __ldg(sp), acc);
-            xs[j] = acc;
+            xs[j] = cscale(acc, sc);   // the IDFT's N^-1/2 on the N_d data bins instead of the N outputs
         }
     }
     __syncthreads();
@@ -120,7 +121,11 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
             for (int r = 0; r < 16; ++r) usm[pidx(16 * j + r)] = X[r];
         }
         __syncthreads();
-        fft_run<LOG2N, +1, 1>(usm, v, tw, tid);
+        if constexpr (KP > 0) {
+            if constexpr (n_passes<LOG2N>() > 2) fft_run<LOG2N, +1, 1, n_passes<LOG2N>() - 1>(usm, v, tw, tid);
+        } else {
+            fft_run<LOG2N, +1, 1>(usm, v, tw, tid);
+        }
     } else {
         // branch-free pass-0 fill: data bins are [0, N_d/2) and [N - N_d/2, N) (reading A7)
         constexpr int R0 = pass_radix<LOG2N>(0);
@@ -134,19 +139,41 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
                 const float2 t = xs[(lo || hi) ? jj : 0];
                 v[q * R0 + r] = (lo || hi) ? t : make_float2(0.f, 0.f);
             }
-        fft_run<LOG2N, +1>(usm, v, tw, tid);
+        if constexpr (KP > 0) {
+            if constexpr (n_passes<LOG2N>() > 1) fft_run<LOG2N, +1, 0, n_passes<LOG2N>() - 1>(usm, v, tw, tid);
+        } else {
+            fft_run<LOG2N, +1>(usm, v, tw, tid);
+        }
     }
     if constexpr (KP > 0) {
-        // run-based GMP: relayout u (scaled) and e = |u|^2 into the swizzled run layouts
+        // last IDFT pass, storing u and e = |u|^2 straight into the swizzled run layouts of the
+        // GMP (no natural-order store + reload + barrier; the N^-1/2 is already in xs)
         using Lay = RunLayout<RS>;
+        constexpr int PL_ = n_passes<LOG2N>() - 1;
+        constexpr int RL = pass_radix<LOG2N>(PL_), NSL = pass_ns<LOG2N>(PL_);
+        constexpr bool FIRST_IS_LAST = PL_ == 0;
+        if constexpr (!FIRST_IS_LAST || PZ > 0) {
+            // pass-0 data came in registers only when the last pass is pass 0 without pruning
+            pass_load_smem<RL, VPT, T, N>(usm, v, tid);
+            __syncthreads();
+        }
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) v[j] = cscale(usm[pidx(tid + T * j)], sc);
-        __syncthreads();
+        for (int q = 0; q < VPT / RL; ++q) {
+            const int j = tid + q * T;
+            const int k = j & (NSL - 1);
+            if constexpr (NSL > 1) {
+                if constexpr (RL == 16) pass_twiddle_tab16<+1>(v, q * RL, k, NSL, tw + tw_pass_off(N, PL_));
+                else pass_twiddle<RL, +1>(v, q * RL, k * (N / (NSL * RL)), tw);
+            }
+            dftR<RL, +1>(v, q * RL);
+            const int dd = (j - k) * RL + k;
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int i = tid + T * j;
-            usm[Lay::u_phys(i)] = v[j];
-            esm[Lay::e_phys(i)] = fmaf(v[j].x, v[j].x, v[j].y * v[j].y);
+            for (int r = 0; r < RL; ++r) {
+                const int i = dd + r * NSL;
+                const float2 x = v[q * RL + r];
+                usm[Lay::u_phys(i)] = x;
+                esm[Lay::e_phys(i)] = fmaf(x.x, x.x, x.y * x.y);
+            }
         }
         __syncthreads();
         float2* yo = y + nb * N;
@@ -190,8 +217,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
         return;
     }
     for (int i = tid; i < N; i += T) {
-        const float2 t = cscale(usm[pidx(i)], sc);
-        usm[pidx(i)] = t;
+        const float2 t = usm[pidx(i)];   // already scaled (xs carries N^-1/2)
         esm[i] = fmaf(t.x, t.x, t.y * t.y);
     }
     __syncthreads();
