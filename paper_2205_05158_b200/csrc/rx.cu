@@ -161,8 +161,26 @@ __global__ void __launch_bounds__(128) k_rx_combine_blk(const float2* __restrict
 #pragma unroll
                 for (int c = 0; c < UC; ++c) acc[s][c] = make_float2(0.f, 0.f);
             const float2* H = hfd + (size_t)u0 * B * N_d + j;
-#pragma unroll 2
-            for (int b = 0; b < B; ++b) {
+            int b = 0;
+            // 4 antennas' loads (4 (UC + NS)) in flight before the MACs
+            for (; b + 4 <= B; b += 4) {
+                float2 hv[4][UC], xv[4][NS];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int c = 0; c < UC; ++c)
+                        hv[q][c] = (u0 + c < U) ? __ldg(H + ((size_t)c * B + b + q) * N_d) : make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) xv[q][s] = __ldg(Xc[s] + (size_t)(b + q) * N_d);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+#pragma unroll
+                        for (int c = 0; c < UC; ++c) acc[s][c] = cfma(hv[q][c], xv[q][s], acc[s][c]);
+            }
+            for (; b < B; ++b) {
                 float2 hv[UC], xv[NS];
 #pragma unroll
                 for (int c = 0; c < UC; ++c)
