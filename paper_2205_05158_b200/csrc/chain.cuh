@@ -67,14 +67,16 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     // mbarrier was 6% slower on C2 — every thread then waits for the whole 38 KB.)
     float2* xs = reinterpret_cast<float2*>(esm);
     stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
-    if (imp.precoded) {
+    const float2* Pb = P + (size_t)n * imp.p_stride + (size_t)b * U * N_d;
+    const float2* sn = s + n * U * N_d;
+    if constexpr (PZ > 0) {
+        // (PZ > 0: the precode is fused into the sparse first IDFT pass below)
+    } else if (imp.precoded) {
         // P holds the precoded spectrum X [n_sym][B][N_d] (chain_txrx_pre): one coalesced
         // pass over the symbol-antenna row into xs
         const float2* Xr = P + nb * N_d;
         for (int j = tid; j < N_d; j += T) xs[j] = cscale(__ldg(Xr + j), sc);
     } else {
-        const float2* Pb = P + (size_t)n * imp.p_stride + (size_t)b * U * N_d;
-        const float2* sn = s + n * U * N_d;
         // (Measured: a 4-subcarrier x 4-user predicated batch of 32 loads was 3% slower on
         // C2 than this loop — the extra address arithmetic outweighs the fewer round trips.)
         for (int j = tid; j < N_d; j += T) {
@@ -98,23 +100,65 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
             xs[j] = cscale(acc, sc);   // the IDFT's N^-1/2 on the N_d data bins instead of the N outputs
         }
     }
-    __syncthreads();
+    if constexpr (PZ == 0) __syncthreads();
     float2 v[VPT];
     const int h = N_d >> 1;
     if constexpr (PZ > 0) {
-        // sparse first IDFT pass: slots r = 0, 15 (and 1, 14 for PZ = 2) of each butterfly
+        // sparse first IDFT pass: slots r = 0, 15 (and 1, 14 for PZ = 2) of each butterfly.
+        // The slots of the radix-16 pass partition the data bins, so each thread precodes
+        // exactly the (2 PZ) bins its butterflies read, straight into registers: no compact
+        // spectrum in shared memory and no barrier between the precode and the first pass.
         static_assert(pass_radix<LOG2N>(0) == 16, "pruned pass 0 needs radix 16");
-        auto bin = [&](int pos) {
-            const bool lo = pos < h, hi = pos >= N - h;
-            const float2 t = xs[lo ? pos + h : (hi ? pos - (N - h) : 0)];
-            return (lo || hi) ? t : make_float2(0.f, 0.f);
-        };
+        constexpr int NB = 2 * PZ;
+        const float2* Xr = P + nb * N_d;
 #pragma unroll
         for (int q = 0; q < VPT / 16; ++q) {
             const int j = tid + q * T;
-            const float2 x0 = bin(j), x15 = bin(j + 15 * (N / 16));
-            const float2 x1 = PZ == 2 ? bin(j + N / 16) : make_float2(0.f, 0.f);
-            const float2 x14 = PZ == 2 ? bin(j + 14 * (N / 16)) : make_float2(0.f, 0.f);
+            int pos[NB];
+            pos[0] = j;
+            pos[NB - 1] = j + 15 * (N / 16);
+            if constexpr (PZ == 2) {
+                pos[1] = j + N / 16;
+                pos[2] = j + 14 * (N / 16);
+            }
+            int jd[NB];
+            bool ok[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const bool lo = pos[i] < h, hi = pos[i] >= N - h;
+                ok[i] = lo || hi;
+                jd[i] = lo ? pos[i] + h : (hi ? pos[i] - (N - h) : 0);
+            }
+            float2 xb[NB];
+            if (imp.precoded) {
+#pragma unroll
+                for (int i = 0; i < NB; ++i) xb[i] = ok[i] ? cscale(__ldg(Xr + jd[i]), sc) : make_float2(0.f, 0.f);
+            } else {
+                float2 acc[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) acc[i] = make_float2(0.f, 0.f);
+                for (int u = 0; u < U; u += 2) {   // 2 users x NB bins x 2 operands in flight
+                    float2 pv[2][NB], sv[2][NB];
+#pragma unroll
+                    for (int k = 0; k < 2; ++k)
+#pragma unroll
+                        for (int i = 0; i < NB; ++i) {
+                            const bool o = ok[i] && u + k < U;
+                            const int e = (u + k) * N_d + jd[i];
+                            pv[k][i] = o ? __ldg(Pb + e) : make_float2(0.f, 0.f);
+                            sv[k][i] = o ? __ldg(sn + e) : make_float2(0.f, 0.f);
+                        }
+#pragma unroll
+                    for (int k = 0; k < 2; ++k)
+#pragma unroll
+                        for (int i = 0; i < NB; ++i) acc[i] = cfma(pv[k][i], sv[k][i], acc[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < NB; ++i) xb[i] = ok[i] ? cscale(acc[i], sc) : make_float2(0.f, 0.f);
+            }
+            const float2 x0 = xb[0], x15 = xb[NB - 1];
+            const float2 x1 = PZ == 2 ? xb[1] : make_float2(0.f, 0.f);
+            const float2 x14 = PZ == 2 ? xb[NB - 2] : make_float2(0.f, 0.f);
             float2 X[16];
             dft16_sparse_in<+1, PZ>(x0, x1, x14, x15, X);
 #pragma unroll
