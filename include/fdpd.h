@@ -307,6 +307,18 @@ int fd_chain_run_device(fd_chain* chain, const void* s, const uint16_t* tx_idx, 
 int fd_chain_run_host(fd_chain* chain, const void* s_host, const uint16_t* tx_idx_host, long long n_sym,
                       long long* counts_host, cudaStream_t stream);
 
+/* HOST QAM index stream (pinned): the transmitter's symbol mapping runs on the device
+ * (qam_map), so only the uint16 indices cross PCIe (2 B instead of 10 B per data
+ * subcarrier); otherwise identical to fd_chain_run_host. */
+int fd_chain_run_host_qam(fd_chain* chain, const uint16_t* tx_idx_host, long long n_sym, long long* counts_host,
+                          cudaStream_t stream);
+
+/* a0 QAM mapping (reading A19; "data symbols"): s = (l_I + j l_Q) c_M with
+ * m = sqrt(M_qam), I = idx mod m, Q = idx div m, l = 2 I - (m - 1), c_M = (2 (M_qam - 1) / 3)^-1/2
+ * evaluated in fp64 and rounded to complex64 (E|s|^2 = 1).  idx device uint16 [count],
+ * s device complex64 [count].  FD_ERR_ARG if M_qam is not a square >= 4 or a pointer is NULL. */
+int qam_map(const uint16_t* idx, void* s, long long count, int M_qam, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,8 @@ SIGNATURES = {
     "fd_chain_destroy": (None, [_vp]),
     "fd_chain_run_device": (_i, [_vp, _vp, _vp, _ll, _vp, _vp, _vp]),
     "fd_chain_run_host": (_i, [_vp, _vp, _vp, _ll, _vp, _vp]),
+    "fd_chain_run_host_qam": (_i, [_vp, _vp, _ll, _vp, _vp]),
+    "qam_map": (_i, [_vp, _vp, _ll, _i, _vp]),
 }
 
 
@@ -151,6 +153,14 @@ def set_cnn_path(path: int):
     """Choose the FD-CNN implementation (include/fdpd.h fd_set_cnn_path): CNN_AUTO (tensor
     cores where every hidden width is 16/32/64), CNN_SIMT or CNN_TENSOR.  Process-wide."""
     _check(lib().fd_set_cnn_path(int(path)))
+
+
+def qam_map(idx, M_qam, out=None):
+    """a0: complex64 QAM points of uint16 indices on the device (include/fdpd.h qam_map)."""
+    _dev(idx, torch.uint16, "idx")
+    out = torch.empty(idx.shape, dtype=torch.complex64, device=idx.device) if out is None else out
+    _check(lib().qam_map(_ptr(idx), _ptr(out), idx.numel(), int(M_qam), _stream(idx)))
+    return out
 
 
 def set_chain_split(mode: int):
@@ -498,6 +508,13 @@ class NativeChain:
         st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         _check(lib().fd_chain_run_host(self.h, C.c_void_p(s_host.data_ptr()), C.c_void_p(idx_host.data_ptr()),
                                        s_host.shape[0], C.c_void_p(counts_host.data_ptr()), st))
+        return counts_host
+
+    def run_host_qam(self, idx_host, counts_host):
+        """idx_host, counts_host: (pinned) CPU tensors; the QAM mapping runs on the device."""
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().fd_chain_run_host_qam(self.h, C.c_void_p(idx_host.data_ptr()), idx_host.shape[0],
+                                           C.c_void_p(counts_host.data_ptr()), st))
         return counts_host
 
     def close(self):

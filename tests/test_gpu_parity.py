@@ -497,12 +497,26 @@ def test_native_runtime_matches(F, name):
     c_host = torch.zeros(3, dtype=torch.int64).pin_memory()
     nat.run_host(torch.from_numpy(inp["s"]).pin_memory(), torch.from_numpy(inp["idx"]).pin_memory(), c_host)
     assert torch.equal(c_host, c_ref.cpu())
+    c_q = torch.zeros(3, dtype=torch.int64).pin_memory()
+    nat.run_host_qam(torch.from_numpy(inp["idx"]).pin_memory(), c_q)      # device QAM mapping
+    assert torch.equal(c_q, c_ref.cpu())
     if name == "C1":
         o = O.run_config(cfg, inp)
         assert c_host[1] == o["counts"][1] and abs(int(c_host[0]) - int(o["counts"][0])) <= int(o["counts"][2])
     with pytest.raises(F.FdpdError):
         nat.run_device(torch.cat([s, s]), torch.cat([idx, idx]), c_dev)     # beyond the plan's batch
     nat.close()
+
+
+@pytest.mark.parametrize("M", [4, 16, 64, 256])
+def test_qam_map_matches_generator(F, M):
+    """a0 on the device: bit-identical to the generator's complex64 points (fp64 then round)."""
+    rng = np.random.default_rng(M)
+    idx = rng.integers(0, M, size=(3, 5, 77)).astype(np.uint16)
+    got = host(F.qam_map(torch.from_numpy(idx.astype(np.int32)).cuda().to(torch.uint16), M))
+    assert np.array_equal(got.view(np.uint64), gen.qam_symbols(idx, M).view(np.uint64))
+    with pytest.raises(F.FdpdError):
+        F.qam_map(torch.zeros(4, dtype=torch.uint16, device="cuda"), 12)
 
 
 # ============================================================================ edge cases / errors
