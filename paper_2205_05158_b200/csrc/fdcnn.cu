@@ -19,9 +19,9 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
                      void* workspace, long long n_sym, int U, int N_d, cudaStream_t stream);
 
 // FD_CNN_AUTO picks the tensor-core path where it applies and some hidden width is >= 32
-// (C3-C5); at width 16 (C2) the whole-network SIMT kernel is faster (measured 0.51 vs 1.02 ms
-// per 1024 symbols: an SS-mode MMA costs the same at N = 32 as at N = 128, and the per-layer
-// tensor path pays an HBM round trip per layer).
+// (C3-C5); at width 16 (C2) the whole-network SIMT kernel is faster (measured 0.51 vs 0.57 ms
+// per 1024 symbols: the per-layer tensor path pays an HBM round trip per layer and its
+// 2 -> 16 first layer is epilogue-bound).
 static int g_cnn_path = FD_CNN_AUTO;
 static bool use_tc(const int* chans, int n_layers) {
     if (g_cnn_path == FD_CNN_SIMT || !tc_supported(chans, n_layers)) return false;
