@@ -426,16 +426,18 @@ def test_end_to_end(F, name, fused):
         assert abs(int(counts[0]) - int(o["counts"][0])) <= int(near.sum())
 
 
-@pytest.mark.parametrize("name,nsym", [("C3", 8), ("C4", 8), ("C5", 8)])
-def test_end_to_end_large(F, name, nsym):
+@pytest.mark.parametrize("name,nsym,pick", [("C3", 8, 5), ("C4", 8, 5), ("C5", 8, 5), ("C3", 512, 509),
+                                           ("C4", 128, 125), ("C5", 32, 29)])
+def test_end_to_end_large(F, name, nsym, pick):
     """The large configurations through the whole step on their own paths: tensor-core CNN
     with the FP32 last layer, the tiled precode + chain_txrx_pre (U >= 16), the N = 8192
-    256-thread / N = 16384 cluster-split chain, the staged-tile channel sum.  One symbol of
-    the batch (index 5, inside the first 8-symbol tile) against the oracle."""
+    256-thread / N = 16384 cluster-split chain, the staged-tile channel sum.  Small batches
+    and the bench's batches (C3 512, C4 128, C5 32 symbols per step); one symbol of the batch
+    (in the last 8-symbol tile for the bench batches) against the oracle."""
     cfg = configs.get(name)
     inp = gen.make_inputs(cfg, range(nsym))
     ch, st, y, yhat, counts, dec = _gpu_chain(F, cfg, inp)
-    pick = [5]
+    pick = [pick]
     o = O.run_config(cfg, gen.make_inputs(cfg, pick))
     assert abs(ch.alpha / o["alpha"] - 1) < 1e-6
     assert rel(st[pick], o["s_tilde"]) < TOL
