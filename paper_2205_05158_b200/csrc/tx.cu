@@ -130,19 +130,73 @@ __device__ __forceinline__ void load_spectrum(float2 (&v)[(1 << LOG2N) / fft_thr
 }
 
 // ============================================================================ OFDM IDFT
-template <int LOG2N>
+// One CTA per (symbol, antenna).  N^-1/2 is applied to the N_d input bins; with PZ > 0 the
+// first radix-16 pass is the sparse one (each thread loads exactly the 2 PZ data bins its
+// butterflies read, see chain.cuh); the last pass writes its outputs straight to global memory
+// (coalesced: for a fixed output slot r the warp's lanes write consecutive samples), so the
+// waveform never makes a natural-order round trip through shared memory.
+template <int LOG2N, int PZ>
 __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>()) k_ofdm(const float2* __restrict__ X, float2* __restrict__ x,
                                                               const float2* __restrict__ tw, int B, int N_d, float sc) {
-    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T;
+    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, NPS = n_passes<LOG2N>();
+    static_assert(PZ == 0 || NPS >= 2, "pruned first pass needs a later pass");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* sm = reinterpret_cast<float2*>(smem_raw);
     const int tid = threadIdx.x;
     const size_t nb = blockIdx.x;
+    const float2* Xnb = X + nb * N_d;
+    const int h = N_d >> 1;
     float2 v[VPT];
-    load_spectrum<LOG2N>(v, X + nb * N_d, N_d, tid);
-    fft_run<LOG2N, +1>(sm, v, tw, tid);
+    if constexpr (PZ > 0) {
+        constexpr int NB = 2 * PZ;
+#pragma unroll
+        for (int q = 0; q < VPT / 16; ++q) {
+            const int j = tid + q * T;
+            int pos[NB];
+            pos[0] = j;
+            pos[NB - 1] = j + 15 * (N / 16);
+            if constexpr (PZ == 2) {
+                pos[1] = j + N / 16;
+                pos[2] = j + 14 * (N / 16);
+            }
+            float2 xb[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const bool lo = pos[i] < h, hi = pos[i] >= N - h;
+                xb[i] = (lo || hi) ? cscale(__ldg(Xnb + (lo ? pos[i] + h : pos[i] - (N - h))), sc)
+                                   : make_float2(0.f, 0.f);
+            }
+            float2 Y[16];
+            dft16_sparse_in<+1, PZ>(xb[0], PZ == 2 ? xb[1] : make_float2(0.f, 0.f),
+                                    PZ == 2 ? xb[NB - 2] : make_float2(0.f, 0.f), xb[NB - 1], Y);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) sm[pidx(16 * j + r)] = Y[r];
+        }
+        __syncthreads();
+        if constexpr (NPS > 2) fft_run<LOG2N, +1, 1, NPS - 1>(sm, v, tw, tid);
+    } else {
+        load_spectrum<LOG2N>(v, Xnb, N_d, tid);
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) v[i] = cscale(v[i], sc);
+        if constexpr (NPS > 1) fft_run<LOG2N, +1, 0, NPS - 1>(sm, v, tw, tid);
+    }
+    // last pass -> global
+    constexpr int PL = NPS - 1, RL = pass_radix<LOG2N>(PL), NSL = pass_ns<LOG2N>(PL);
+    if constexpr (PL > 0) pass_load_smem<RL, VPT, T, N>(sm, v, tid);
     float2* xo = x + nb * N;
-    for (int i = tid; i < N; i += T) xo[i] = cscale(sm[pidx(i)], sc);
+#pragma unroll
+    for (int q = 0; q < VPT / RL; ++q) {
+        const int j = tid + q * T;
+        const int k = j & (NSL - 1);
+        if constexpr (NSL > 1) {
+            if constexpr (RL == 16) pass_twiddle_tab16<+1>(v, q * RL, k, NSL, tw + tw_pass_off(N, PL));
+            else pass_twiddle<RL, +1>(v, q * RL, k * (N / (NSL * RL)), tw);
+        }
+        dftR<RL, +1>(v, q * RL);
+        const int dd = (j - k) * RL + k;
+#pragma unroll
+        for (int r = 0; r < RL; ++r) xo[dd + r * NSL] = v[q * RL + r];
+    }
 }
 
 // ============================================================================ GMP (standalone)
@@ -212,9 +266,19 @@ static int launch_ofdm(const float2* X, float2* x, long long n_sym, int B, int N
     const float2* tw = twiddle_table(N, st);
     if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
     const size_t smem = sizeof(float2) * padded_len(N);
-    set_smem(k_ofdm<LOG2N>, smem);
-    k_ofdm<LOG2N><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(X, x, tw, B, N_d,
-                                                                          (float)(1.0 / std::sqrt((double)N)));
+    const float sc = (float)(1.0 / std::sqrt((double)N));
+    const int pz = LOG2N >= 8 ? prune_slots(N, N_d) : 0;
+    auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        kern<<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(X, x, tw, B, N_d, sc);
+    };
+    if constexpr (LOG2N >= 8) {
+        if (pz == 1) go(k_ofdm<LOG2N, 1>);
+        else if (pz == 2) go(k_ofdm<LOG2N, 2>);
+        else go(k_ofdm<LOG2N, 0>);
+    } else {
+        go(k_ofdm<LOG2N, 0>);
+    }
     return check_launch("ofdm_modulate");
 }
 

@@ -44,7 +44,8 @@ def crandn(rng, *shape, scale=1.0):
 
 # ============================================================================ a4 / FFT
 @pytest.mark.parametrize("N,Nd", [(16, 8), (32, 20), (64, 64), (128, 36), (256, 100), (512, 300), (1024, 600),
-                                  (2048, 1200), (4096, 600), (8192, 1200), (16384, 3300)])
+                                  (2048, 1200), (4096, 600), (8192, 1200), (16384, 3300), (4096, 384), (256, 20),
+                                  (256, 34), (16384, 16384)])
 def test_ofdm_modulate(F, N, Nd):
     rng = np.random.default_rng(N)
     X = crandn(rng, 3, 5, Nd)
