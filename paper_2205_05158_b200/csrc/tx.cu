@@ -135,8 +135,12 @@ __device__ __forceinline__ void load_spectrum(float2 (&v)[(1 << LOG2N) / fft_thr
 // butterflies read, see chain.cuh); the last pass writes its outputs straight to global memory
 // (coalesced: for a fixed output slot r the warp's lanes write consecutive samples), so the
 // waveform never makes a natural-order round trip through shared memory.
+// (4 CTAs per SM up to N = 4096: no GMP state, so 64 registers suffice and the extra CTA
+// keeps more of the waveform stores in flight)
+template <int LOG2N>
+__host__ __device__ constexpr int ofdm_min_blocks() { return LOG2N <= 12 ? 4 : fft_min_blocks<LOG2N>(); }
 template <int LOG2N, int PZ>
-__global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>()) k_ofdm(const float2* __restrict__ X, float2* __restrict__ x,
+__global__ void __launch_bounds__(fft_threads<LOG2N>(), ofdm_min_blocks<LOG2N>()) k_ofdm(const float2* __restrict__ X, float2* __restrict__ x,
                                                               const float2* __restrict__ tw, int B, int N_d, float sc) {
     constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, NPS = n_passes<LOG2N>();
     static_assert(PZ == 0 || NPS >= 2, "pruned first pass needs a later pass");
