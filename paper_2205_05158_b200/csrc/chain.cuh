@@ -299,14 +299,6 @@ inline int launch_chain_one(const float2* P, const float2* s, const float2* coef
 }
 
 
-// Number of leading / trailing radix-16 slots holding data bins: ceil(h / (N/16)) for
-// h = N_d / 2, or 0 when the pruned passes do not apply (h > N/8 or N < 16).
-inline int prune_slots(int N, int N_d) {
-    const int h = N_d / 2, w = N / 16;
-    if (N < 16 || h < 1) return 0;
-    const int nz = (h + w - 1) / w;
-    return nz <= 2 ? nz : 0;
-}
 // Cluster-split chain_txrx for N = 8192 / 16384 (chain_cl.cu); returns -1 when it does not apply.
 int launch_chain_cluster(int log2n, int variant, const float2* P, const float2* s, const float2* coef, float2* y,
                          float2* XPA, long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp,

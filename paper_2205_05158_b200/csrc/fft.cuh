@@ -317,4 +317,12 @@ __device__ __forceinline__ int data_to_bin(int j, int N, int N_d) {
     return j >= h ? j - h : N - h + j;
 }
 
+// Number of leading / trailing radix-16 slots holding data bins: ceil(h / (N/16)) for
+// h = N_d / 2, or 0 when the pruned passes do not apply (h > N/8 or N < 16).
+inline int prune_slots(int N, int N_d) {
+    const int h = N_d / 2, w = N / 16;
+    if (N < 16 || h < 1) return 0;
+    const int nz = (h + w - 1) / w;
+    return nz <= 2 ? nz : 0;
+}
 }  // namespace fdpd

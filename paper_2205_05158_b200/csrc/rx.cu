@@ -6,7 +6,9 @@ namespace fdpd {
 
 // ============================================================================ receive DFT
 // XPA[n][b][j] = N^-1/2 sum_m y[n][b][m] e^{-2 pi i k_j m / N}
-template <int LOG2N>
+// PZ > 0 (N = 16^k, data bins within the first / last PZ radix-16 output slots): the last
+// pass computes only the outputs at data bins and writes XPA from registers (chain.cuh).
+template <int LOG2N, int PZ = 0>
 __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>()) k_rx_fft(const float2* __restrict__ y, float2* __restrict__ XPA,
                                                                 const float2* __restrict__ tw, int N_d, float sc) {
     constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
@@ -20,9 +22,31 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
     for (int q = 0; q < VPT / R0; ++q)
 #pragma unroll
         for (int r = 0; r < R0; ++r) v[q * R0 + r] = __ldg(yi + pass_pos<R0, VPT, T, N>(tid, q, r));
-    fft_run<LOG2N, -1>(sm, v, tw, tid);
     float2* xo = XPA + nb * N_d;
-    for (int j = tid; j < N_d; j += T) xo[j] = cscale(sm[pidx(data_to_bin(j, N, N_d))], sc);
+    if constexpr (PZ > 0) {
+        static_assert(LOG2N % 4 == 0 && LOG2N >= 8, "pruned last pass needs N = 16^k");
+        constexpr int NPS = n_passes<LOG2N>();
+        const int h = N_d >> 1;
+        fft_run<LOG2N, -1, 0, NPS - 1>(sm, v, tw, tid);
+        pass_load_smem<16, VPT, T, N>(sm, v, tid);
+#pragma unroll
+        for (int q = 0; q < VPT / 16; ++q) {
+            const int j = tid + q * T;
+            pass_twiddle_tab16<-1>(v, q * 16, j, N / 16, tw + tw_pass_off(N, NPS - 1));
+            float2 out[2 * PZ];
+            dft16_sparse_out<-1, PZ>(v, q * 16, out);
+#pragma unroll
+            for (int o = 0; o < 2 * PZ; ++o) {
+                const int r = o < PZ ? o : 16 - 2 * PZ + o;
+                const int k = j + r * (N / 16);
+                if (k < h) xo[k + h] = cscale(out[o], sc);
+                else if (k >= N - h) xo[k - (N - h)] = cscale(out[o], sc);
+            }
+        }
+    } else {
+        fft_run<LOG2N, -1>(sm, v, tw, tid);
+        for (int j = tid; j < N_d; j += T) xo[j] = cscale(sm[pidx(data_to_bin(j, N, N_d))], sc);
+    }
 }
 
 // ============================================================================ slicer
@@ -388,9 +412,19 @@ static int launch_rx_fft(const float2* y, float2* XPA, long long n_sym, int B, i
     const float2* tw = twiddle_table(N, st);
     if (!tw) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
     const size_t smem = sizeof(float2) * padded_len(N);
-    cudaFuncSetAttribute(k_rx_fft<LOG2N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_rx_fft<LOG2N><<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(y, XPA, tw, N_d,
-                                                                            (float)(1.0 / std::sqrt((double)N)));
+    const float sc = (float)(1.0 / std::sqrt((double)N));
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)(n_sym * B), fft_threads<LOG2N>(), smem, st>>>(y, XPA, tw, N_d, sc);
+    };
+    if constexpr (LOG2N % 4 == 0 && LOG2N >= 8) {
+        const int pz = prune_slots(N, N_d);
+        if (pz == 1) go(k_rx_fft<LOG2N, 1>);
+        else if (pz == 2) go(k_rx_fft<LOG2N, 2>);
+        else go(k_rx_fft<LOG2N, 0>);
+    } else {
+        go(k_rx_fft<LOG2N, 0>);
+    }
     return check_launch("ue_receive (fft)");
 }
 
