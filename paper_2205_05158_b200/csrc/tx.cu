@@ -216,13 +216,26 @@ __global__ void __launch_bounds__(256, 2) k_gmp(const float2* __restrict__ x, co
     const int b = (int)(nb % B);
     stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
     const float2* xi = x + nb * N;
-    for (int i = tid; i < N; i += T) {
-        const float2 t = xi[i];
-        usm[pidx(i)] = t;
-        esm[i] = fmaf(t.x, t.x, t.y * t.y);
+    if constexpr (KP > 0) {
+        // run-based evaluation (gmp.cuh, as in the fused chain): u and e = |u|^2 in the
+        // swizzled run layouts, runs of 4 samples, 128-bit stores of y
+        using Lay = RunLayout<4>;
+        for (int i = tid; i < N; i += T) {
+            const float2 t = __ldg(xi + i);
+            usm[Lay::u_phys(i)] = t;
+            esm[Lay::e_phys(i)] = fmaf(t.x, t.x, t.y * t.y);
+        }
+        __syncthreads();
+        gmp_runs_symbol<KP, L, M, 4>(usm, esm, cf, N, y + nb * N, tid, T);
+    } else {
+        for (int i = tid; i < N; i += T) {
+            const float2 t = xi[i];
+            usm[pidx(i)] = t;
+            esm[i] = fmaf(t.x, t.x, t.y * t.y);
+        }
+        __syncthreads();
+        gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
     }
-    __syncthreads();
-    gmp_symbol<KP, L, M, RS>(usm, esm, cf, N, d, y + nb * N, tid, T);
 }
 
 // ============================================================================ host side
