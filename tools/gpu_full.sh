@@ -10,6 +10,10 @@ for c in "C1" "C3 --batch 512" "C4 --batch 128" "C5 --batch 32" "P"; do
   tag=$(echo $c | cut -d' ' -f1)
   timeout 400 python bench.py --no-cpu-baseline --config $c > gpurun_out/bench_${T}_$tag.log 2>&1
 done
+timeout 400 python bench.py --no-cpu-baseline --impair > gpurun_out/bench_${T}_impair.log 2>&1
+timeout 400 python bench.py --no-cpu-baseline --redraw --steps 10 > gpurun_out/bench_${T}_redraw.log 2>&1
+timeout 400 python bench.py --no-cpu-baseline --unfused > gpurun_out/bench_${T}_unfused.log 2>&1
+timeout 600 python tools/stage_bench.py C2 1024 10 > gpurun_out/stage_${T}_c2.json 2>&1
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain_$T.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_$T.log 2>&1
 mkdir -p /tmp/reps
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_chain_tx|k_cnn_fused|k_rx_combine" -s 3 -c 3 -o /tmp/reps/c2 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_${T}.log 2>&1
