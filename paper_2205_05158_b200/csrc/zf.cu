@@ -164,6 +164,169 @@ __global__ void __launch_bounds__(256) k_zf(const float2* __restrict__ H, int T,
     }
 }
 
+// Warp-per-subcarrier variant for small U x B (C1-C3, P; per-warp shared slice <= 24 KB):
+// the same arithmetic, in the same order, as k_zf (so the results are bit-identical), but
+// eight subcarriers per CTA and no CTA-wide barriers — the per-symbol build of NEXT f4
+// (--redraw) issues N_d x n_sym of these tiny problems, where k_zf's 256-thread CTAs with
+// ten barriers each were mostly idle.
+constexpr int ZFW_WARPS = 8;
+__host__ __device__ inline size_t zf_warp_smem(int T, int U, int B) {
+    return ((sizeof(double2) * (3 * (size_t)U * U + T) + sizeof(float2) * (size_t)U * B) + 15) & ~(size_t)15;
+}
+__global__ void __launch_bounds__(32 * ZFW_WARPS) k_zf_warp(const float2* __restrict__ H, int T, int U, int B, int N,
+                                                          int N_d, int b0, int B_loc, float2* __restrict__ hfd,
+                                                          float2* __restrict__ P, double* __restrict__ tr,
+                                                          int* __restrict__ flag, const float2* __restrict__ Herr,
+                                                          double eta) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = blockIdx.x * ZFW_WARPS + warp;
+    if (j >= N_d) return;                                   // whole warp; no CTA barriers below
+    unsigned char* base = smem_raw + (size_t)warp * zf_warp_smem(T, U, B);
+    double2* G = reinterpret_cast<double2*>(base);
+    double2* Lm = G + U * U;
+    double2* Li = Lm + U * U;
+    double2* tw = Li + U * U;
+    float2* Hs = reinterpret_cast<float2*>(tw + T);
+    {
+        const size_t c = blockIdx.y;
+        H += c * T * U * B;
+        hfd += c * (size_t)U * B_loc * N_d;
+        P += c * (size_t)B_loc * U * N_d;
+        tr += c * N_d;
+    }
+    const int k = data_to_bin(j, N, N_d);
+    for (int t = lane; t < T; t += 32) {
+        double sn, cs;
+        sincospi(-2.0 * (double)(((long long)k * t) % N) / (double)N, &sn, &cs);
+        tw[t] = make_double2(cs, sn);
+    }
+    __syncwarp();
+    const double ce = sqrt(1.0 - eta), se = sqrt(eta);
+    for (int i = lane; i < U * B; i += 32) {
+        double2 acc = make_double2(0.0, 0.0), ace = make_double2(0.0, 0.0);
+        for (int t = 0; t < T; ++t) {
+            const float2 h = H[(size_t)t * U * B + i];
+            const double2 w = tw[t];
+            acc.x += (double)h.x * w.x - (double)h.y * w.y;
+            acc.y += (double)h.x * w.y + (double)h.y * w.x;
+            if (Herr) {
+                const float2 e = Herr[(size_t)t * U * B + i];
+                const double ex = ce * h.x + se * e.x, ey = ce * h.y + se * e.y;
+                ace.x += ex * w.x - ey * w.y;
+                ace.y += ex * w.y + ey * w.x;
+            }
+        }
+        const float2 hf = make_float2((float)acc.x, (float)acc.y);
+        Hs[i] = Herr ? make_float2((float)ace.x, (float)ace.y) : hf;
+        const int u = i / B, b = i % B;
+        if (b >= b0 && b < b0 + B_loc) hfd[((size_t)u * B_loc + (b - b0)) * N_d + j] = hf;
+    }
+    __syncwarp();
+    const int npair = U * (U + 1) / 2;
+    for (int pr = 0; pr < npair; ++pr) {
+        int u = 0;
+        while ((u + 1) * (u + 2) / 2 <= pr) ++u;
+        const int v = pr - u * (u + 1) / 2;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int b = lane; b < B; b += 32) {
+            const float2 a = Hs[u * B + b], c = Hs[v * B + b];
+            acc.x += (double)a.x * c.x + (double)a.y * c.y;
+            acc.y += (double)a.y * c.x - (double)a.x * c.y;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+        if (lane == 0) {
+            G[u * U + v] = acc;
+            G[v * U + u] = make_double2(acc.x, -acc.y);
+        }
+    }
+    for (int i = lane; i < U * U; i += 32) { Lm[i] = make_double2(0.0, 0.0); Li[i] = make_double2(0.0, 0.0); }
+    __syncwarp();
+    int bad = 0;
+    for (int c = 0; c < U; ++c) {
+        if (lane == 0) {
+            double d = G[c * U + c].x;
+            for (int p = 0; p < c; ++p) d -= Lm[c * U + p].x * Lm[c * U + p].x + Lm[c * U + p].y * Lm[c * U + p].y;
+            if (!(d > 1e-300)) { bad = 1; d = 1.0; }
+            Lm[c * U + c] = make_double2(sqrt(d), 0.0);
+        }
+        __syncwarp();
+        for (int i = c + 1 + lane; i < U; i += 32) {
+            double2 sv = G[i * U + c];
+            for (int p = 0; p < c; ++p) {
+                const double2 q = dcmulc(Lm[i * U + p], Lm[c * U + p]);
+                sv.x -= q.x;
+                sv.y -= q.y;
+            }
+            const double inv = 1.0 / Lm[c * U + c].x;
+            Lm[i * U + c] = make_double2(sv.x * inv, sv.y * inv);
+        }
+        __syncwarp();
+    }
+    bad = __shfl_sync(0xffffffffu, bad, 0);
+    if (bad && lane == 0) atomicExch(flag, 1);
+    for (int c = lane; c < U; c += 32) {
+        Li[c * U + c] = make_double2(1.0 / Lm[c * U + c].x, 0.0);
+        for (int i = c + 1; i < U; ++i) {
+            double2 sv = make_double2(0.0, 0.0);
+            for (int p = c; p < i; ++p) {
+                const double2 q = dcmul(Lm[i * U + p], Li[p * U + c]);
+                sv.x += q.x;
+                sv.y += q.y;
+            }
+            const double inv = -1.0 / Lm[i * U + i].x;
+            Li[i * U + c] = make_double2(sv.x * inv, sv.y * inv);
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < U * U; i += 32) {
+        const int u = i / U, v = i % U;
+        double2 sv = make_double2(0.0, 0.0);
+        for (int p = (u > v ? u : v); p < U; ++p) {
+            const double2 q = dcmulc(Li[p * U + v], Li[p * U + u]);
+            sv.x += q.x;
+            sv.y += q.y;
+        }
+        G[i] = sv;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double t = 0.0;
+        for (int u = 0; u < U; ++u) t += G[u * U + u].x;
+        tr[j] = t;
+    }
+    for (int i = lane; i < B_loc * U; i += 32) {
+        const int bl = i / U, u = i % U, b = bl + b0;
+        double2 sv = make_double2(0.0, 0.0);
+        for (int v = 0; v < U; ++v) {
+            const float2 h = Hs[v * B + b];
+            const double2 g = G[v * U + u];
+            sv.x += (double)h.x * g.x + (double)h.y * g.y;
+            sv.y += (double)h.x * g.y - (double)h.y * g.x;
+        }
+        P[((size_t)bl * U + u) * N_d + j] = make_float2((float)sv.x, (float)sv.y);
+    }
+}
+
+// Launches k_zf_warp where its per-warp slice fits (<= 24 KB), else k_zf.
+static void launch_zf_any(const float2* H, int T, int U, int B, int N, int N_d, int b0, int B_loc, float2* hfd,
+                          float2* P, double* tr, int* flag, const float2* Herr, double eta, int n_ch, size_t smem_cta,
+                          cudaStream_t st) {
+    const size_t per_warp = zf_warp_smem(T, U, B);
+    if (per_warp <= 24 * 1024) {
+        const size_t smem = per_warp * ZFW_WARPS;
+        cudaFuncSetAttribute(k_zf_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_zf_warp<<<dim3((N_d + ZFW_WARPS - 1) / ZFW_WARPS, n_ch), 32 * ZFW_WARPS, smem, st>>>(
+            H, T, U, B, N, N_d, b0, B_loc, hfd, P, tr, flag, Herr, eta);
+    } else {
+        cudaFuncSetAttribute(k_zf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cta);
+        k_zf<<<dim3(N_d, n_ch), 256, smem_cta, st>>>(H, T, U, B, N, N_d, b0, B_loc, hfd, P, tr, flag, Herr, eta);
+    }
+}
+
 // One CTA per channel realisation c: fixed-order fp64 sum of tr_j, alpha_c (A12); also a
 // float copy for the slicer when alpha_f != NULL.
 __global__ void k_zf_alpha(const double* __restrict__ tr, int N_d, double scale, double rho, double* alpha,
@@ -244,10 +407,8 @@ int zf_precoder_build_ex(const void* h_taps, const void* h_err, float eta, int T
     double* dalpha = tr + N_d;
     int* flag = (int*)(dalpha + 1);
     if (cudaMemsetAsync(flag, 0, sizeof(int), stream) != cudaSuccess) return check_launch("zf memset");
-    cudaFuncSetAttribute(k_zf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_zf<<<N_d, 256, smem, stream>>>((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc, (float2*)h_fd,
-                                     (float2*)P, tr, flag, eta > 0.f ? (const float2*)h_err : nullptr,
-                                     (double)eta);
+    launch_zf_any((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc, (float2*)h_fd, (float2*)P, tr, flag,
+                  eta > 0.f ? (const float2*)h_err : nullptr, (double)eta, 1, smem, stream);
     rc = check_launch("zf_precoder_build");
     if (rc) return rc;
     k_zf_alpha<<<1, 256, 0, stream>>>(tr, N_d, (double)B * (double)N_ifft, (double)rho, dalpha, nullptr);
@@ -283,9 +444,8 @@ int zf_precoder_build_batched(const void* h_taps, int n_ch, int T, int U, int B,
     double* dalpha = tr + (size_t)n_ch * N_d;
     int* flag = status ? status : (int*)(dalpha + n_ch);
     if (cudaMemsetAsync(flag, 0, sizeof(int), stream) != cudaSuccess) return check_launch("zf memset");
-    cudaFuncSetAttribute(k_zf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_zf<<<dim3(N_d, n_ch), 256, smem, stream>>>((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc,
-                                                 (float2*)h_fd, (float2*)P, tr, flag, nullptr, 0.0);
+    launch_zf_any((const float2*)h_taps, T, U, B, N_ifft, N_d, b0, B_loc, (float2*)h_fd, (float2*)P, tr, flag,
+                  nullptr, 0.0, n_ch, smem, stream);
     rc = check_launch("zf_precoder_build_batched");
     if (rc) return rc;
     k_zf_alpha<<<n_ch, 256, 0, stream>>>(tr, N_d, (double)B * (double)N_ifft, (double)rho, dalpha, alpha);
