@@ -173,6 +173,9 @@ constexpr int ZFW_WARPS = 8;
 __host__ __device__ inline size_t zf_warp_smem(int T, int U, int B) {
     return ((sizeof(double2) * (3 * (size_t)U * U + T) + sizeof(float2) * (size_t)U * B) + 15) & ~(size_t)15;
 }
+__host__ __device__ inline bool zf_taps_fit(int T, int U, int B) {
+    return sizeof(double2) * (size_t)T * U * B <= 48 * 1024;
+}
 __global__ void __launch_bounds__(32 * ZFW_WARPS) k_zf_warp(const float2* __restrict__ H, int T, int U, int B, int N,
                                                           int N_d, int b0, int B_loc, float2* __restrict__ hfd,
                                                           float2* __restrict__ P, double* __restrict__ tr,
@@ -181,8 +184,20 @@ __global__ void __launch_bounds__(32 * ZFW_WARPS) k_zf_warp(const float2* __rest
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = blockIdx.x * ZFW_WARPS + warp;
-    if (j >= N_d) return;                                   // whole warp; no CTA barriers below
     unsigned char* base = smem_raw + (size_t)warp * zf_warp_smem(T, U, B);
+    // the realisation's taps, converted to fp64 once per CTA and shared by its 8 subcarriers
+    // (when they fit: C1, C2, P) — the per-warp float loads + F2F conversions dominated
+    double2* Hd = reinterpret_cast<double2*>(smem_raw + (size_t)ZFW_WARPS * zf_warp_smem(T, U, B));
+    const bool shared_taps = Herr == nullptr && zf_taps_fit(T, U, B);
+    if (shared_taps) {
+        const float2* Hc = H + (size_t)blockIdx.y * T * U * B;
+        for (int i = threadIdx.x; i < T * U * B; i += blockDim.x) {
+            const float2 h = __ldg(Hc + i);
+            Hd[i] = make_double2((double)h.x, (double)h.y);
+        }
+        __syncthreads();
+    }
+    if (j >= N_d) return;                                   // whole warp; no CTA barriers below
     double2* G = reinterpret_cast<double2*>(base);
     double2* Lm = G + U * U;
     double2* Li = Lm + U * U;
@@ -205,16 +220,25 @@ __global__ void __launch_bounds__(32 * ZFW_WARPS) k_zf_warp(const float2* __rest
     const double ce = sqrt(1.0 - eta), se = sqrt(eta);
     for (int i = lane; i < U * B; i += 32) {
         double2 acc = make_double2(0.0, 0.0), ace = make_double2(0.0, 0.0);
-        for (int t = 0; t < T; ++t) {
-            const float2 h = H[(size_t)t * U * B + i];
-            const double2 w = tw[t];
-            acc.x += (double)h.x * w.x - (double)h.y * w.y;
-            acc.y += (double)h.x * w.y + (double)h.y * w.x;
-            if (Herr) {
-                const float2 e = Herr[(size_t)t * U * B + i];
-                const double ex = ce * h.x + se * e.x, ey = ce * h.y + se * e.y;
-                ace.x += ex * w.x - ey * w.y;
-                ace.y += ex * w.y + ey * w.x;
+        if (shared_taps) {
+            for (int t = 0; t < T; ++t) {
+                const double2 h = Hd[(size_t)t * U * B + i];
+                const double2 w = tw[t];
+                acc.x += h.x * w.x - h.y * w.y;
+                acc.y += h.x * w.y + h.y * w.x;
+            }
+        } else {
+            for (int t = 0; t < T; ++t) {
+                const float2 h = H[(size_t)t * U * B + i];
+                const double2 w = tw[t];
+                acc.x += (double)h.x * w.x - (double)h.y * w.y;
+                acc.y += (double)h.x * w.y + (double)h.y * w.x;
+                if (Herr) {
+                    const float2 e = Herr[(size_t)t * U * B + i];
+                    const double ex = ce * h.x + se * e.x, ey = ce * h.y + se * e.y;
+                    ace.x += ex * w.x - ey * w.y;
+                    ace.y += ex * w.y + ey * w.x;
+                }
             }
         }
         const float2 hf = make_float2((float)acc.x, (float)acc.y);
@@ -317,7 +341,8 @@ static void launch_zf_any(const float2* H, int T, int U, int B, int N, int N_d, 
                           cudaStream_t st) {
     const size_t per_warp = zf_warp_smem(T, U, B);
     if (per_warp <= 24 * 1024) {
-        const size_t smem = per_warp * ZFW_WARPS;
+        const size_t smem = per_warp * ZFW_WARPS +
+                            ((Herr == nullptr && zf_taps_fit(T, U, B)) ? sizeof(double2) * (size_t)T * U * B : 0);
         cudaFuncSetAttribute(k_zf_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_zf_warp<<<dim3((N_d + ZFW_WARPS - 1) / ZFW_WARPS, n_ch), 32 * ZFW_WARPS, smem, st>>>(
             H, T, U, B, N, N_d, b0, B_loc, hfd, P, tr, flag, Herr, eta);
