@@ -115,7 +115,10 @@ int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N
 
 /* -------------------------------------------------------------------------
  * a3. Precode — Eq. (1):  X[n][b][j] = sum_u P[b][u][j] * s[n][u][j].
- *  P [B_loc][U][N_d], s [n_sym][U][N_d] -> X [n_sym][B_loc][N_d], complex64.
+ *  P [B_loc][U][N_d], s [n_sym][U][N_d] -> X [n_sym][B_loc][N_d], complex64.  Summation over
+ *  u in ascending order (FP32 complex FMA), identical to the fused chain prologue.  FD_ERR_ARG
+ *  for bad sizes / NULL / misaligned pointers or U too large for the staged tile (8 U KB of
+ *  shared memory; U <= 800).
  * ------------------------------------------------------------------------- */
 int precode(const void* P, const void* s, void* X,
             long long n_sym, int B_loc, int U, int N_d, cudaStream_t stream);
