@@ -355,7 +355,8 @@ def run_ours(args, cfg):
         cnn_launches = 1                                   # whole network in shared memory
     else:
         cnn_launches = 2 * (len(cfg.chans) - 1)            # weight transpose + conv per layer
-    launches_per_step = cnn_launches + 1 + (2 if args.unfused else 1) + (3 if args.redraw else 0)
+    chain_launches = 2 if (cfg.U >= fdpd.SPLIT_PRECODE_MIN_U and not args.unfused) else 1   # (+ precode)
+    launches_per_step = cnn_launches + chain_launches + (2 if args.unfused else 1) + (3 if args.redraw else 0)
     if not args.unfused:                       # chain_txrx also runs the receive FFT
         tx_flop += 5 * cfg.N_ifft * int(np.log2(cfg.N_ifft)) * cfg.B * n
         achieved = tx_flop / (st_tx / 1e3) / 1e12
