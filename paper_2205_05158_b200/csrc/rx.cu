@@ -168,7 +168,9 @@ __global__ void __launch_bounds__(128) k_rx_combine_blk(const float2* __restrict
                                                         const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
                                                         long long* counts, SliceParams sp, Impair imp) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n0 = (long long)blockIdx.y * NS;
+    // symbols in reverse launch order: the chain kernel wrote the last symbols last, so their
+    // XPA rows are still in L2 when the first channel-sum CTAs start
+    const long long n0 = (long long)(gridDim.y - 1 - blockIdx.y) * NS;
     int err = 0, near = 0, cnt = 0;
     if (j < N_d) {
         const float2* Xc[NS];
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(256) k_rx_combine_tile(const float2* __restric
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = blockIdx.y * 32 + lane;
     const bool jok = j < N_d;
-    const long long n0 = (long long)blockIdx.x * NT;
+    const long long n0 = (long long)(gridDim.x - 1 - blockIdx.x) * NT;   // last-written symbols first (L2)
     const int nt = (int)min((long long)NT, n_sym - n0);
     const int u0 = warp * UPT;
     float2 acc[NT][UPT];
