@@ -15,7 +15,7 @@ struct ChainSmem {
 __host__ __device__ inline ChainSmem chain_smem(int N, int N_d, const GmpDesc& d, bool ysm) {
     ChainSmem s;
     const int r16 = 15;
-    s.off_e = (int)sizeof(float2) * padded_len(N);
+    s.off_e = ((int)sizeof(float2) * padded_len(N) + r16) & ~r16;   // 16-B aligned: float4 window loads (N = 16)
     const int e_bytes = ((N * 4 > N_d * 8 ? N * 4 : N_d * 8) + r16) & ~r16;
     s.off_cf = s.off_e + e_bytes;
     s.off_y = s.off_cf + ((8 * coef_smem_elems(d.Kp, d.L, d.M) + r16) & ~r16);

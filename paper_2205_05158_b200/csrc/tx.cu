@@ -204,13 +204,16 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), ofdm_min_blocks<LOG2N>()
 }
 
 // ============================================================================ GMP (standalone)
+__host__ __device__ inline int gmp_off_e(int N) { return ((int)sizeof(float2) * padded_len(N) + 15) & ~15; }
+__host__ __device__ inline int gmp_off_cf(int N) { return (gmp_off_e(N) + (int)sizeof(float) * N + 15) & ~15; }
 template <int KP, int L, int M, int RS>
 __global__ void __launch_bounds__(256, 2) k_gmp(const float2* __restrict__ x, const float2* __restrict__ coef,
                                              float2* __restrict__ y, int B, int N, GmpDesc d) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // regions 16-byte aligned (float4 window / coefficient loads; padded_len(16) * 8 = 136)
     float2* usm = reinterpret_cast<float2*>(smem_raw);
-    float* esm = reinterpret_cast<float*>(usm + padded_len(N));
-    float2* cf = reinterpret_cast<float2*>(esm + N);
+    float* esm = reinterpret_cast<float*>(smem_raw + gmp_off_e(N));
+    float2* cf = reinterpret_cast<float2*>(smem_raw + gmp_off_cf(N));
     const int tid = threadIdx.x, T = blockDim.x;
     const size_t nb = blockIdx.x;
     const int b = (int)(nb % B);
@@ -302,7 +305,7 @@ static int launch_ofdm(const float2* X, float2* x, long long n_sym, int B, int N
 template <int KP, int L, int M, int RS>
 static int launch_gmp(const float2* x, const float2* coef, float2* y, long long n_sym, int B, int N, const GmpDesc& d,
                       cudaStream_t st) {
-    const size_t smem = sizeof(float2) * padded_len(N) + sizeof(float) * N + sizeof(float2) * coef_smem_elems(d.Kp, d.L, d.M);
+    const size_t smem = (size_t)gmp_off_cf(N) + sizeof(float2) * coef_smem_elems(d.Kp, d.L, d.M);
     set_smem(k_gmp<KP, L, M, RS>, smem);
     k_gmp<KP, L, M, RS><<<(unsigned)(n_sym * B), 256, smem, st>>>(x, coef, y, B, N, d);
     return check_launch("gmp_pa");

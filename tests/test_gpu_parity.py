@@ -327,6 +327,44 @@ def test_chain_txrx_pruned_fft(F, N, N_d, orders, L, M):
     assert rel(host(XPA), want) < 2e-6
 
 
+_GMP_SHAPES = [((1, 3, 5), 2, 1), ((1, 3, 5, 7), 4, 2), ((1, 3, 5, 7, 9), 6, 3), ((1, 3, 5, 7), 3, 1), ((1, 5), 2, 1)]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_chain_random_shapes(F, seed):
+    """Seeded random shapes over every kernel variant (transform sizes 16..16384 incl. the
+    cluster split, pruned and generic FFT passes, specialised and generic GMP, ragged U/B):
+    fused chain_txrx vs the oracle and the fp64 FFT, chain_txrx_pre(precode) vs chain_txrx,
+    and the standalone ofdm_modulate -> gmp_pa vs the fused waveform."""
+    rng = np.random.default_rng(1000 + seed)
+    N = 1 << int(rng.integers(4, 15))
+    N_d = 2 * int(rng.integers(1, N // 2 + 1))
+    if seed % 3 == 0:
+        N_d = 4 * max(1, N_d // 4)          # N_d % 4 == 0 (cluster-split eligible at N = 16384)
+    U = int(rng.integers(1, 9))
+    B = int(rng.integers(U, U + 5))
+    n = int(rng.integers(1, 3))
+    orders, L, M = _GMP_SHAPES[seed % len(_GMP_SHAPES)]
+    if L + 2 * M >= N:
+        L, M = 1, 0
+    Kp = len(orders)
+    ncoef = Kp * (L + 1) + 2 * (Kp - 1) * (L + 1) * M
+    P = crandn(rng, B, U, N_d, scale=0.5)
+    s = crandn(rng, n, U, N_d)
+    coef = crandn(rng, B, ncoef, scale=0.05)
+    coef[:, 0] = 1.0
+    y, XPA = F.chain_txrx(dev(P), dev(s), dev(coef), orders, L, M, N)
+    x = O.ofdm_modulate(O.precode(P.transpose(2, 0, 1), s), N)
+    assert rel(host(y), O.gmp_pa(x, coef, orders, L, M)) < TOL, (N, N_d, U, B, orders, L, M)
+    want = np.fft.fft(host(y).astype(np.complex128), axis=-1, norm="ortho")[..., O.data_bins(N_d, N)]
+    assert rel(host(XPA), want) < 2e-6
+    X = F.precode(dev(P), dev(s))
+    y_pre, XPA_pre = F.chain_txrx_pre(X, dev(coef), orders, L, M, N)
+    assert rel(host(y_pre), host(y)) < 1e-6 and rel(host(XPA_pre), host(XPA)) < 1e-6
+    y2 = F.gmp_pa(F.ofdm_modulate(X, N), dev(coef), orders, L, M)
+    assert rel(host(y2), host(y)) < 1e-6
+
+
 @pytest.mark.parametrize("orders,L,M", [((1, 5, 9), 3, 0), ((1, 3), 1, 1)])
 def test_chain_txrx_generic_gmp(F, orders, L, M):
     cfg = configs.C2
