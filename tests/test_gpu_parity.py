@@ -129,6 +129,26 @@ def test_fdcnn_paths(F, cnn_path, path, chans, N_d, nsym, U):
     assert rel(got - s, want - s) < 1e-4
 
 
+@pytest.mark.parametrize("path", ["simt", "tensor"])
+@pytest.mark.parametrize("seed", range(8))
+def test_fdcnn_random_shapes(F, cnn_path, path, seed):
+    """Seeded random networks / image sizes on both CNN paths (tensor path: hidden widths in
+    {16, 32, 64}; SIMT path: any width) against the fp64 oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    depth = int(rng.integers(1, 5))
+    widths = [16, 32, 64] if path == "tensor" else [3, 8, 16, 20, 32]
+    chans = (2,) + tuple(int(rng.choice(widths)) for _ in range(depth)) + (2,)
+    N_d = 2 * int(rng.integers(1, 300))
+    U, nsym = int(rng.integers(1, 5)), int(rng.integers(1, 4))
+    cnn_path(F.CNN_SIMT if path == "simt" else F.CNN_TENSOR)
+    s = crandn(rng, nsym, U, N_d, scale=0.7)
+    n_par = sum(co * ci * 9 + co for ci, co in zip(chans[:-1], chans[1:]))
+    params = (0.05 * rng.standard_normal(n_par)).astype(np.float32)
+    got = host(F.fdcnn_forward(dev(params, torch.float32), chans, dev(s)))
+    want = O.fdcnn_forward(s, params, chans, N_d)
+    assert rel(got, want) < TOL, (chans, N_d, U, nsym)
+
+
 def test_fdcnn_tensor_full_batch_sampled(F, cnn_path):
     """C2 at the bench batch (1024 symbols) on the tensor-core path; the oracle checks
     sampled symbols one by one (the CNN acts per symbol image)."""
@@ -330,7 +350,7 @@ def test_chain_txrx_pruned_fft(F, N, N_d, orders, L, M):
 _GMP_SHAPES = [((1, 3, 5), 2, 1), ((1, 3, 5, 7), 4, 2), ((1, 3, 5, 7, 9), 6, 3), ((1, 3, 5, 7), 3, 1), ((1, 5), 2, 1)]
 
 
-@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("seed", range(24))
 def test_chain_random_shapes(F, seed):
     """Seeded random shapes over every kernel variant (transform sizes 16..16384 incl. the
     cluster split, pruned and generic FFT passes, specialised and generic GMP, ragged U/B):
