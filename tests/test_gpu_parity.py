@@ -383,6 +383,8 @@ def test_chain_random_shapes(F, seed):
     assert rel(host(y_pre), host(y)) < 1e-6 and rel(host(XPA_pre), host(XPA)) < 1e-6
     y2 = F.gmp_pa(F.ofdm_modulate(X, N), dev(coef), orders, L, M)
     assert rel(host(y2), host(y)) < 1e-6
+    h = crandn(rng, U, B, N_d, scale=0.3)                      # standalone receive path
+    assert rel(host(F.ue_receive(y, dev(h))), host(F.ue_combine(XPA, dev(h)))) < 2e-6
 
 
 @pytest.mark.parametrize("orders,L,M", [((1, 5, 9), 3, 0), ((1, 3), 1, 1)])
