@@ -65,75 +65,6 @@ __device__ __forceinline__ void stage_coefs(const float2* __restrict__ cg, float
     }
 }
 
-// Specialised path: orders = {1, 3, ..., 2 KP - 1}; coefficients in the CoefRow layout.
-// G accumulations are packed FP32 (FFMA2: complex coefficient x real feature).
-template <int KP, int L, int M, int RS>
-__device__ __forceinline__ void gmp_group(const float2* __restrict__ usm, const float* __restrict__ esm,
-                                          const float2* __restrict__ cf, int N, const int (&m)[RS],
-                                          float2 (&out)[RS]) {
-    using Row = CoefRow<KP, M>;
-    constexpr int W = 2 * M + 1;
-    constexpr int NP = KP > 1 ? KP - 1 : 1;
-    const int mask = N - 1;
-    float w[RS][W][NP];
-#pragma unroll
-    for (int r = 0; r < RS; ++r) {
-        out[r] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            const float e = esm[(m[r] - M + i) & mask];
-            w[r][i][0] = e;
-#pragma unroll
-            for (int k = 1; k < NP; ++k) w[r][i][k] = w[r][i][k - 1] * e;
-        }
-    }
-#pragma unroll
-    for (int l = 0; l <= L; ++l) {
-        if (l > 0) {
-#pragma unroll
-            for (int r = 0; r < RS; ++r) {
-#pragma unroll
-                for (int i = W - 1; i >= 1; --i)
-#pragma unroll
-                    for (int k = 0; k < NP; ++k) w[r][i][k] = w[r][i - 1][k];
-                const float e = esm[(m[r] - l - M) & mask];
-                w[r][0][0] = e;
-#pragma unroll
-                for (int k = 1; k < NP; ++k) w[r][0][k] = w[r][0][k - 1] * e;
-            }
-        }
-        const float4* row = reinterpret_cast<const float4*>(cf + l * Row::STRIDE);
-        float2 G[RS];
-#pragma unroll
-        for (int kk = 0; kk < Row::KPE / 2; ++kk) {
-            const float4 q = row[kk];
-            const float2 a0 = make_float2(q.x, q.y), a1 = make_float2(q.z, q.w);
-#pragma unroll
-            for (int r = 0; r < RS; ++r) {
-                G[r] = (kk == 0) ? a0 : cfma_real(a0, w[r][M][2 * kk - 1], G[r]);
-                if (2 * kk + 1 < KP) G[r] = cfma_real(a1, w[r][M][2 * kk], G[r]);
-            }
-        }
-#pragma unroll
-        for (int k = 1; k < KP; ++k)
-#pragma unroll
-            for (int g = 1; g <= M; ++g) {
-                const float4 q = row[Row::KPE / 2 + (k - 1) * M + (g - 1)];
-                const float2 bb = make_float2(q.x, q.y), cc = make_float2(q.z, q.w);
-#pragma unroll
-                for (int r = 0; r < RS; ++r) {
-                    G[r] = cfma_real(bb, w[r][M - g][k - 1], G[r]);
-                    G[r] = cfma_real(cc, w[r][M + g][k - 1], G[r]);
-                }
-            }
-#pragma unroll
-        for (int r = 0; r < RS; ++r) {
-            const float2 ul = usm[pidx((m[r] - l) & mask)];
-            out[r] = cfma2(ul, G[r], out[r]);
-        }
-    }
-}
-
 __device__ __forceinline__ float ipow(float e, int n) {
     float r = 1.f;
     for (int i = 0; i < n; ++i) r *= e;
@@ -173,42 +104,24 @@ __device__ __forceinline__ float2 gmp_sample_generic(const float2* __restrict__ 
     return out;
 }
 
-// Evaluate the GMP over the whole staged symbol and stream it to y (global).
-// Sample groups: thread handles m_r = i0 + r * (N / RS), i0 = tid, tid + T, ...
-// (consecutive threads -> consecutive samples: conflict-free LDS, coalesced STG).
-// KP == 0 selects the generic path.
+// Generic path over the whole staged symbol (pidx layout): any odd ascending orders,
+// runtime Kp, L, M; y (global) gets N samples.  (The specialised shapes use the run-based
+// evaluation below.)
 template <int KP, int L, int M, int RS>
 __device__ __forceinline__ void gmp_symbol(const float2* __restrict__ usm, const float* __restrict__ esm,
                                            const float2* __restrict__ cf, int N, const GmpDesc& d,
                                            float2* __restrict__ y, int tid, int T, const Impair* im = nullptr,
                                            unsigned long long nbase = 0) {
-    if constexpr (KP > 0) {
-        const int stride = N / RS;
-        for (int i0 = tid; i0 < stride; i0 += T) {
-            // keep the broadcast coefficient loads inside the loop (no hoisting of all
-            // n_coef complex values into registers, which would cap occupancy)
-            asm volatile("" ::: "memory");
-            int m[RS];
-            float2 out[RS];
-#pragma unroll
-            for (int r = 0; r < RS; ++r) m[r] = i0 + r * stride;
-            gmp_group<KP, L, M, RS>(usm, esm, cf, N, m, out);
-#pragma unroll
-            for (int r = 0; r < RS; ++r) y[m[r]] = im ? pa_impair(out[r], nbase + m[r], *im) : out[r];
-        }
-    } else {
-        for (int m = tid; m < N; m += T) {
-            const float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
-            y[m] = im ? pa_impair(o, nbase + m, *im) : o;
-        }
+    for (int m = tid; m < N; m += T) {
+        const float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
+        y[m] = im ? pa_impair(o, nbase + m, *im) : o;
     }
 }
 
-// Same as gmp_symbol for a CTA of T = fft_threads threads, but also leaves this
-// thread's outputs in `v` in the pass-0 register layout of the N-point FFT
-// (fft.cuh pass_pos): the samples a thread evaluates, {tid + T j : j < N/T}, are
-// exactly its pass-0 FFT inputs, so the receive DFT starts without a shared-memory
-// round trip.  y may be NULL (waveform not stored).
+// Same as gmp_symbol for a CTA of T = fft_threads threads, but also leaves this thread's
+// outputs in `v` in the pass-0 register layout of the N-point FFT (fft.cuh pass_pos): the
+// samples a thread evaluates, {tid + T j : j < N/T}, are exactly its pass-0 FFT inputs, so the
+// receive DFT starts without a shared-memory round trip.  y may be NULL (waveform not stored).
 template <int LOG2N, int KP, int L, int M, int RS>
 __device__ __forceinline__ void gmp_symbol_to_fft(const float2* __restrict__ usm, const float* __restrict__ esm,
                                                   const float2* __restrict__ cf, const GmpDesc& d,
@@ -219,36 +132,13 @@ __device__ __forceinline__ void gmp_symbol_to_fft(const float2* __restrict__ usm
     constexpr int QN = VPT / R0;      // pass-0 butterflies per thread
     // register slot of sample tid + T*j in the pass-0 layout: j = q + QN * r'
     auto slot = [](int j) { return (j % QN) * R0 + (j / QN); };
-    if constexpr (KP > 0) {
-        static_assert(VPT % RS == 0, "RS must divide N/T");
-        constexpr int G = VPT / RS;   // sample groups per thread; group k: j = k + G r
-#pragma unroll 1
-        for (int k = 0; k < G; ++k) {
-            asm volatile("" ::: "memory");
-            int m[RS];
-            float2 out[RS];
 #pragma unroll
-            for (int r = 0; r < RS; ++r) m[r] = tid + T * (k + G * r);
-            gmp_group<KP, L, M, RS>(usm, esm, cf, N, m, out);
-#pragma unroll
-            for (int r = 0; r < RS; ++r) {
-                if (im) out[r] = pa_impair(out[r], nbase + m[r], *im);
-                if (y) y[m[r]] = out[r];
-                // k is a runtime loop index: select the slot with a compile-time switch over k
-#pragma unroll
-                for (int kk = 0; kk < G; ++kk)
-                    if (kk == k) v[slot(kk + G * r)] = out[r];
-            }
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int m = tid + T * j;
-            float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
-            if (im) o = pa_impair(o, nbase + m, *im);
-            if (y) y[m] = o;
-            v[slot(j)] = o;
-        }
+    for (int j = 0; j < VPT; ++j) {
+        const int m = tid + T * j;
+        float2 o = gmp_sample_generic(usm, esm, cf, N, m, d);
+        if (im) o = pa_impair(o, nbase + m, *im);
+        if (y) y[m] = o;
+        v[slot(j)] = o;
     }
 }
 

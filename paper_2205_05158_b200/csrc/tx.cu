@@ -6,30 +6,14 @@ namespace fdpd {
 
 // ============================================================================ precode
 // X[n][b][j] = sum_u P[b][u][j] s[n][u][j]          (Eq. 1)
-__global__ void k_precode(const float2* __restrict__ P, const float2* __restrict__ s, float2* __restrict__ X,
-                          long long n_sym, int B, int U, int N_d) {
-    const long long total = n_sym * B * (long long)N_d;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int j = (int)(i % N_d);
-        const long long nb = i / N_d;
-        const int b = (int)(nb % B);
-        const long long n = nb / B;
-        float2 acc = make_float2(0.f, 0.f);
-        for (int u = 0; u < U; ++u)
-            acc = cfma(__ldg(P + ((size_t)b * U + u) * N_d + j), __ldg(s + ((size_t)n * U + u) * N_d + j), acc);
-        X[i] = acc;
-    }
-}
-
-// Tiled form used by the product path.  Per data subcarrier j the contraction is a small
-// complex GEMM X_j[n][b] = sum_u s_j[n][u] P_j[b][u] (K = U); the naive kernel above re-reads
-// P_b for every symbol and s_n for every antenna (U-fold L2 gathers per output).  Here a CTA
+// Per data subcarrier j the contraction is a small complex GEMM X_j[n][b] = sum_u s_j[n][u]
+// P_j[b][u] (K = U); a thread-per-output kernel re-reads P_b for every symbol and s_n for
+// every antenna (U-fold L2 gathers per output, the first version).  Here a CTA
 // owns 32 consecutive subcarriers (lane = j: coalesced 256-byte rows) x NT symbols x a range
 // of antennas: s_n for its NT symbols is staged once in shared memory ([NT][U][32], reused by
 // every antenna), and each thread accumulates NT x BPT outputs, so a P value fetched from L2
 // feeds NT symbols and an s value from shared memory BPT antennas.  The u summation order
-// (ascending, one complex FMA per term) is the same as k_precode and the fused chains.
+// (ascending, one complex FMA per term) is the same as the fused chains.
 constexpr int PC_NT = 8, PC_BPT = 4, PC_WARPS = 8;
 template <int NT, int BPT>
 __global__ void __launch_bounds__(32 * PC_WARPS) k_precode_tile(const float2* __restrict__ P, const float2* __restrict__ s,
@@ -97,25 +81,6 @@ __global__ void __launch_bounds__(32 * PC_WARPS) k_precode_tile(const float2* __
 }
 
 // ============================================================================ helpers
-// Fill the pass-0 registers with the precoded spectrum X = P_b s_n at data bins, 0 on guards.
-template <int LOG2N>
-__device__ __forceinline__ void load_precoded(float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
-                                              const float2* __restrict__ Pb, const float2* __restrict__ sn,
-                                              int U, int N_d, int tid) {
-    constexpr int N = 1 << LOG2N, T = fft_threads<LOG2N>(), VPT = N / T, R0 = pass_radix<LOG2N>(0);
-#pragma unroll
-    for (int q = 0; q < VPT / R0; ++q)
-#pragma unroll
-        for (int r = 0; r < R0; ++r) {
-            const int jj = bin_to_data(pass_pos<R0, VPT, T, N>(tid, q, r), N, N_d);
-            float2 acc = make_float2(0.f, 0.f);
-            if (jj >= 0)
-                for (int u = 0; u < U; ++u)
-                    acc = cfma(__ldg(Pb + (size_t)u * N_d + jj), __ldg(sn + (size_t)u * N_d + jj), acc);
-            v[q * R0 + r] = acc;
-        }
-}
-
 template <int LOG2N>
 __device__ __forceinline__ void load_spectrum(float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
                                               const float2* __restrict__ Xnb, int N_d, int tid) {
