@@ -79,16 +79,22 @@ __global__ void k_tc_weights(const float* __restrict__ W, float* __restrict__ Wg
 // Rings: A chunks (na) with a_full (256 arrivals) / a_empty (tcgen05.commit), weight slices
 // (ws) with wfull (TMA bytes) / wempty (commit), two TMEM accumulators with acc_full
 // (commit) / acc_empty (256 arrivals).
-constexpr int TC_EPI_WARPS = 8, TC_LOAD_WARPS = 8;
-constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_LOAD_WARPS, TC_W_WARP = TC_MMA_WARP + 1;
-constexpr int TC_THREADS = 32 * (TC_W_WARP + 1);
-constexpr int TC_LOAD_THREADS = 32 * TC_LOAD_WARPS;
-constexpr int TC_EPI_THREADS = 32 * TC_EPI_WARPS;
+// The first layer (IN_MODE 1: one K step per tap, C_out tanh per pixel) is bound by its
+// epilogue's dependent tanh chains at two warps per scheduler, so it runs 16 epilogue warps
+// (four column groups per TMEM lane quadrant) where C_out >= 32.
+template <int IN_MODE, int NP>
+struct TcRoles {
+    static constexpr int EPI = (IN_MODE == 1 && NP >= 32) ? 16 : 8;
+    static constexpr int LOAD = 8;
+    static constexpr int MMA_WARP = EPI + LOAD, W_WARP = MMA_WARP + 1;
+    static constexpr int THREADS = 32 * (W_WARP + 1);
+    static constexpr int LOAD_THREADS = 32 * LOAD, EPI_THREADS = 32 * EPI;
+};
 
 __host__ __device__ constexpr int tc_ck(int cinp) { return cinp >= 32 ? 32 : cinp; }
 
 template <int CINP, int NP, int IN_MODE, int OUT_MODE>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
     k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const float* __restrict__ Wg,
               const float* __restrict__ bias, float* __restrict__ act_out, float2* __restrict__ s_out, TcConv g) {
     constexpr int G = CINP / 4;           // 16-byte channel groups of a pixel in global memory
@@ -102,6 +108,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // the A_lo MMA reads only the first NP rows of B (W_hi): A_lo W_lo (~2^-22 relative) is
     // dropped and the MMA reads 25 % fewer shared-memory bytes
     constexpr uint32_t IDESC_LO = idesc_tf32_m128(NP);
+    using Roles = TcRoles<IN_MODE, NP>;
+    constexpr int TC_EPI_WARPS = Roles::EPI, TC_LOAD_WARPS = Roles::LOAD;
+    constexpr int TC_MMA_WARP = Roles::MMA_WARP, TC_W_WARP = Roles::W_WARP;
+    constexpr int TC_LOAD_THREADS = Roles::LOAD_THREADS, TC_EPI_THREADS = Roles::EPI_THREADS;
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + g.off_bar);
@@ -294,6 +304,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else {
         // ------------------------------------------------------------ epilogue (warps 0-7)
         // warp w reads TMEM lanes 32 (w % 4) .. + 31 (its pixels) and the column half w / 4
+        constexpr int NGRP = TC_EPI_WARPS / 4;    // column groups per TMEM lane quadrant
         const int quad = warp & 3, half = warp >> 2;
         int img = (int)blockIdx.x / g.n_tiles, t = (int)blockIdx.x - img * g.n_tiles;
         const int dimg = (int)gridDim.x / g.n_tiles, dt = (int)gridDim.x - dimg * g.n_tiles;
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const bool interior = pos < g.q_end && pcol >= 1 && pcol <= g.S;
             if constexpr (OUT_MODE == 0) {
                 float* o = act_out + ((size_t)img * g.P + pos) * NP;
-                constexpr int HC = NP / 2;            // columns per warp (>= 8)
+                constexpr int HC = NP / NGRP;         // columns per warp (>= 8)
 #pragma unroll
                 for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 8) {
                     float v[8], w[8], v2[8], w2[8];
@@ -529,12 +540,13 @@ static int launch_tc_na(const TcConv& g, size_t smem, const float* act_in, const
     auto kern = k_conv_tc<CINP, NP, IN_MODE, OUT_MODE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, dev = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, smem);
+    constexpr int THREADS = TcRoles<IN_MODE, NP>::THREADS;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long tiles = g.n_img * g.n_tiles;
     const long long grid = std::min<long long>(tiles, (long long)nsm * std::max(per_sm, 1));
-    kern<<<(unsigned)grid, TC_THREADS, smem, st>>>(act_in, s_in, Wg, bias, act_out, s_out, g);
+    kern<<<(unsigned)grid, THREADS, smem, st>>>(act_in, s_in, Wg, bias, act_out, s_out, g);
     return check_launch("fdcnn_forward (tensor-core conv)");
 }
 
