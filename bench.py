@@ -4,16 +4,18 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
 
 A step = one pass of the whole hot path over one batch
-of synthetic OFDM symbols of BASELINE.json configs[1] (C2: U=4, B=64, N_ifft=4096,
-1024 symbols): FD-CNN -> fused precode/IDFT/GMP (PA waveform written to HBM) ->
-receive DFT + channel sum + slicing/SER.  The ZF precoder (a2) is built once per
-channel realisation before timing (reading A10) and timed separately.
+of synthetic OFDM symbols.  Default workload: BASELINE.json configs[4] = C5, the
+north-star configuration (U=32, B=512, N_ifft=16384, N_d=3300, 256-QAM, 5-layer 64-channel
+FD-CNN), 32 symbols per GPU per step (SURVEY §8(d) streaming batch; the 4096-symbol run's
+275 GB waveform never coexists in memory).  Step: FD-CNN -> precode -> fused IDFT/GMP (PA
+waveform written to HBM) + receive DFT -> channel sum + slicing/SER.  The ZF precoder (a2)
+is built once per channel realisation before timing (reading A10) and timed separately.
 
-Multi-GPU (torchrun): symbol-batch sharding, weak scaling — each rank runs its
-own 1024-symbol batch (symbol indices rank*n_sym + i); the only collective is
-the int64 SER-counter all-reduce at the end of each step.  Timing: CUDA events
-per step on the launching stream, L2 flushed between steps (256 MiB write,
-outside the events), barrier + synchronize around the timed loop, max over ranks.
+Multi-GPU (torchrun): symbol-batch sharding (Mode S), weak scaling — each rank runs its
+own batch (symbol indices rank*n + i); the only collective is the int64 SER-counter
+all-reduce of each step.  Timing: CUDA events per step on the launching stream, L2
+flushed between steps (256 MiB write, outside the events), barrier + synchronize around
+the timed loop, max over ranks.
 """
 from __future__ import annotations
 
@@ -37,13 +39,14 @@ FP32_LANES_PER_SM = 128          # FP32 FMA lanes per SM (Blackwell SM: 4 SMSP x
 
 
 def peaks():
-    p = {"hbm_gbs": 6538.9, "sm_max_mhz": 1965.0, "src": "fallback"}
+    """Roofline denominators: MEASURED_PEAKS.json (driver-measured on this pool's B200s), else the
+    fallback of /opt/skills/guides/B200_PROFILING.md (6.65 TB/s, 1.59 PFLOP/s bf16)."""
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "src": "fallback"}
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as f:
             m = json.load(f)
-        p.update({"hbm_gbs": m.get("hbm_gbs", p["hbm_gbs"]), "sm_max_mhz": m.get("sm_max_mhz", p["sm_max_mhz"]),
-                  "src": "measured"})
+        p.update({k: m.get(k, p[k]) for k in ("hbm_gbs", "bf16_tflops", "sm_max_mhz")}, src="measured")
     return p
 
 
@@ -128,34 +131,56 @@ class ClockSampler:
 
 
 # ============================================================================ oracle timing
-def oracle_symbols_per_s(cfg, symbols, rank_seed_offset=0):
-    """Time the fp64 oracle (as it stands) on a bounded sample: the per-step stages
-    (CNN, precode, IDFT, GMP, receive, slice) over `symbols`; ZF built untimed, like the GPU."""
-    from oracle import fdpd_oracle as O
+def git_sha():
+    """The commit, or (on a GPU box, where the snapshot has no .git) a sha256 over the product
+    sources and bench.py, so a line can be matched to the code that produced it."""
     try:
-        from threadpoolctl import threadpool_limits
-    except ImportError:  # pragma: no cover
-        threadpool_limits = None
+        sha = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True, text=True,
+                             timeout=10).stdout.strip()
+        if sha:
+            return sha
+    except Exception:
+        pass
+    import hashlib
+    h = hashlib.sha256()
+    for d in ("paper_2205_05158_b200/csrc", "include", "paper_2205_05158_b200"):
+        full = os.path.join(ROOT, d)
+        for f in sorted(os.listdir(full)):
+            if f.endswith((".cu", ".cuh", ".h", ".py")):
+                with open(os.path.join(full, f), "rb") as fh:
+                    h.update(fh.read())
+    with open(os.path.join(ROOT, "bench.py"), "rb") as fh:
+        h.update(fh.read())
+    return "src-" + h.hexdigest()[:16]
+
+
+def oracle_sample(cfg, first_symbol, budget_cpu_s=20.0, max_wall_s=60.0, workers=None):
+    """Time the fp64 oracle (as it stands, oracle/parallel.py) on a bounded sample of the workload:
+    per-step stages (CNN, precode, IDFT, GMP, receive, slice) one OFDM symbol at a time, spread over
+    all host cores; ZF built untimed like the GPU's.  Runs symbols until ~budget_cpu_s of CPU work
+    (at least one).  Returns the cpu_baseline dict."""
+    from oracle import parallel as OP
+    cores = OP.host_cores() if workers is None else workers
+    per_sym_guess = {"C1": 0.002, "C2": 0.35, "C3": 1.7, "C4": 18.0, "C5": 45.0}.get(cfg.name[:2], 1.0)
+    k = int(max(1, min(64, budget_cpu_s // per_sym_guess)))
+    symbols = list(range(first_symbol, first_symbol + k))
     inp = gen.make_inputs(cfg, symbols)
-    Hfd = O.channel_fd(inp["h_taps"], cfg.N_ifft, cfg.N_d)
-    P, alpha, _ = O.zf_precoder(Hfd, cfg.N_ifft, cfg.rho)
-
-    def run():
-        t0 = time.perf_counter()
-        for i in range(len(symbols)):
-            s = inp["s"][i:i + 1]
-            st = O.fdcnn_forward(s, inp["params"], cfg.chans, cfg.N_d)
-            x = O.ofdm_modulate(O.precode(P, st), cfg.N_ifft)
-            y = O.gmp_pa(x, inp["coef"], cfg.orders, cfg.L, cfg.M)
-            O.slice_ser(O.ue_receive(y, Hfd, cfg.N_d), alpha, inp["idx"][i:i + 1], cfg.M_qam)
-        return time.perf_counter() - t0
-
-    if threadpool_limits is not None:
-        with threadpool_limits(limits=1):
-            dt = run()
-    else:
-        dt = run()
-    return len(symbols) / dt, dt
+    walls, cpus = [], []
+    with OP.OracleRunner(cfg, inp, workers=cores) as r:
+        for i in range(k):
+            _, w, c = r.symbol(i)
+            walls.append(w)
+            cpus.append(c)
+            if sum(walls) > max_wall_s:
+                break
+    n = len(walls)
+    return {"value": n / sum(walls), "unit": "symbols/s", "cores": cores, "kind": "oracle",
+            "value_1core": n / sum(cpus),
+            "sample": f"{n} symbol(s) of {cfg.name} (per-step stages a1, a3-a6; ZF built untimed), fp64 numpy oracle "
+                      f"over {cores} worker processes (1 BLAS thread each; FD-CNN per UE, precode/IDFT/GMP/receive "
+                      f"per antenna block), wall {sum(walls):.1f} s; value_1core = symbols / summed task CPU time "
+                      f"({sum(cpus):.1f} s)",
+            "cpu_model": OP.cpu_model(), "affinity_cores": OP.host_cores()}
 
 
 # ============================================================================ main arms
@@ -166,26 +191,44 @@ def init_dist():
     return ws, rank, local
 
 
+def batch_of(cfg, args):
+    return args.batch or cfg.bench_batch or cfg.n_sym
+
+
 def run_reference(args, cfg):
+    """The reference arm: the fp64 oracle as it stands, on the host cores of rank 0 (the other
+    ranks exit without work).  Each step = one OFDM symbol of the same workload (a bounded sample:
+    a C5 symbol is ~45 s of single-core work), spread over all host cores."""
+    from oracle import parallel as OP
     ws, rank, _ = init_dist()
     if rank != 0:
         return
-    k = max(1, args.ref_step_symbols)
-    for _ in range(args.warmup):
-        oracle_symbols_per_s(cfg, list(range(1)))
-    times = []
-    for st in range(args.steps):
-        _, dt = oracle_symbols_per_s(cfg, list(range(st * k, st * k + k)))
-        times.append(dt)
+    k = max(1, args.ref_step_symbols or (1 if cfg.name[:2] in ("C4", "C5") else 4))
+    total_steps = args.warmup + args.steps
+    inp = gen.make_inputs(cfg, list(range(total_steps * k)))
+    times, cpus = [], []
+    with OP.OracleRunner(cfg, inp) as r:
+        for st in range(total_steps):
+            w = c = 0.0
+            for i in range(st * k, st * k + k):
+                _, dw, dc = r.symbol(i)
+                w += dw
+                c += dc
+            if st >= args.warmup:
+                times.append(w)
+                cpus.append(c)
+        cores = r.workers
     total = sum(times)
     value = args.steps * k / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(cfg, ws, k),
-        "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{k} symbols of {cfg.name} per step, fp64 numpy oracle, 1 BLAS thread"},
+        "config": config_dict(cfg, ws, batch_of(cfg, args)),
+        "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": cores, "kind": "oracle",
+                         "value_1core": args.steps * k / sum(cpus), "cpu_model": OP.cpu_model(),
+                         "sample": f"{k} symbol(s) of {cfg.name} per step over {cores} worker processes (fp64 numpy "
+                                   f"oracle as it stands, 1 BLAS thread each); value_1core from summed task CPU time"},
         "e2e": {"value": value, "unit": "symbols/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -194,8 +237,17 @@ def run_reference(args, cfg):
 def config_dict(cfg, ws, batch):
     return {"workload": cfg.name, "U": cfg.U, "B": cfg.B, "N_ifft": cfg.N_ifft, "N_d": cfg.N_d, "M_qam": cfg.M_qam,
             "gmp": {"orders": list(cfg.orders), "L": cfg.L, "M": cfg.M}, "cnn_chans": list(cfg.chans),
+            "seed": cfg.seed, "git_sha": git_sha(),
             "symbols_per_gpu_per_step": batch, "global_batch_symbols": batch * ws,
             "parallelism": f"symbol-batch x{ws}", "l2": "flushed between steps (256 MiB write outside the events)"}
+
+
+def cnn_flop_per_symbol(cfg):
+    """Algorithmic FD-CNN FLOPs per OFDM symbol: 2 x 9 C_in C_out per pixel and layer, S^2 pixels
+    per UE image (P:180-195 counting convention, BASELINE network)."""
+    if cfg.head == "paper":
+        return 0
+    return cfg.U * cfg.S ** 2 * sum(2 * 9 * a * b for a, b in zip(cfg.chans[:-1], cfg.chans[1:]))
 
 
 def run_ours(args, cfg):
@@ -212,7 +264,7 @@ def run_ours(args, cfg):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     fdpd.lib()
-    n = args.batch or cfg.n_sym
+    n = batch_of(cfg, args)
     symbols = D.symbol_range(n, rank)          # Mode S, weak scaling
     inp = gen.make_inputs(cfg, symbols)
 
@@ -233,23 +285,33 @@ def run_ours(args, cfg):
     s = torch.from_numpy(inp["s"]).to(dev)
     idx = torch.from_numpy(inp["idx"]).to(dev)
     taps_all = torch.from_numpy(gen.channel_taps_per_symbol(cfg, symbols)).to(dev) if args.redraw else None
-    counts = torch.zeros(3, dtype=torch.int64, device=dev)
+    counts = torch.zeros(3, dtype=torch.int64, device=dev)          # one step's counters
+    total = torch.zeros(3, dtype=torch.int64, device=dev)           # summed over the timed steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sym0 = symbols[0]
+    split = ch.split_precode and not (args.redraw or args.unfused)
 
     def step(ev=None):
+        """ev: 4 events recorded after the CNN, the precode, the chain kernel and the combine."""
+        counts.zero_()
         st = ch.dpd(s)
         if ev is not None:
             ev[0].record(stream)
+        if split:
+            X = ch.precode(st)
+        if ev is not None:
+            ev[1].record(stream)
         if args.redraw:
             XPA = ch.redraw_txrx(st, taps_all, sym0)       # batched per-symbol ZF + chain_txrx_ps
         elif args.unfused:
             y = ch.tx(st)
+        elif split:
+            _, XPA = ch.txrx_pre(X, sym0)
         else:
             _, XPA = ch.txrx(st, sym0)
         if ev is not None:
-            ev[1].record(stream)
+            ev[2].record(stream)
         if args.redraw:
             ch.redraw_combine(XPA, idx, counts=counts, sym0=sym0)
         elif args.unfused:
@@ -257,19 +319,21 @@ def run_ours(args, cfg):
         else:
             ch.combine(XPA, idx, counts=counts, sym0=sym0)
         if ev is not None:
-            ev[2].record(stream)
+            ev[3].record(stream)
         if ws > 1:
             D.allreduce_counts(counts)
+        total.add_(counts)
 
     for _ in range(args.warmup):
         step()
         flush.zero_()
     torch.cuda.synchronize()
+    total.zero_()
     if ws > 1:
         dist.barrier()
 
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    evs = [(E(), E(), E(), E(), E()) for _ in range(args.steps)]
+    evs = [tuple(E() for _ in range(6)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         if ws > 1:
             dist.barrier()
@@ -277,13 +341,16 @@ def run_ours(args, cfg):
         for i in range(args.steps):
             flush.zero_()
             evs[i][0].record(stream)
-            step(ev=(evs[i][1], evs[i][2], evs[i][3]))
-            evs[i][4].record(stream)
+            step(ev=evs[i][1:5])
+            evs[i][5].record(stream)
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        # end-to-end through the C runtime (fd_chain_run_host): pinned host s and tx indices
-        # copied in, the step, the SER counters copied back, every step
+        total_h = total.cpu()
+        if int(total_h[1]) != args.steps * ws * n * cfg.U * cfg.N_d:
+            raise RuntimeError(f"step counters wrong: {total_h.tolist()}")
+        # end-to-end through the C runtime (fd_chain_run_host*): pinned host inputs copied in, the
+        # step, the SER counters copied back, every step
         s_h = torch.from_numpy(inp["s"]).pin_memory()
         i_h = torch.from_numpy(inp["idx"]).pin_memory()
         c_h = torch.zeros(3, dtype=torch.int64).pin_memory()
@@ -292,13 +359,21 @@ def run_ours(args, cfg):
         # per-call path as the timed step, with the host copies added around it
         use_native = not (args.impair or args.redraw or args.unfused)
         s_d, i_d = torch.empty_like(s), torch.empty_like(idx)
+        c_d = torch.zeros(3, dtype=torch.int64, device=dev)
+
+        def reduce_host(ch_host):
+            """all-reduce host counters through a persistent device buffer (Mode S counter sum)."""
+            if ws > 1:
+                c_d.copy_(ch_host, non_blocking=True)
+                D.allreduce_counts(c_d)
+                ch_host.copy_(c_d, non_blocking=True)
+
         for i in range(args.steps):
             flush.zero_()
             e2e_ev[i][0].record(stream)
             if use_native:
                 native.run_host(s_h, i_h, c_h)
-                if ws > 1:
-                    D.allreduce_counts(c_h.to(dev))
+                reduce_host(c_h)
             else:
                 s_d.copy_(s_h, non_blocking=True)
                 i_d.copy_(i_h, non_blocking=True)
@@ -311,7 +386,7 @@ def run_ours(args, cfg):
                 c_h.copy_(counts, non_blocking=True)
             e2e_ev[i][1].record(stream)
         torch.cuda.synchronize()
-        if int(c_h[1]) != n * cfg.U * cfg.N_d:
+        if int(c_h[1]) != ws * n * cfg.U * cfg.N_d:
             raise RuntimeError(f"e2e counters wrong: {c_h.tolist()}")
         # end-to-end from the QAM index stream (fd_chain_run_host_qam): only the uint16 indices
         # are copied in and the symbol mapping runs on the device
@@ -321,22 +396,22 @@ def run_ours(args, cfg):
             flush.zero_()
             e2e_q_ev[i][0].record(stream)
             native.run_host_qam(i_h, cq_h)
-            if ws > 1:
-                D.allreduce_counts(cq_h.to(dev))
+            reduce_host(cq_h)
             e2e_q_ev[i][1].record(stream)
         torch.cuda.synchronize()
         if use_native and not torch.equal(cq_h, c_h):
             raise RuntimeError(f"e2e (QAM indices) counters {cq_h.tolist()} != {c_h.tolist()}")
-    ms = sum(e[0].elapsed_time(e[4]) for e in evs)
+    ms = sum(e[0].elapsed_time(e[5]) for e in evs)
     ms_e2e = sum(a.elapsed_time(b) for a, b in e2e_ev)
     ms_e2e_q = sum(a.elapsed_time(b) for a, b in e2e_q_ev) if e2e_q_ev else 0.0
     st_dpd = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    st_tx = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-    st_rx = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
-    t = torch.tensor([ms, ms_e2e, st_tx, ms_e2e_q], dtype=torch.float64, device=dev)
+    st_pre = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    st_tx = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    st_rx = statistics.mean(e[3].elapsed_time(e[4]) for e in evs)
+    t = torch.tensor([ms, ms_e2e, st_tx, ms_e2e_q, st_dpd], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, ms_e2e, st_tx, ms_e2e_q = t.tolist()
+    ms, ms_e2e, st_tx, ms_e2e_q, st_dpd = t.tolist()
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -345,8 +420,17 @@ def run_ours(args, cfg):
     value = total_symbols / (ms / 1e3)
     pk = peaks()
     fp32_peak = 148 * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12       # TFLOP/s
-    tx_flop = chain_tx_flop_per_symbol(cfg) * n
-    achieved = tx_flop / (st_tx / 1e3) / 1e12
+    N = cfg.N_ifft
+    fft_flop = 5 * N * int(np.log2(N)) * cfg.B
+    if args.unfused:
+        kern, tx_flop = "chain_tx (precode+IDFT+GMP)", chain_tx_flop_per_symbol(cfg)
+    elif split:
+        kern = "chain_txrx_pre (IDFT+GMP+receive DFT)"
+        tx_flop = fft_flop + gmp_flop_per_sample(cfg) * N * cfg.B + fft_flop
+    else:
+        kern = "chain_txrx (precode+IDFT+GMP+receive DFT)"
+        tx_flop = chain_tx_flop_per_symbol(cfg) + fft_flop
+    achieved = tx_flop * n / (st_tx / 1e3) / 1e12
     bytes_sym = chain_bytes_per_symbol(cfg, fused=not args.unfused)
     hbm_achieved = bytes_sym * n * args.steps / (ms / 1e3) / 1e9
     if cfg.head == "paper":
@@ -354,36 +438,44 @@ def run_ours(args, cfg):
     elif fdpd.lib().fdcnn_workspace_bytes(fdpd._ints(cfg.chans), len(cfg.chans) - 1, n, cfg.U, cfg.N_d) == 0:
         cnn_launches = 1                                   # whole network in shared memory
     else:
-        cnn_launches = 2 * (len(cfg.chans) - 1)            # weight transpose + conv per layer
-    chain_launches = 2 if (cfg.U >= fdpd.SPLIT_PRECODE_MIN_U and not args.unfused) else 1   # (+ precode)
+        cnn_launches = 2 * (len(cfg.chans) - 1)            # weight split + conv per layer
+    chain_launches = 2 if split else 1                     # (+ precode)
     launches_per_step = cnn_launches + chain_launches + (2 if args.unfused else 1) + (3 if args.redraw else 0)
-    if not args.unfused:                       # chain_txrx also runs the receive FFT
-        tx_flop += 5 * cfg.N_ifft * int(np.log2(cfg.N_ifft)) * cfg.B * n
-        achieved = tx_flop / (st_tx / 1e3) / 1e12
+    # the tensor-core FD-CNN: 3 TF32 products per FP32-accurate MAC (hi/lo split), against the TF32
+    # peak = measured bf16 x the guide's nominal TF32/BF16 ratio (1.1 / 2.25)
+    tf32_peak = pk["bf16_tflops"] * 1.1 / 2.25
+    cnn_flop = cnn_flop_per_symbol(cfg) * n
     cpu = None
-    if not args.no_cpu_baseline and ws == 1 or (rank == 0 and not args.no_cpu_baseline):
-        k = args.ref_symbols
-        v, dt = oracle_symbols_per_s(cfg, list(range(k)))
-        cpu = {"value": v, "unit": "symbols/s", "cores": 1, "kind": "oracle",
-               "sample": f"{k} symbols of {cfg.name} (per-step stages, ZF untimed), fp64 numpy, 1 BLAS thread, "
-                         f"{dt:.1f} s"}
+    if not args.no_cpu_baseline and ws == 1:
+        cpu = oracle_sample(cfg, first_symbol=0)
     line = {
         "metric": METRIC, "value": value, "unit": "symbols/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, workload/gen.py)",
         "config": dict(config_dict(cfg, ws, n), impairments=bool(args.impair),
                        channel=("per-symbol redraw, ZF in the step" if args.redraw else
-                                "one realisation per run, ZF before timing")),
-        "roofline": {"kernel": ("chain_tx (precode+IDFT+GMP)" if args.unfused else
-                                "chain_txrx (precode+IDFT+GMP+receive DFT)"), "bound": "alu", "achieved": achieved,
+                                "one realisation per run, ZF before timing"),
+                       precode=("tensor cores, " + args.precode_math if split and args.precode_math != "simt"
+                                else ("FP32 SIMT kernel" if split else "fused into the chain kernel"))),
+        "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "traffic": measured_traffic(cfg, n, args),
-                     "peak_src": f"148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
-                     "flop_per_symbol": tx_flop / n, "ms_per_launch": st_tx},
+                     "peak_src": f"derived: 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
+                     "flop_per_symbol": tx_flop, "ms_per_launch": st_tx},
+        "roofline_cnn": ({"kernel": "fdcnn_forward (tcgen05 kind::tf32, hi/lo split)", "bound": "tensor",
+                          "algorithmic_tflops": cnn_flop / (st_dpd / 1e3) / 1e12,
+                          "issued_tf32_tflops": 3 * cnn_flop / (st_dpd / 1e3) / 1e12,
+                          "peak": tf32_peak, "unit": "TFLOP/s",
+                          "frac": 3 * cnn_flop / (st_dpd / 1e3) / 1e12 / tf32_peak,
+                          "peak_src": "measured bf16 x 1.1/2.25 (guide's nominal TF32/BF16 ratio)",
+                          "ms_per_step": st_dpd}
+                         if cnn_flop and cfg.chans[1] >= 32 else None),
         "hbm": {"algorithmic_bytes_per_symbol": bytes_sym, "achieved_GBps": hbm_achieved, "peak_GBps": pk["hbm_gbs"],
                 "frac": hbm_achieved / pk["hbm_gbs"], "peak_src": pk["src"]},
-        "stage_ms": {"fdcnn": st_dpd, ("chain_tx" if args.unfused else "chain_txrx"): st_tx,
+        "stage_ms": {"fdcnn": st_dpd, "precode": st_pre if split else 0.0,
+                     ("chain_tx" if args.unfused else ("chain_txrx_pre" if split else "chain_txrx")): st_tx,
                      ("ue_receive_ser" if args.unfused else "ue_combine_ser"): st_rx, "zf_build_once_s": t_zf},
+        "counters": {"errors": int(total_h[0]), "total": int(total_h[1]), "near_boundary": int(total_h[2])},
         "cpu_baseline": cpu,
         "e2e": ({"value": total_symbols / (ms_e2e_q / 1e3), "unit": "symbols/s",
                  "h2d_bytes_per_step": int(inp["idx"].nbytes), "d2h_bytes_per_step": 24,
@@ -406,18 +498,20 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--batch", type=int, default=0, help="symbols per GPU per step (default: the config's n_sym)")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--batch", type=int, default=0, help="symbols per GPU per step (default: the config's bench batch)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-symbols", type=int, default=64, help="oracle symbols per CPU sample (~10 s)")
-    ap.add_argument("--ref-step-symbols", type=int, default=4, help="oracle symbols per --impl reference step")
+    ap.add_argument("--ref-step-symbols", type=int, default=0,
+                    help="oracle symbols per --impl reference step (default 1 at C4/C5, else 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="chain_tx + ue_receive_ser instead of chain_txrx")
     ap.add_argument("--impair", action="store_true", help="PA clip + noise, AWGN, imperfect CSI (NEXT f3)")
     ap.add_argument("--redraw", action="store_true", help="per-symbol channel redraw, ZF on the hot path (NEXT f4)")
     ap.add_argument("--split-precode", action="store_true", help="precode kernel + chain_txrx_pre")
+    ap.add_argument("--precode-math", default="simt", choices=["simt", "tf32", "fp32tc"],
+                    help="split-path precode: FP32 SIMT, TF32 tensor cores, or FP32-accurate split-TF32 tensor cores")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

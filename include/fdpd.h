@@ -115,13 +115,32 @@ int zf_precoder_build(const void* h_taps, int T, int U, int B, int N_ifft, int N
 
 /* -------------------------------------------------------------------------
  * a3. Precode — Eq. (1):  X[n][b][j] = sum_u P[b][u][j] * s[n][u][j].
- *  P [B_loc][U][N_d], s [n_sym][U][N_d] -> X [n_sym][B_loc][N_d], complex64.  Summation over
- *  u in ascending order (FP32 complex FMA), identical to the fused chain prologue.  FD_ERR_ARG
- *  for bad sizes / NULL / misaligned pointers or U too large for the staged tile (8 U KB of
- *  shared memory; U <= 800).
+ *  P [B_loc][U][N_d], s [n_sym][U][N_d] -> X [n_sym][B_loc][N_d], complex64.
+ *
+ *  math (BASELINE configs[2] "TF32 tensor-core precoding variant"):
+ *   FD_MATH_FP32     FP32 SIMT complex FMAs, u summed in ascending order (identical to the
+ *                    fused chain prologue); U <= 800 (8 U KB of shared memory).
+ *   FD_MATH_TF32     tensor cores (tcgen05.mma kind::tf32): per subcarrier the real GEMM
+ *                    [Re P | Im P] (K = 2U) x [[Re s, Im s], [-Im s, Re s]]; operands rounded to
+ *                    TF32, FP32 accumulation: relative error ~1e-3 (parity bar 2e-3).
+ *   FD_MATH_FP32_TC  tensor cores with FP32-accurate split-TF32 operands (x = hi + lo, three
+ *                    products A_hi s_hi + A_hi s_lo + A_lo s_hi): parity bar 2e-5 like FP32.
+ *  Tensor-core modes need U % 4 == 0, U <= 32, P and X 16-byte aligned; they gather P with
+ *  8-byte loads — the fast form is precode_packed on a precode_pack'ed precoder.
+ *  FD_ERR_ARG for bad sizes / NULL / misaligned pointers / unknown math.
  * ------------------------------------------------------------------------- */
+enum { FD_MATH_FP32 = 0, FD_MATH_TF32 = 1, FD_MATH_FP32_TC = 2 };
 int precode(const void* P, const void* s, void* X,
-            long long n_sym, int B_loc, int U, int N_d, cudaStream_t stream);
+            long long n_sym, int B_loc, int U, int N_d, int math, cudaStream_t stream);
+/* The precoder in the tensor cores' per-subcarrier layout, written once per channel
+ * realisation (off the hot path, like zf_precoder_build): Ppk [N_d][B_loc][2U] float with
+ * row (j, b) = Re P[b][0..U)[j], Im P[b][0..U)[j] (the A operand rows of subcarrier j, read as
+ * contiguous 8U-byte rows).  Same bytes as P.  Ppk 16-byte aligned, precode_pack_bytes() bytes. */
+size_t precode_pack_bytes(int B_loc, int U, int N_d);
+int precode_pack(const void* P, void* Ppk, int B_loc, int U, int N_d, cudaStream_t stream);
+/* precode with a packed precoder; math = FD_MATH_TF32 or FD_MATH_FP32_TC (tensor cores). */
+int precode_packed(const void* Ppk, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d,
+                   int math, cudaStream_t stream);
 
 /* -------------------------------------------------------------------------
  * a4. OFDM IDFT — Eq. (2) P:54-57 (unitary, guards zero):

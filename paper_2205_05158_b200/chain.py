@@ -114,17 +114,28 @@ class Chain:
         sh = self.sh
         XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
         if self.split_precode:
-            # precode as its own bandwidth-bound kernel, then the fused chain on X
-            if getattr(self, "X", None) is None or self.X.shape[0] < n:
-                self.X = torch.empty((max(n, self.cap), self.B_loc, sh.N_d), dtype=torch.complex64,
-                                     device=self.device)
-            X = fdpd.precode(self.P, s_tilde, out=self.X[:n])
-            return fdpd.chain_txrx_pre(X, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft,
-                                       imp=self._imp(sym0) if self.impair else None, y=self.y[:n], XPA=XPA)
+            # precode as its own kernel, then the fused chain on X
+            return self.txrx_pre(self.precode(s_tilde), sym0)
         if self.impair:
             return fdpd.chain_txrx_ex(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, self._imp(sym0),
                                       y=self.y[:n], XPA=XPA)
         return fdpd.chain_txrx(self.P, s_tilde, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft, y=self.y[:n], XPA=XPA)
+
+    def precode(self, s_tilde):
+        """a3 on its own (the split path): X = precode(P, s_tilde) into the plan's buffer."""
+        n = s_tilde.shape[0]
+        if getattr(self, "X", None) is None or self.X.shape[0] < n:
+            self.X = torch.empty((max(n, self.cap), self.B_loc, self.sh.N_d), dtype=torch.complex64,
+                                 device=self.device)
+        return fdpd.precode(self.P, s_tilde, out=self.X[:n])
+
+    def txrx_pre(self, X, sym0=0):
+        """IDFT -> GMP (waveform stored) -> receive DFT on a precoded spectrum X (split path)."""
+        n = X.shape[0]
+        sh = self.sh
+        XPA = self.ws_rx[: 8 * n * self.B_loc * sh.N_d].view(torch.complex64).view(n, self.B_loc, sh.N_d)
+        return fdpd.chain_txrx_pre(X, self.coef, sh.orders, sh.L, sh.M, sh.N_ifft,
+                                   imp=self._imp(sym0) if self.impair else None, y=self.y[:n], XPA=XPA)
 
     def combine(self, XPA, tx_idx, counts=None, dec=None, sym0=0):
         n = XPA.shape[0]

@@ -202,6 +202,8 @@ int launch_chain_cluster(int log2n, int variant, const float2* P, const float2* 
     // and measured faster than the split (C3: 7.41 vs 8.10 ms per 512 symbols); N = 16384 splits
     // (C4: 13.83 -> 12.68 ms per 128 symbols, C5: 7.37 -> 6.77 ms per 32).
     if (g_chain_split == 1 || log2n != 14 || N_d % 4 != 0) return -1;
+    // two CTAs per (symbol, antenna): the grid must stay within gridDim.x (else the single-CTA kernel)
+    if (2 * n_sym * (long long)B > 0x7fffffffLL) return -1;
     const int NL = 1 << (log2n - 1);
     const int pz = prune_slots(NL, N_d / 2);
     if (log2n == 13) {

@@ -1,0 +1,436 @@
+// precode_tc.cu — ZF precoding (Eq. 1) as per-subcarrier complex GEMMs on the
+// 5th-generation tensor cores (tcgen05.mma kind::tf32, accumulators in TMEM).
+//
+//   X[n][b][j] = sum_u P[b][u][j] s[n][u][j]
+//
+// For one data subcarrier j this is X_j = P_j s_j, a (B x U) . (U x n) complex product.  As a
+// real GEMM with K = 2U:
+//   A_j[b][k]     = [ Re P[b][u] (k = u) | Im P[b][u] (k = U + u) ]                (M = 128 antennas)
+//   Bs_j[(n,0)][k] = [ Re s[n][u] | -Im s[n][u] ]   ->  D[b][(n,0)] = Re X[n][b][j]
+//   Bs_j[(n,1)][k] = [ Im s[n][u] |  Re s[n][u] ]   ->  D[b][(n,1)] = Im X[n][b][j]
+// (Bs rows are the GEMM's N dimension, both operands K-major in shared memory.)
+//
+// Precision (SURVEY §8(b) `math`):
+//  * FD_MATH_TF32 (HL = 1): one TF32 pass (operands rounded to TF32, FP32 accumulation),
+//    the north star's "TF32 tensor-core precoding" variant, parity 2e-3 (BASELINE configs[2]);
+//    64 symbols per tile (N = 128).
+//  * FD_MATH_FP32_TC (HL = 2): FP32-accurate split TF32.  x = hi + lo, hi = rna_tf32(x),
+//    lo = rna_tf32(x - hi); the symbol operand carries both halves as rows (Bs = [s_hi ; s_lo],
+//    N = 128 for 32 symbols) and every K step issues A_hi Bs (N = 128) and A_lo Bs_hi (N = 64):
+//    D_big = A_hi s_hi, D_small = A_hi s_lo + A_lo s_hi (A_lo s_lo ~ 2^-22 relative dropped),
+//    summed in FP32 in the epilogue.  Parity 2e-5 like the FP32 SIMT kernel.
+//
+// P operand: either the plain layout P [B][U][N_d] (8-byte gathers; the standalone `precode`)
+// or the per-subcarrier packed layout Ppk [N_d][B][2U] written once per channel realisation by
+// precode_pack (the rows of A_j, contiguous 256-byte rows at U = 32).
+//
+// CTA = (antenna tile of 128, symbol tile, contiguous range of subcarriers); one pipeline stage
+// per subcarrier.  Warp roles (mbarrier rings, no CTA barrier in the loop):
+//   warps 0-15  epilogue: TMEM lane quadrant (w % 4) = 32 antennas x column group (w / 4) = a
+//               quarter of the symbols; sums big + small, buffers JB subcarriers in registers
+//               and writes X[n][b][j..j+JB) as 16-byte runs
+//   warps 16-23 producers: load P / s for the stage (loads issued before waiting for the
+//               buffer), split, store the K-major operands, fence.proxy.async, arrive
+//   warp 24     MMA issue (one elected lane), commits to the stage's empty barrier and the TMEM
+//               slot's full barrier
+// Stages: NS shared-memory buffers; TMEM: 4 slots of 128 columns (512).
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace fdpd {
+
+constexpr int PT_EPI = 16, PT_PROD = 8;
+constexpr int PT_MMA_WARP = PT_EPI + PT_PROD;
+constexpr int PT_THREADS = 32 * (PT_MMA_WARP + 1);
+constexpr int PT_ROWS = 128;                 // rows of every operand plane (M = 128, N = 128)
+constexpr int PT_PLANE = (PT_ROWS + 1) * 16; // bytes per 16-byte K chunk (4 tf32) plane, +1 row: conflict-free stores
+constexpr int PT_SLOTS = 4, PT_COLS = 128;   // TMEM accumulator ring
+
+struct PtGeom {
+    int U, B, N_d;
+    long long n_sym;
+    int planes;                // 2U / 4 K planes per operand
+    int ns;                    // shared-memory stages
+    int stage_bytes;           // A (HL planes sets) + Bs
+    int n_btiles, n_ntiles, jper, n_jgroups;
+};
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void split4(float4 x, float4& hi, float4& lo) {
+    hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
+    hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
+    hi.z = tf32_rna(x.z); lo.z = tf32_rna(x.z - hi.z);
+    hi.w = tf32_rna(x.w); lo.w = tf32_rna(x.w - hi.w);
+}
+__device__ __forceinline__ float4 rna4(float4 x) {
+    return make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+}
+
+// HL = 1 (TF32) or 2 (split TF32); PACKED: P is Ppk [N_d][B][2U] (else P [B][U][N_d]).
+template <int HL, bool PACKED>
+__global__ void __launch_bounds__(PT_THREADS, 1)
+    k_precode_tc(const float* __restrict__ P, const float2* __restrict__ s, float2* __restrict__ X, PtGeom g) {
+    constexpr int NT = 64 / HL;              // symbols per tile (Bs rows = HL * 2 NT = 128)
+    constexpr int NPW = NT / 4;              // symbols per epilogue warp column group
+    constexpr int JB = HL;                   // subcarriers buffered per epilogue store (register budget)
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int plane_set = g.planes * PT_PLANE;             // bytes of one operand (all K planes)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)g.ns * g.stage_bytes);
+    uint64_t* full = bars;                   // [ns]
+    uint64_t* empty = bars + g.ns;           // [ns]
+    uint64_t* tfull = empty + g.ns;          // [4]
+    uint64_t* tempty = tfull + PT_SLOTS;     // [4]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + PT_SLOTS);
+
+    if (tid == 0) {
+        for (int i = 0; i < g.ns; ++i) {
+            mbar_init(&full[i], 32 * PT_PROD);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < PT_SLOTS; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 32 * PT_EPI);
+        }
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, PT_SLOTS * PT_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // work of this CTA: (antenna tile, symbol tile) fixed, subcarriers [ja, jb)
+    int w = blockIdx.x;
+    const int jg = w % g.n_jgroups;
+    w /= g.n_jgroups;
+    const int bt = w % g.n_btiles, nt = w / g.n_btiles;
+    const int b0 = bt * PT_ROWS;
+    const long long n0 = (long long)nt * NT;
+    const int ja = jg * g.jper, jb = min(g.N_d, ja + g.jper);
+    const int n_stages = max(0, jb - ja);
+    const int U = g.U, B = g.B, N_d = g.N_d;
+
+    if (warp >= PT_EPI && warp < PT_MMA_WARP) {
+        // ---------------------------------------------------------------- producers
+        const int pt = tid - 32 * PT_EPI;
+        const int KQ = g.planes;             // 16-byte k-quads per row (= U / 2)
+        const int UQ = U >> 2;               // u-quads
+        int buf = 0;
+        uint32_t ph = 0;
+        for (int i = 0; i < n_stages; ++i) {
+            const int j = ja + i;
+            // A rows: packed -> item (row, k-quad) one float4; plain -> item (row, u-quad), 4 float2
+            constexpr int MAXA = PACKED ? 8 : 4;   // items per thread at U <= 32 (128 rows x U/2 or U/4 quads)
+            float4 av[MAXA];
+            const int na = PACKED ? PT_ROWS * KQ : PT_ROWS * UQ;
+            float2 pv[PACKED ? 1 : MAXA][4];
+#pragma unroll
+            for (int t = 0; t < MAXA; ++t) {
+                const int it = pt + t * 32 * PT_PROD;
+                if (it >= na) break;
+                if constexpr (PACKED) {
+                    const int kq = it % KQ, r = it / KQ;
+                    av[t] = (b0 + r < B) ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)j * B + b0 + r) * 2 * U) + kq)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+                    const int uq = it % UQ, r = it / UQ;
+                    const float2* src = reinterpret_cast<const float2*>(P) + ((size_t)(b0 + r) * U + 4 * uq) * N_d + j;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        pv[t][q] = (b0 + r < B) ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
+                }
+            }
+            // symbol rows: item (n, u-quad), 4 float2 (NT x U/4 <= 512 items: <= 2 per thread)
+            constexpr int MAXS = 2;
+            float2 sv[MAXS][4];
+            const int ns_items = NT * UQ;
+#pragma unroll
+            for (int t = 0; t < MAXS; ++t) {
+                const int it = pt + t * 32 * PT_PROD;
+                const int su = it % UQ, sn = it / UQ;
+                const bool ok = it < ns_items && n0 + sn < g.n_sym;
+                const float2* src = s + ((size_t)(n0 + sn) * U + 4 * su) * N_d + j;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sv[t][q] = ok ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
+            }
+            if (i >= g.ns) mbar_wait(&empty[buf], ph ^ 1u);
+            unsigned char* st = sm + (size_t)buf * g.stage_bytes;
+            unsigned char* a_hi = st;
+            unsigned char* a_lo = st + plane_set;
+            unsigned char* bs = st + (HL == 2 ? 2 : 1) * plane_set;
+#pragma unroll
+            for (int t = 0; t < MAXA; ++t) {
+                const int it = pt + t * 32 * PT_PROD;
+                if (it >= na) break;
+                if constexpr (PACKED) {
+                    const int kq = it % KQ, r = it / KQ;
+                    const size_t off = (size_t)kq * PT_PLANE + r * 16;
+                    if constexpr (HL == 2) {
+                        float4 hi, lo;
+                        split4(av[t], hi, lo);
+                        *reinterpret_cast<float4*>(a_hi + off) = hi;
+                        *reinterpret_cast<float4*>(a_lo + off) = lo;
+                    } else {
+                        *reinterpret_cast<float4*>(a_hi + off) = rna4(av[t]);
+                    }
+                } else {
+                    const int uq = it % UQ, r = it / UQ;
+                    const float4 re = make_float4(pv[t][0].x, pv[t][1].x, pv[t][2].x, pv[t][3].x);
+                    const float4 im = make_float4(pv[t][0].y, pv[t][1].y, pv[t][2].y, pv[t][3].y);
+                    const size_t ore = (size_t)uq * PT_PLANE + r * 16, oim = (size_t)(UQ + uq) * PT_PLANE + r * 16;
+                    if constexpr (HL == 2) {
+                        float4 hi, lo;
+                        split4(re, hi, lo);
+                        *reinterpret_cast<float4*>(a_hi + ore) = hi;
+                        *reinterpret_cast<float4*>(a_lo + ore) = lo;
+                        split4(im, hi, lo);
+                        *reinterpret_cast<float4*>(a_hi + oim) = hi;
+                        *reinterpret_cast<float4*>(a_lo + oim) = lo;
+                    } else {
+                        *reinterpret_cast<float4*>(a_hi + ore) = rna4(re);
+                        *reinterpret_cast<float4*>(a_hi + oim) = rna4(im);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < MAXS; ++t) {
+                const int it = pt + t * 32 * PT_PROD;
+                if (it >= ns_items) break;
+                const int su = it % UQ, sn = it / UQ;
+                const float4 re = make_float4(sv[t][0].x, sv[t][1].x, sv[t][2].x, sv[t][3].x);
+                const float4 im = make_float4(sv[t][0].y, sv[t][1].y, sv[t][2].y, sv[t][3].y);
+                // row (n, 0): [Re s | -Im s];  row (n, 1): [Im s | Re s]
+                const int r0 = 2 * sn, r1 = 2 * sn + 1;
+                const size_t p1 = (size_t)su * PT_PLANE, p2 = (size_t)(UQ + su) * PT_PLANE;
+                if constexpr (HL == 2) {
+                    float4 hi, lo;
+                    split4(re, hi, lo);
+                    *reinterpret_cast<float4*>(bs + p1 + r0 * 16) = hi;
+                    *reinterpret_cast<float4*>(bs + p1 + (64 + r0) * 16) = lo;
+                    *reinterpret_cast<float4*>(bs + p2 + r1 * 16) = hi;
+                    *reinterpret_cast<float4*>(bs + p2 + (64 + r1) * 16) = lo;
+                    split4(im, hi, lo);
+                    *reinterpret_cast<float4*>(bs + p1 + r1 * 16) = hi;
+                    *reinterpret_cast<float4*>(bs + p1 + (64 + r1) * 16) = lo;
+                    *reinterpret_cast<float4*>(bs + p2 + r0 * 16) = make_float4(-hi.x, -hi.y, -hi.z, -hi.w);
+                    *reinterpret_cast<float4*>(bs + p2 + (64 + r0) * 16) = make_float4(-lo.x, -lo.y, -lo.z, -lo.w);
+                } else {
+                    const float4 hre = rna4(re), him = rna4(im);
+                    *reinterpret_cast<float4*>(bs + p1 + r0 * 16) = hre;
+                    *reinterpret_cast<float4*>(bs + p2 + r0 * 16) = make_float4(-him.x, -him.y, -him.z, -him.w);
+                    *reinterpret_cast<float4*>(bs + p1 + r1 * 16) = him;
+                    *reinterpret_cast<float4*>(bs + p2 + r1 * 16) = hre;
+                }
+            }
+            fence_proxy_async();
+            mbar_arrive(&full[buf]);
+            if (++buf == g.ns) { buf = 0; ph ^= 1u; }
+        }
+    } else if (warp == PT_MMA_WARP) {
+        // ---------------------------------------------------------------- MMA issue
+        const uint32_t base = smem_u32(sm);
+        constexpr uint32_t ID_FULL = idesc_tf32_m128(128);
+        constexpr uint32_t ID_HALF = idesc_tf32_m128(64);
+        const int ksteps = g.planes / 2;     // K = 8 per MMA = two 16-byte planes
+        int buf = 0;
+        uint32_t ph = 0;
+        for (int i = 0; i < n_stages; ++i) {
+            const int slot = i & (PT_SLOTS - 1);
+            if (i >= PT_SLOTS) mbar_wait(&tempty[slot], (uint32_t)(((i / PT_SLOTS) - 1) & 1));
+            mbar_wait(&full[buf], ph);
+            tc_fence_after();
+            const uint32_t sb = base + (uint32_t)buf * g.stage_bytes;
+            const uint64_t dhi = umma_desc(sb, PT_PLANE, 128);
+            const uint64_t dlo = umma_desc(sb + plane_set, PT_PLANE, 128);
+            const uint64_t dbs = umma_desc(sb + (HL == 2 ? 2 : 1) * plane_set, PT_PLANE, 128);
+            const uint32_t d = tmem + (uint32_t)slot * PT_COLS;
+            if (elect_one()) {
+                for (int k = 0; k < ksteps; ++k) {
+                    const uint64_t kadv = (uint64_t)((2u * k * PT_PLANE) >> 4);
+                    mma_tf32(d, dhi + kadv, dbs + kadv, ID_FULL, k > 0 ? 1u : 0u);
+                    if constexpr (HL == 2) mma_tf32(d + 64, dlo + kadv, dbs + kadv, ID_HALF, 1u);
+                }
+                umma_commit(&empty[buf]);
+                umma_commit(&tfull[slot]);
+            }
+            __syncwarp();
+            if (++buf == g.ns) { buf = 0; ph ^= 1u; }
+        }
+    } else if (warp < PT_EPI) {
+        // ---------------------------------------------------------------- epilogue
+        const int quad = warp & 3, grp = warp >> 2;
+        const int b = b0 + quad * 32 + lane;
+        const int nb = grp * NPW;            // first symbol (within the tile) of this warp
+        float2 acc[JB][NPW];
+        int jfirst = ja;
+        for (int i = 0; i < n_stages; ++i) {
+            const int slot = i & (PT_SLOTS - 1);
+            mbar_wait(&tfull[slot], (uint32_t)((i / PT_SLOTS) & 1));
+            tc_fence_after();
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)slot * PT_COLS;
+            const int jj = i % JB;
+            // columns 2n + c (c = Re / Im); HL = 2: big at 0..63, small at 64..127
+#pragma unroll
+            for (int h = 0; h < NPW / 4; ++h) {     // 8 columns = 4 symbols per TMEM load
+                float v[8];
+                tmem_ld8(ta + 2 * (nb + 4 * h), v);
+                if constexpr (HL == 2) {
+                    float w2[8];
+                    tmem_ld8(ta + 64 + 2 * (nb + 4 * h), w2);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] += w2[q];
+                }
+#pragma unroll
+                for (int t = 0; t < JB; ++t)        // compile-time register index
+                    if (t == jj)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[t][4 * h + q] = make_float2(v[2 * q], v[2 * q + 1]);
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[slot]);
+            const int j = ja + i;
+            if (jj == JB - 1 || i == n_stages - 1) {
+                const int cnt = jj + 1;
+                if (b < B) {
+                    const bool vec = cnt == 2 && ((((size_t)b * N_d + jfirst) & 1) == 0) && ((N_d & 1) == 0);
+#pragma unroll
+                    for (int q = 0; q < NPW; ++q) {
+                        const long long n = n0 + nb + q;
+                        if (n >= g.n_sym) break;
+                        float2* dst = X + ((size_t)n * B + b) * N_d + jfirst;
+                        if (vec) {
+                            *reinterpret_cast<float4*>(dst) = make_float4(acc[0][q].x, acc[0][q].y, acc[1][q].x,
+                                                                          acc[1][q].y);
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < JB; ++t)
+                                if (t < cnt) dst[t] = acc[t][q];
+                        }
+                    }
+                }
+                jfirst = j + 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, PT_SLOTS * PT_COLS);
+    }
+}
+
+// P [B][U][N_d] -> Ppk [N_d][B][2U]: row (j, b) = Re P[b][0..U)[j], Im P[b][0..U)[j] (fp32).
+// CTA = (antenna b, 32 subcarriers): coalesced 256-byte reads of P rows, transposed in shared memory.
+__global__ void __launch_bounds__(256) k_precode_pack(const float2* __restrict__ P, float* __restrict__ Ppk, int B,
+                                                       int U, int N_d) {
+    extern __shared__ __align__(16) float2 tile[];          // [U][33]
+    const int b = blockIdx.y, j0 = blockIdx.x * 32;
+    for (int e = threadIdx.x; e < U * 32; e += blockDim.x) {
+        const int u = e >> 5, l = e & 31;
+        tile[u * 33 + l] = j0 + l < N_d ? P[((size_t)b * U + u) * N_d + j0 + l] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 2 * U; e += blockDim.x) {
+        const int k = e % (2 * U), l = e / (2 * U);
+        if (j0 + l >= N_d) continue;
+        const float2 v = tile[(k % U) * 33 + l];
+        Ppk[((size_t)(j0 + l) * B + b) * 2 * U + k] = k < U ? v.x : v.y;
+    }
+}
+
+int precode_simt(const void* P, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d,
+                 cudaStream_t stream);
+
+static int launch_precode_tc(const void* P, bool packed, const void* s, void* X, long long n_sym, int B, int U,
+                             int N_d, int math, cudaStream_t st) {
+    FD_REQUIRE(U % 4 == 0 && U <= 32, "precode (tensor cores): U=%d must be a multiple of 4 and <= 32", U);
+    FD_REQUIRE(aligned16(P) && aligned8(s) && aligned16(X), "precode (tensor cores): P / X 16-byte, s 8-byte aligned");
+    const int HL = math == FD_MATH_TF32 ? 1 : 2;
+    const int NT = 64 / HL;
+    PtGeom g{};
+    g.U = U;
+    g.B = B;
+    g.N_d = N_d;
+    g.n_sym = n_sym;
+    g.planes = U / 2;
+    g.stage_bytes = (HL + 1) * g.planes * PT_PLANE;
+    const size_t bar_bytes = 8 * (2 * 8 + 2 * PT_SLOTS) + 16;
+    const size_t limit = 227 * 1024;
+    g.ns = (int)std::min<size_t>(8, (limit - bar_bytes) / (size_t)g.stage_bytes);
+    FD_REQUIRE(g.ns >= 2, "precode (tensor cores): U=%d too large", U);
+    g.n_btiles = (B + PT_ROWS - 1) / PT_ROWS;
+    const long long ntiles = (n_sym + NT - 1) / NT;
+    FD_REQUIRE(ntiles * g.n_btiles < 65536, "precode (tensor cores): batch too large");
+    g.n_ntiles = (int)ntiles;
+    // one wave of persistent CTAs (one per SM: ~200 KB of stages, 512 TMEM columns); subcarrier ranges in multiples of the epilogue's 2-subcarrier runs
+    const int pairs = (N_d + 1) / 2;
+    int jg = std::max(1, (int)std::min<long long>(pairs, (148LL + g.n_btiles * ntiles - 1) / (g.n_btiles * ntiles)));
+    g.jper = 2 * ((pairs + jg - 1) / jg);
+    g.n_jgroups = (N_d + g.jper - 1) / g.jper;
+    const size_t smem = (size_t)g.ns * g.stage_bytes + bar_bytes;
+    const unsigned grid = (unsigned)(g.n_jgroups * g.n_btiles * ntiles);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, PT_THREADS, smem, st>>>((const float*)P, (const float2*)s, (float2*)X, g);
+    };
+    if (HL == 1) packed ? go(k_precode_tc<1, true>) : go(k_precode_tc<1, false>);
+    else packed ? go(k_precode_tc<2, true>) : go(k_precode_tc<2, false>);
+    return check_launch("precode (tensor cores)");
+}
+
+}  // namespace fdpd
+
+using namespace fdpd;
+
+extern "C" {
+
+int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d, int math,
+            cudaStream_t stream) {
+    FD_REQUIRE(math == FD_MATH_FP32 || math == FD_MATH_TF32 || math == FD_MATH_FP32_TC, "precode: math=%d", math);
+    if (math == FD_MATH_FP32) return precode_simt(P, s, X, n_sym, B_loc, U, N_d, stream);
+    FD_REQUIRE(n_sym >= 0 && B_loc >= 1 && U >= 1 && N_d >= 1, "precode: bad sizes");
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(P && s && X, "precode: NULL pointer");
+    return launch_precode_tc(P, false, s, X, n_sym, B_loc, U, N_d, math, stream);
+}
+
+size_t precode_pack_bytes(int B_loc, int U, int N_d) {
+    if (B_loc < 1 || U < 1 || N_d < 1) return 0;
+    return (size_t)N_d * B_loc * 2 * U * sizeof(float);
+}
+
+int precode_pack(const void* P, void* Ppk, int B_loc, int U, int N_d, cudaStream_t stream) {
+    FD_REQUIRE(B_loc >= 1 && U >= 1 && N_d >= 1 && B_loc <= 65535, "precode_pack: bad sizes");
+    FD_REQUIRE(P && Ppk, "precode_pack: NULL pointer");
+    FD_REQUIRE(aligned8(P) && aligned16(Ppk), "precode_pack: P 8-byte, Ppk 16-byte aligned");
+    const size_t smem = sizeof(float2) * U * 33;
+    FD_REQUIRE(smem <= 200 * 1024, "precode_pack: U=%d too large", U);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_precode_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((N_d + 31) / 32, B_loc);
+    k_precode_pack<<<grid, 256, smem, stream>>>((const float2*)P, (float*)Ppk, B_loc, U, N_d);
+    return check_launch("precode_pack");
+}
+
+int precode_packed(const void* Ppk, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d, int math,
+                   cudaStream_t stream) {
+    FD_REQUIRE(math == FD_MATH_TF32 || math == FD_MATH_FP32_TC, "precode_packed: math=%d (1 = TF32, 2 = FP32 TC)",
+               math);
+    FD_REQUIRE(n_sym >= 0 && B_loc >= 1 && U >= 1 && N_d >= 1, "precode_packed: bad sizes");
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(Ppk && s && X, "precode_packed: NULL pointer");
+    return launch_precode_tc(Ppk, true, s, X, n_sym, B_loc, U, N_d, math, stream);
+}
+
+}  // extern "C"

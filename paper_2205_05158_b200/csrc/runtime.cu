@@ -118,7 +118,7 @@ int run_chunk(fd_chain* c, const void* s, const uint16_t* tx_idx, long long s0, 
     if (c->X) {
         // many users: tiled precode kernel, then the chain on the precoded spectrum
         float2* X = c->X + s0 * pb;
-        rc = precode(c->P, st, X, n, d.B, d.U, d.N_d, stream);
+        rc = precode(c->P, st, X, n, d.B, d.U, d.N_d, FD_MATH_FP32, stream);
         if (rc) return rc;
         rc = chain_txrx_pre(X, c->coef, c->y + s0 * py, XPA, d.orders, d.n_orders, d.L, d.M, n, d.B, d.N_d, d.N_ifft,
                             nullptr, stream);
@@ -144,6 +144,8 @@ int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_tap
     FD_REQUIRE(d.n_layers >= 1 && d.n_layers <= FD_CHAIN_MAX_LAYERS, "fd_chain_create: n_layers");
     FD_REQUIRE(d.n_orders >= 1 && d.n_orders <= 8, "fd_chain_create: n_orders");
     FD_REQUIRE(max_batch >= 0, "fd_chain_create: max_batch < 0");
+    // ue_combine_ser takes at most 65535 symbols per call and a step runs the whole batch
+    FD_REQUIRE(max_batch <= 65535, "fd_chain_create: max_batch=%lld exceeds 65535 symbols per step", max_batch);
     fd_chain* c = new (std::nothrow) fd_chain();
     if (!c) return fdpd::fail_arg("fd_chain_create: out of host memory");
     c->d = d;

@@ -320,7 +320,15 @@ using namespace fdpd;
 
 extern "C" {
 
-int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d, cudaStream_t stream) {
+}  // extern "C"
+
+// FD_MATH_FP32 path of precode (precode_tc.cu dispatches on `math`)
+namespace fdpd {
+int precode_simt(const void* P, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d,
+                 cudaStream_t stream);
+}
+int fdpd::precode_simt(const void* P, const void* s, void* X, long long n_sym, int B_loc, int U, int N_d,
+                       cudaStream_t stream) {
     FD_REQUIRE(n_sym >= 0 && B_loc >= 1 && U >= 1 && N_d >= 1, "precode: bad sizes");
     const long long total = n_sym * B_loc * (long long)N_d;
     if (total == 0) return FD_OK;
@@ -342,6 +350,8 @@ int precode(const void* P, const void* s, void* X, long long n_sym, int B_loc, i
                                                                         (float2*)X, n_sym, B_loc, U, N_d, bpc);
     return check_launch("precode");
 }
+
+extern "C" {
 
 int ofdm_modulate(const void* X, void* x, long long n_sym, int B, int N_d, int N_ifft, cudaStream_t stream) {
     int rc = validate_ofdm(n_sym, B, N_d, N_ifft);

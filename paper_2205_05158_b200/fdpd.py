@@ -55,7 +55,10 @@ SIGNATURES = {
     "fdcnn_paper_forward": (_i, [_vp, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
     "zf_workspace_bytes": (_sz, [_i]),
     "zf_precoder_build": (_i, [_vp, _i, _i, _i, _i, _i, _f, _i, _i, _vp, _vp, C.POINTER(C.c_float), _vp, _sz, _vp]),
-    "precode": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _vp]),
+    "precode": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _i, _vp]),
+    "precode_pack_bytes": (_sz, [_i, _i, _i]),
+    "precode_pack": (_i, [_vp, _vp, _i, _i, _i, _vp]),
+    "precode_packed": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _i, _vp]),
     "ofdm_modulate": (_i, [_vp, _vp, _ll, _i, _i, _i, _vp]),
     "gmp_pa": (_i, [_vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _vp]),
     "chain_tx": (_i, [_vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _vp]),
@@ -303,13 +306,37 @@ def make_impairments(clip=0.0, pa_noise_std=0.0, awgn_n0=0.0, csi_eta=0.0, noise
 
 
 # ----------------------------------------------------------------------------- a3-a5
-def precode(P, s, out=None):
+MATH_FP32, MATH_TF32, MATH_FP32_TC = 0, 1, 2
+MATH = {"simt": MATH_FP32, "fp32": MATH_FP32, "tf32": MATH_TF32, "fp32tc": MATH_FP32_TC}
+
+
+def precode(P, s, out=None, math=MATH_FP32):
+    """P [B][U][N_d], s [n][U][N_d] -> X [n][B][N_d]; math 0 FP32 SIMT, 1 TF32 / 2 split-TF32 tensor cores."""
     _dev(P, torch.complex64, "P")
     _dev(s, torch.complex64, "s")
     B, U, N_d = P.shape
     n_sym = s.shape[0]
     out = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=s.device) if out is None else out
-    _check(lib().precode(_ptr(P), _ptr(s), _ptr(out), n_sym, B, U, N_d, _stream(s)))
+    _check(lib().precode(_ptr(P), _ptr(s), _ptr(out), n_sym, B, U, N_d, int(math), _stream(s)))
+    return out
+
+
+def precode_pack(P, out=None):
+    """P [B][U][N_d] complex64 -> Ppk [N_d][B][2U] float32 (per-subcarrier tensor-core layout)."""
+    _dev(P, torch.complex64, "P")
+    B, U, N_d = P.shape
+    out = torch.empty((N_d, B, 2 * U), dtype=torch.float32, device=P.device) if out is None else out
+    _check(lib().precode_pack(_ptr(P), _ptr(out), B, U, N_d, _stream(P)))
+    return out
+
+
+def precode_packed(Ppk, s, out=None, math=MATH_FP32_TC):
+    _dev(Ppk, torch.float32, "Ppk")
+    _dev(s, torch.complex64, "s")
+    N_d, B, U2 = Ppk.shape
+    n_sym = s.shape[0]
+    out = torch.empty((n_sym, B, N_d), dtype=torch.complex64, device=s.device) if out is None else out
+    _check(lib().precode_packed(_ptr(Ppk), _ptr(s), _ptr(out), n_sym, B, U2 // 2, N_d, int(math), _stream(s)))
     return out
 
 

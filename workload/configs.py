@@ -42,6 +42,7 @@ class ChainConfig:
     pa_noise_std: float = 0.0   # PA measurement noise std per complex sample, CN(0, std^2)
     awgn_n0: float = 0.0        # AWGN variance N_0 at the UEs, per data subcarrier (unitary DFT)
     csi_eta: float = 0.0        # imperfect-CSI weight eta
+    bench_batch: int = 0        # OFDM symbols per GPU per bench step (0: n_sym); SURVEY §8(d) streaming
 
     @property
     def N_ifft(self) -> int:
@@ -86,13 +87,13 @@ C2 = ChainConfig("C2", U=4, B=64, N_fft=1024, N_d=600, os=4, M_qam=64, n_sym=102
                  spread=0.05, seed=1)
 C3 = ChainConfig("C3", U=8, B=128, N_fft=2048, N_d=1200, os=4, M_qam=64, n_sym=2048, T=16,
                  pdp="exp3dB", orders=(1, 3, 5, 7), L=4, M=2, chans=(2, 32, 32, 32, 2),
-                 spread=0.05, seed=2)
+                 spread=0.05, seed=2, bench_batch=512)
 C4 = ChainConfig("C4", U=16, B=256, N_fft=4096, N_d=3300, os=4, M_qam=256, n_sym=2048, T=16,
                  pdp="exp3dB", orders=(1, 3, 5, 7, 9), L=6, M=3, chans=(2, 32, 32, 32, 2),
-                 spread=0.05, seed=3)
+                 spread=0.05, seed=3, bench_batch=128)
 C5 = ChainConfig("C5", U=32, B=512, N_fft=4096, N_d=3300, os=4, M_qam=256, n_sym=4096, T=16,
                  pdp="exp3dB", orders=(1, 3, 5, 7, 9), L=6, M=3,
-                 chans=(2, 64, 64, 64, 64, 2), spread=0.10, seed=4)
+                 chans=(2, 64, 64, 64, 64, 2), spread=0.10, seed=4, bench_batch=32)
 
 # The paper's own workload with the paper's FD-CNN head (NEXT f2):
 # N = 4096 IDFT, N_d = 384, U = 8, B = 32, 256-QAM, T = 10 uniform-PDP taps, FD-CNN
