@@ -274,7 +274,7 @@ def run_ours(args, cfg):
                       noise_key=inp["noise_key"], h_err=inp["h_err"])
     t_zf0 = time.perf_counter()
     ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device=dev, max_batch=n,
-               impair=impair)
+               impair=impair, precode_math=args.precode_math)
     torch.cuda.synchronize()
     t_zf = time.perf_counter() - t_zf0
     if args.split_precode:
@@ -495,6 +495,142 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_antenna(args, cfg):
+    """Mode A (BASELINE configs[4]): antenna rows [b0, b0 + B/N) per rank, FD-CNN on
+    the rank's n symbols, all_gather_into_tensor of s_tilde, precode -> IDFT/GMP/receive DFT on the
+    local antennas for the world batch of N n symbols, partial channel sum, reduce_scatter_tensor
+    (each rank gets y_hat of its own symbols), slicing, counter all-reduce; two micro-batches so the
+    collectives overlap the next micro-batch's compute.  Weak scaling: per GPU, n symbols of CNN and
+    N n symbols x B/N antennas of chain = the 1-GPU step's work."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_05158_b200 import fdpd
+    from paper_2205_05158_b200 import dist as D
+    from paper_2205_05158_b200.chain import AntennaOps, Chain, Shapes
+
+    ws, rank, local = init_dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    fdpd.lib()
+    n = batch_of(cfg, args)
+    micro = 2 if n % 2 == 0 else 1
+    symbols = D.symbol_range(n, rank)
+    inp = gen.make_inputs(cfg, symbols)
+    b0, B_loc = D.antenna_shard(cfg.B, ws, rank)
+    math = args.precode_math if args.precode_math != "simt" else "simt"
+    t0 = time.perf_counter()
+    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device=dev,
+               max_batch=ws * n // micro, b0=b0, B_loc=B_loc, precode_math=math)
+    torch.cuda.synchronize()
+    t_zf = time.perf_counter() - t0
+    chain_ev = []
+    ops = AntennaOps(ch, events=chain_ev)
+    step = D.AntennaShardedStep(ops, n, cfg.U, cfg.N_d, micro=micro,
+                                alloc=lambda shp: torch.empty(shp, dtype=torch.complex64, device=dev))
+    s = torch.from_numpy(inp["s"]).to(dev)
+    idx = torch.from_numpy(inp["idx"]).to(dev)
+    counts = torch.zeros(3, dtype=torch.int64, device=dev)
+    total = torch.zeros(3, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        counts.zero_()
+        step.step(s, idx, counts)
+        flush.zero_()
+    torch.cuda.synchronize()
+    chain_ev.clear()
+    if ws > 1:
+        dist.barrier()
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    evs = [(E(), E()) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            counts.zero_()
+            step.step(s, idx, counts)
+            total.add_(counts)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        n_chain = len(chain_ev)
+        ms_chain = sum(a.elapsed_time(b) for a, b in chain_ev) / max(1, n_chain)
+        chain_ev.clear()
+        ops.events = None
+        if ws > 1:
+            dist.barrier()
+        total_h = total.cpu()
+        if int(total_h[1]) != args.steps * ws * n * cfg.U * cfg.N_d:
+            raise RuntimeError(f"step counters wrong: {total_h.tolist()}")
+        # end to end: this rank's QAM symbols and indices from pinned host memory, the step, the
+        # world SER counters back to the host, every step
+        s_h = torch.from_numpy(inp["s"]).pin_memory()
+        i_h = torch.from_numpy(inp["idx"]).pin_memory()
+        c_h = torch.zeros(3, dtype=torch.int64).pin_memory()
+        s_d, i_d = torch.empty_like(s), torch.empty_like(idx)
+        e2e = [(E(), E()) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.zero_()
+            e2e[i][0].record(stream)
+            s_d.copy_(s_h, non_blocking=True)
+            i_d.copy_(i_h, non_blocking=True)
+            counts.zero_()
+            step.step(s_d, i_d, counts)
+            c_h.copy_(counts, non_blocking=True)
+            e2e[i][1].record(stream)
+        torch.cuda.synchronize()
+        if int(c_h[1]) != ws * n * cfg.U * cfg.N_d:
+            raise RuntimeError(f"e2e counters wrong: {c_h.tolist()}")
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    ms_e2e = sum(a.elapsed_time(b) for a, b in e2e)
+    t = torch.tensor([ms, ms_e2e, ms_chain], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ms_e2e, ms_chain = t.tolist()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    total_symbols = n * ws * args.steps
+    pk = peaks()
+    fp32_peak = 148 * FP32_LANES_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+    N = cfg.N_ifft
+    flop_sym_ant = 2 * 5 * N * int(np.log2(N)) + gmp_flop_per_sample(cfg) * N     # IDFT + GMP + receive DFT
+    achieved = flop_sym_ant * (ws * n // micro) * B_loc / (ms_chain / 1e3) / 1e12
+    comm = 8 * ws * n * cfg.U * cfg.N_d
+    line = {
+        "metric": METRIC, "value": total_symbols / (ms / 1e3), "unit": "symbols/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, workload/gen.py)",
+        "config": dict(config_dict(cfg, ws, n), parallelism=f"antenna x{ws} (Mode A: {B_loc} antennas per GPU)",
+                       precode=("tensor cores, " + math) if math != "simt" else "FP32 SIMT kernel",
+                       micro_batches=micro, world_batch_symbols=ws * n,
+                       collectives="all_gather_into_tensor(s_tilde) + reduce_scatter_tensor(y_hat partials) per "
+                                   "micro-batch (NCCL, async, overlapped) + int64 counter all_reduce",
+                       comm_bytes_per_rank_per_step={"all_gather_in": comm * (ws - 1) // ws,
+                                                     "reduce_scatter_out": comm * (ws - 1) // ws}),
+        "roofline": {"kernel": "chain_txrx_pre (IDFT+GMP+receive DFT)", "bound": "alu", "achieved": achieved,
+                     "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                     "peak_src": f"derived: 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
+                     "ms_per_launch": ms_chain},
+        "counters": {"errors": int(total_h[0]), "total": int(total_h[1]), "near_boundary": int(total_h[2])},
+        "stage_ms": {"zf_build_once_s": t_zf},
+        "cpu_baseline": None,
+        "e2e": {"value": total_symbols / (ms_e2e / 1e3), "unit": "symbols/s",
+                "h2d_bytes_per_step": int(inp["s"].nbytes + inp["idx"].nbytes), "d2h_bytes_per_step": 24,
+                "api": "Mode A step (per-call path) with host copies of each rank's symbols and indices"},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+    }
+    cnn_l = 2 * (len(cfg.chans) - 1)
+    line["gpu_launches"] = args.steps * micro * (cnn_l + (2 if math != "simt" else 2) + 2)
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -512,6 +648,9 @@ def main():
     ap.add_argument("--split-precode", action="store_true", help="precode kernel + chain_txrx_pre")
     ap.add_argument("--precode-math", default="simt", choices=["simt", "tf32", "fp32tc"],
                     help="split-path precode: FP32 SIMT, TF32 tensor cores, or FP32-accurate split-TF32 tensor cores")
+    ap.add_argument("--mode", default="auto", choices=["auto", "symbol", "antenna"],
+                    help="multi-GPU partitioning: symbol batches (Mode S) or antennas (Mode A); auto = antenna "
+                         "for C5 at N > 1 (BASELINE configs[4]), else symbol")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
@@ -520,8 +659,14 @@ def main():
         cfg = configs.impaired(cfg)
     if (args.impair or args.redraw) and args.unfused:
         ap.error("--impair/--redraw run on the fused path only")
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    antenna = args.mode == "antenna" or (args.mode == "auto" and ws > 1 and cfg.name == "C5")
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif antenna:
+        if args.impair or args.redraw or args.unfused:
+            ap.error("Mode A runs the default chain only")
+        run_antenna(args, cfg)
     else:
         run_ours(args, cfg)
 

@@ -73,6 +73,11 @@ void fd_shutdown(void);
  * ------------------------------------------------------------------------- */
 enum { FD_CNN_AUTO = 0, FD_CNN_SIMT = 1, FD_CNN_TENSOR = 2 };
 int fd_set_cnn_path(int path);
+/* Operand precision of the tensor-core hidden layers (process-wide): 0 = FP16 split (default:
+ * fp16 hi + lo halves with exact power-of-two scales, kind::f16, K = 16 per MMA), 1 = TF32 split
+ * (kind::tf32).  Both keep three of the four hi/lo products (22 significant bits per operand),
+ * FP32 accumulation.  FD_ERR_ARG for other modes. */
+int fd_set_cnn_tc_precision(int mode);
 size_t fdcnn_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d);
 int fdcnn_forward(const float* params, const int* chans, int n_layers,
                   const void* s_in, void* s_out, void* workspace, size_t workspace_bytes,

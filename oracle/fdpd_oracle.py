@@ -385,8 +385,12 @@ def run_config_redraw(cfg, inp, h_taps_per_symbol):
 
 
 def run_config(cfg, inp):
-    """run_chain with a workload.configs.ChainConfig and a workload.gen.make_inputs bundle."""
-    return run_chain(inp["s"], inp["idx"], inp["h_taps"], inp["coef"], inp["params"],
+    """run_chain with a workload.configs.ChainConfig and a workload.gen.make_inputs bundle.  The
+    transmitted symbols are derived here from the QAM indices (qam_points), rounded to
+    complex64 like the canonical GPU input (the oracle runs on the canonical fp32
+    inputs upcast exactly), so the oracle does not take the generator's symbol values."""
+    s = qam_points(inp["idx"], cfg.M_qam).astype(np.complex64).astype(np.complex128)
+    return run_chain(s, inp["idx"], inp["h_taps"], inp["coef"], inp["params"],
                      chans=cfg.chans, orders=cfg.orders, L=cfg.L, M=cfg.M,
                      N_ifft=cfg.N_ifft, M_qam=cfg.M_qam, rho=cfg.rho, head=cfg.head, n_conv=cfg.n_conv,
                      clip=cfg.clip, pa_noise_std=cfg.pa_noise_std, awgn_n0=cfg.awgn_n0, csi_eta=cfg.csi_eta,

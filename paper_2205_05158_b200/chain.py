@@ -42,8 +42,10 @@ class Shapes:
 
 class Chain:
     def __init__(self, shapes: Shapes, h_taps, coef, params, device="cuda", max_batch=1, b0=0, B_loc=None,
-                 impair=None):
-        """impair (NEXT f3, optional): dict with clip, pa_noise_std, awgn_n0, csi_eta, noise_key, h_err."""
+                 impair=None, precode_math="simt"):
+        """impair (NEXT f3, optional): dict with clip, pa_noise_std, awgn_n0, csi_eta, noise_key, h_err.
+        precode_math (split path): "simt" FP32 SIMT, "tf32" TF32 tensor cores, "fp32tc" FP32-accurate
+        split-TF32 tensor cores (the latter two on the precode_pack'ed precoder)."""
         self.sh = shapes
         self.device = torch.device(device)
         dev = self.device
@@ -66,6 +68,8 @@ class Chain:
         else:
             self.h_fd, self.P, self.alpha = fdpd.zf_precoder_build(self.h_taps, shapes.N_ifft, shapes.N_d,
                                                                    shapes.rho, b0=b0, B_loc=self.B_loc)
+        self.precode_math = precode_math
+        self.Ppk = fdpd.precode_pack(self.P) if precode_math != "simt" else None
         self.reserve(max_batch)
 
     def _imp(self, sym0):
@@ -127,6 +131,8 @@ class Chain:
         if getattr(self, "X", None) is None or self.X.shape[0] < n:
             self.X = torch.empty((max(n, self.cap), self.B_loc, self.sh.N_d), dtype=torch.complex64,
                                  device=self.device)
+        if self.Ppk is not None:
+            return fdpd.precode_packed(self.Ppk, s_tilde, out=self.X[:n], math=fdpd.MATH[self.precode_math])
         return fdpd.precode(self.P, s_tilde, out=self.X[:n])
 
     def txrx_pre(self, X, sym0=0):
@@ -194,3 +200,42 @@ class Chain:
             return self.rx(self.tx(st), tx_idx, counts=counts, dec=dec)
         _, XPA = self.txrx(st, sym0)
         return self.combine(XPA, tx_idx, counts=counts, dec=dec, sym0=sym0)
+
+
+class AntennaOps:
+    """Per-rank compute of the Mode A step (dist.AntennaShardedStep) on the CUDA path: a Chain
+    built on this rank's antenna rows [b0, b0 + B_loc) (zf_precoder_build emits only those rows
+    from the replicated taps; alpha is the global one)."""
+
+    def __init__(self, chain: Chain, events=None):
+        self.ch = chain
+        self.events = events          # optional list: (start, end) CUDA events around each chain launch
+
+    def dpd(self, s, out):
+        ch = self.ch
+        if ch.sh.head == "paper":
+            return fdpd.fdcnn_paper_forward(ch.params, ch.sh.n_conv, s, out=out, workspace=ch.ws_cnn)
+        return fdpd.fdcnn_forward(ch.params, ch.sh.chans, s, out=out, workspace=ch.ws_cnn)
+
+    def tx(self, st_all, XPA=None):
+        """precode (split path) -> IDFT -> GMP (waveform into the plan's y) -> receive DFT."""
+        ch, sh = self.ch, self.ch.sh
+        n = st_all.shape[0]
+        if XPA is None:
+            XPA = torch.empty((n, ch.B_loc, sh.N_d), dtype=torch.complex64, device=ch.device)
+        X = ch.precode(st_all)
+        if self.events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+        fdpd.chain_txrx_pre(X, ch.coef, sh.orders, sh.L, sh.M, sh.N_ifft, y=ch.y[:n], XPA=XPA)
+        if self.events is not None:
+            ev[1].record()
+            self.events.append(ev)
+        return XPA
+
+    def combine(self, XPA, out):
+        return fdpd.ue_combine(XPA, self.ch.h_fd, out=out)
+
+    def slice(self, yhat, idx, counts):
+        return fdpd.ue_slice_ser(yhat, self.ch.alpha, idx, self.ch.sh.M_qam, counts=counts,
+                                 boundary_eps=self.ch.sh.eps)

@@ -65,6 +65,48 @@ __global__ void k_tc_weights(const float* __restrict__ W, float* __restrict__ Wg
     }
 }
 
+// FP16 split (hidden layers, F16 = true): the same three products with fp16 halves (11 significant
+// bits each, 22 together, like the TF32 split) on kind::f16, which takes K = 16 per MMA for the
+// same 32 operand bytes per row: half the MMAs and half the shared-memory operand reads of the
+// TF32 split.  fp16's range is handled by exact power-of-two scales: activations (tanh outputs,
+// |x| <= 1) x 2^12, weights x 2^e with max |W| 2^e <= 2^14 (k_w_scale); the epilogue multiplies
+// the accumulators by 2^-(12+e) (exact).  Residuals below the fp16 normal range (|x| < 2^-15)
+// keep an absolute error <= 2^-37 instead of 2^-22 relative: negligible against the sums.
+constexpr float TC_ACT_SCALE = 4096.f;
+
+__global__ void k_w_scale(const float* __restrict__ W, int n, float* __restrict__ scale) {
+    __shared__ float red[32];
+    float m = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(W[i]));
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) scale[0] = m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+    }
+}
+
+// fp16 weights: per tap [ci/8][n][8] with rows n < NP = hi(W[n] s), NP + co = lo(W[co] s).
+__global__ void k_tc_weights_f16(const float* __restrict__ W, __half* __restrict__ Wg, int Cin, int Cout, int CINP,
+                                 int NP, const float* __restrict__ scale) {
+    const int per_tap = 2 * CINP * NP;
+    const int n = 9 * per_tap;
+    const float sc = scale[0];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const int tap = e / per_tap;
+        int r = e - tap * per_tap;
+        const int gq = r / (2 * NP * 8);
+        r -= gq * 2 * NP * 8;
+        const int row = r >> 3, ci = 8 * gq + (r & 7);
+        const int hl = row >= NP, co = row - hl * NP;
+        const float w = (co < Cout && ci < Cin) ? W[((size_t)co * Cin + ci) * 9 + tap] * sc : 0.f;
+        const __half hi = __float2half_rn(w);
+        Wg[e] = hl ? __float2half_rn(w - __half2float(hi)) : hi;
+    }
+}
+
 // Warp roles (no CTA-wide barrier inside the tile loop; mbarrier pipelines between roles):
 //   warps 0-7   epilogue: TMEM lane quadrant (w % 4) (pixels 32(w%4)..+31) x column half w / 4
 //   warps 8-15  A producers: load, split hi/lo, store one K chunk (CK input channels) of a tile
@@ -91,23 +133,29 @@ struct TcRoles {
     static constexpr int LOAD_THREADS = 32 * LOAD, EPI_THREADS = 32 * EPI;
 };
 
-__host__ __device__ constexpr int tc_ck(int cinp) { return cinp >= 32 ? 32 : cinp; }
+__host__ __device__ constexpr int tc_ck(int cinp, bool f16) {
+    return f16 ? (cinp >= 64 ? 64 : cinp) : (cinp >= 32 ? 32 : cinp);
+}
 
-template <int CINP, int NP, int IN_MODE, int OUT_MODE>
+template <int CINP, int NP, int IN_MODE, int OUT_MODE, bool F16>
 __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
-    k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const float* __restrict__ Wg,
-              const float* __restrict__ bias, float* __restrict__ act_out, float2* __restrict__ s_out, TcConv g) {
-    constexpr int G = CINP / 4;           // 16-byte channel groups of a pixel in global memory
-    constexpr int CK = tc_ck(CINP);       // input channels per K chunk
+    k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const void* __restrict__ Wg,
+              const float* __restrict__ bias, const float* __restrict__ wscale, float* __restrict__ act_out,
+              float2* __restrict__ s_out, TcConv g) {
+    static_assert(!F16 || IN_MODE == 0, "the fp16 split serves the hidden layers");
+    constexpr int EB = F16 ? 2 : 4;       // operand bytes per element in shared memory
+    constexpr int G = CINP / 4;           // 16-byte fp32 channel groups of a pixel in global memory
+    constexpr int CK = tc_ck(CINP, F16);  // input channels per K chunk
     constexpr int NCH = CINP / CK;        // K chunks per tile
-    constexpr int GC = CK / 4;            // 16-byte planes per hi / lo of one chunk
-    constexpr int KSC = CK / 8;           // K = 8 steps per chunk (two MMAs each: A_hi, A_lo)
+    constexpr int GC = CK * EB / 16;      // 16-byte planes per hi / lo of one chunk
+    constexpr int KPM = 32 / EB;          // K per MMA: 8 (tf32) or 16 (f16) = 32 bytes per row
+    constexpr int KSC = CK / KPM;         // K steps per chunk (two MMAs each: A_hi, A_lo)
     constexpr int NW = 9 * NCH;           // weight slices per tile, order (chunk, tap)
-    constexpr uint32_t WCB = (uint32_t)CK * 2 * NP * 4;   // bytes per weight slice
-    constexpr uint32_t IDESC = idesc_tf32_m128(2 * NP);
+    constexpr uint32_t WCB = (uint32_t)CK * 2 * NP * EB;  // bytes per weight slice
+    constexpr uint32_t IDESC = F16 ? idesc_f16_m128(2 * NP) : idesc_tf32_m128(2 * NP);
     // the A_lo MMA reads only the first NP rows of B (W_hi): A_lo W_lo (~2^-22 relative) is
     // dropped and the MMA reads 25 % fewer shared-memory bytes
-    constexpr uint32_t IDESC_LO = idesc_tf32_m128(NP);
+    constexpr uint32_t IDESC_LO = F16 ? idesc_f16_m128(NP) : idesc_tf32_m128(NP);
     using Roles = TcRoles<IN_MODE, NP>;
     constexpr int TC_EPI_WARPS = Roles::EPI, TC_LOAD_WARPS = Roles::LOAD;
     constexpr int TC_MMA_WARP = Roles::MMA_WARP, TC_W_WARP = Roles::W_WARP;
@@ -141,6 +189,7 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
         }
     }
     if (tid < NP) bsm[tid] = tid < g.Cout ? bias[tid] : 0.f;
+    if (tid == NP) bsm[NP] = F16 ? 1.f / (TC_ACT_SCALE * wscale[0]) : 1.f;   // accumulator scale
     if (warp == 0) tmem_alloc(tmem_slot, g.tmem_cols);
     tc_fence_before();
     __syncthreads();
@@ -165,7 +214,40 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
             for (int c = 0; c < NCH; ++c, ++n_staged) {
                 if (n_staged >= g.na) mbar_wait(&a_empty[buf], ph ^ 1u);
                 unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
-                if constexpr (IN_MODE == 0) {
+                if constexpr (IN_MODE == 0 && F16) {
+                    // 8 channels (two fp32 float4) -> 16 bytes of fp16 hi and 16 bytes of lo
+                    const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP) + c * (CK / 4);
+                    constexpr int PB = 4;
+                    const int ne = g.A_px * GC;
+                    for (int e0 = lt; e0 < ne; e0 += PB * TC_LOAD_THREADS) {
+                        float4 x[PB][2];
+#pragma unroll
+                        for (int k = 0; k < PB; ++k) {
+                            const int e = e0 + k * TC_LOAD_THREADS;
+                            const int p = e / GC, gq = e - p * GC;
+                            const int pos = qa + p;
+                            x[k][0] = x[k][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (e < ne && pos >= 0 && pos < g.P) {
+                                x[k][0] = __ldg(src + (size_t)pos * G + 2 * gq);
+                                x[k][1] = __ldg(src + (size_t)pos * G + 2 * gq + 1);
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < PB; ++k) {
+                            const int e = e0 + k * TC_LOAD_THREADS;
+                            if (e >= ne) break;
+                            const int p = e / GC, gq = e - p * GC;
+                            constexpr float S = TC_ACT_SCALE;
+                            uint4 hi, lo;
+                            split_f16x2(x[k][0].x * S, x[k][0].y * S, hi.x, lo.x);
+                            split_f16x2(x[k][0].z * S, x[k][0].w * S, hi.y, lo.y);
+                            split_f16x2(x[k][1].x * S, x[k][1].y * S, hi.z, lo.z);
+                            split_f16x2(x[k][1].z * S, x[k][1].w * S, hi.w, lo.w);
+                            *reinterpret_cast<uint4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
+                            *reinterpret_cast<uint4*>(ab + (size_t)(GC + gq) * g.PL + p * 16) = lo;
+                        }
+                    }
+                } else if constexpr (IN_MODE == 0) {
                     const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP) + c * GC;
                     // PB independent 16-byte loads in flight per thread before any split / store
                     constexpr int PB = 8;
@@ -238,8 +320,9 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
             if (elect_one()) {
                 const int c = sl / 9, tap = sl - 9 * c;
                 mbar_arrive_expect_tx(&wfull[lslot], WCB);
-                tma_bulk_g2s(sm + (size_t)lslot * WCB, Wg + (size_t)tap * CINP * 2 * NP + (size_t)c * CK * 2 * NP, WCB,
-                             &wfull[lslot]);
+                tma_bulk_g2s(sm + (size_t)lslot * WCB,
+                             static_cast<const char*>(Wg) + ((size_t)tap * CINP * 2 * NP + (size_t)c * CK * 2 * NP) * EB,
+                             WCB, &wfull[lslot]);
             }
             __syncwarp();
             if (++lslot == g.ws) { lslot = 0; lph ^= 1u; }
@@ -281,13 +364,16 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
                             const uint64_t ahi = at + (uint64_t)(2u * k * PL16);
                             const uint64_t alo = ahi + (uint64_t)(GC * PL16);
                             const uint64_t b = wb + (uint64_t)(2 * k * 2 * NP);
-                            mma_tf32(dt, ahi, b, IDESC, (c | k) != 0 || (tap != 0 && tap != 5) ? 1u : 0u);
+                            const uint32_t accum = (c | k) != 0 || (tap != 0 && tap != 5) ? 1u : 0u;
+                            if constexpr (F16) mma_f16(dt, ahi, b, IDESC, accum);
+                            else mma_tf32(dt, ahi, b, IDESC, accum);
                             // A_lo x W_hi (N = NP) into the small-term half (columns NP..2NP, next to
                             // A_hi x W_lo): the tensor core's FP32 accumulation rounds toward zero,
                             // so every MMA into the large A_hi W_hi accumulator adds a bias of ~1/2
                             // ulp of the running sum; keeping the small products out of it halves
                             // that bias (C5: the CNN output's coherent error 1.1e-6 -> see DESIGN)
-                            mma_tf32(dt + NP, alo, b, IDESC_LO, 1u);
+                            if constexpr (F16) mma_f16(dt + NP, alo, b, IDESC_LO, 1u);
+                            else mma_tf32(dt + NP, alo, b, IDESC_LO, 1u);
                         }
                         if (!resident) umma_commit(&wempty[cslot]);
                     }
@@ -317,6 +403,7 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
             const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)acc * (4 * NP);
             const int prow = pos / g.Wp, pcol = pos - prow * g.Wp;
             const bool interior = pos < g.q_end && pcol >= 1 && pcol <= g.S;
+            const float dscale = bsm[NP];
             if constexpr (OUT_MODE == 0) {
                 float* o = act_out + ((size_t)img * g.P + pos) * NP;
                 constexpr int HC = NP / NGRP;         // columns per warp (>= 8)
@@ -329,7 +416,7 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
                     tmem_ld8(tbase + 3 * NP + c0, w2);
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        v[j] = interior ? tanhf(((v[j] + v2[j]) + (w[j] + w2[j])) + bsm[c0 + j]) : 0.f;
+                        v[j] = interior ? tanhf(((v[j] + v2[j]) + (w[j] + w2[j])) * dscale + bsm[c0 + j]) : 0.f;
                     if (pos < g.q_end) {
                         reinterpret_cast<float4*>(o + c0)[0] = make_float4(v[0], v[1], v[2], v[3]);
                         reinterpret_cast<float4*>(o + c0)[1] = make_float4(v[4], v[5], v[6], v[7]);
@@ -362,7 +449,7 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
                 if (half == 0 && interior && k < g.N_d) {
                     const size_t o = (size_t)img * g.N_d + k;
                     const float2 z = __ldg(s_in + o);
-                    s_out[o] = make_float2(z.x + ((v[0] + w[0]) + bsm[0]), z.y + ((v[1] + w[1]) + bsm[1]));
+                    s_out[o] = make_float2(z.x + ((v[0] + w[0]) * dscale + bsm[0]), z.y + ((v[1] + w[1]) * dscale + bsm[1]));
                 }
             }
         }
@@ -496,14 +583,15 @@ static TcConv tc_geom(int S, int N_d, int Cin, int Cout, long long n_img) {
 // smem plan: weight slices (ws slots of CK x 2NP) | A chunk ring (na buffers) | bias |
 // barriers.  Order of preference: resident weights with >= 2 A chunks in flight; a weight
 // ring of >= 4 slices with >= 2 A chunks; then shallower variants.
-static size_t tc_plan(TcConv& g, int CINP, int NP) {
-    const int CK = tc_ck(CINP), NW = 9 * (CINP / CK);
-    const size_t slice = (size_t)CK * 2 * NP * 4, abuf = 2ull * (CK / 4) * g.PL;
+static size_t tc_plan(TcConv& g, int CINP, int NP, bool f16) {
+    const int EB = f16 ? 2 : 4;
+    const int CK = tc_ck(CINP, f16), NW = 9 * (CINP / CK);
+    const size_t slice = (size_t)CK * 2 * NP * EB, abuf = 2ull * (CK * EB / 16) * g.PL;
     const size_t limit = 227 * 1024;
     auto bytes_of = [&](int ws, int na, size_t& off_a, size_t& off_bias, size_t& off_bar) {
         off_a = ws * slice;
         off_bias = off_a + na * abuf;
-        off_bar = (off_bias + NP * 4 + 15) & ~(size_t)15;
+        off_bar = (off_bias + (NP + 4) * 4 + 15) & ~(size_t)15;
         return off_bar + 8 * (4 + 2 * na + 2 * ws) + 16;
     };
     auto take = [&](int ws, int na) -> size_t {
@@ -534,10 +622,10 @@ static size_t tc_plan(TcConv& g, int CINP, int NP) {
     return 0;
 }
 
-template <int CINP, int NP, int IN_MODE, int OUT_MODE>
-static int launch_tc_na(const TcConv& g, size_t smem, const float* act_in, const float2* s_in, const float* Wg,
-                        const float* bias, float* act_out, float2* s_out, cudaStream_t st) {
-    auto kern = k_conv_tc<CINP, NP, IN_MODE, OUT_MODE>;
+template <int CINP, int NP, int IN_MODE, int OUT_MODE, bool F16>
+static int launch_tc_na(const TcConv& g, size_t smem, const float* act_in, const float2* s_in, const void* Wg,
+                        const float* bias, const float* wscale, float* act_out, float2* s_out, cudaStream_t st) {
+    auto kern = k_conv_tc<CINP, NP, IN_MODE, OUT_MODE, F16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, dev = 0, nsm = 148;
     constexpr int THREADS = TcRoles<IN_MODE, NP>::THREADS;
@@ -546,19 +634,22 @@ static int launch_tc_na(const TcConv& g, size_t smem, const float* act_in, const
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long tiles = g.n_img * g.n_tiles;
     const long long grid = std::min<long long>(tiles, (long long)nsm * std::max(per_sm, 1));
-    kern<<<(unsigned)grid, THREADS, smem, st>>>(act_in, s_in, Wg, bias, act_out, s_out, g);
+    kern<<<(unsigned)grid, THREADS, smem, st>>>(act_in, s_in, Wg, bias, wscale, act_out, s_out, g);
     return check_launch("fdcnn_forward (tensor-core conv)");
 }
 
-template <int IN_MODE, int OUT_MODE, int CINP>
-static int launch_tc_n(int NP, const TcConv& g, size_t smem, const float* act_in, const float2* s_in, const float* Wg,
-                       const float* bias, float* act_out, float2* s_out, cudaStream_t st) {
+template <int IN_MODE, int OUT_MODE, int CINP, bool F16>
+static int launch_tc_n(int NP, const TcConv& g, size_t smem, const float* act_in, const float2* s_in, const void* Wg,
+                       const float* bias, const float* wscale, float* act_out, float2* s_out, cudaStream_t st) {
     switch (NP) {
-        case 16: return launch_tc_na<CINP, 16, IN_MODE, OUT_MODE>(g, smem, act_in, s_in, Wg, bias, act_out, s_out, st);
-        case 32: return launch_tc_na<CINP, 32, IN_MODE, OUT_MODE>(g, smem, act_in, s_in, Wg, bias, act_out, s_out, st);
-        default: return launch_tc_na<CINP, 64, IN_MODE, OUT_MODE>(g, smem, act_in, s_in, Wg, bias, act_out, s_out, st);
+        case 16: return launch_tc_na<CINP, 16, IN_MODE, OUT_MODE, F16>(g, smem, act_in, s_in, Wg, bias, wscale, act_out, s_out, st);
+        case 32: return launch_tc_na<CINP, 32, IN_MODE, OUT_MODE, F16>(g, smem, act_in, s_in, Wg, bias, wscale, act_out, s_out, st);
+        default: return launch_tc_na<CINP, 64, IN_MODE, OUT_MODE, F16>(g, smem, act_in, s_in, Wg, bias, wscale, act_out, s_out, st);
     }
 }
+
+// Hidden-layer operand precision: FP16 split (default) or the TF32 split (fd_set_cnn_tc_precision).
+static int g_tc_f16 = 1;
 
 // Workspace: two channels-last haloed activation buffers + the split weights of every layer.
 size_t fdcnn_tc_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d) {
@@ -570,7 +661,7 @@ size_t fdcnn_tc_workspace_bytes(const int* chans, int n_layers, long long n_sym,
     const size_t one = (((size_t)n_sym * U * P * cmax * 4) + 255) & ~(size_t)255;
     size_t bytes = (n_layers > 2 ? 2 : 1) * one;
     for (int l = 0; l < n_layers; ++l)
-        bytes += ((size_t)9 * 2 * pad_ch(chans[l]) * pad_n(chans[l + 1]) * 4 + 255) & ~(size_t)255;
+        bytes += (((size_t)9 * 2 * pad_ch(chans[l]) * pad_n(chans[l + 1]) * 4 + 255) & ~(size_t)255) + 256;
     return bytes;
 }
 
@@ -594,19 +685,28 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
         const float* W = params + off;
         const float* b = W + (size_t)co * ci * 9;
         off += (size_t)co * ci * 9 + co;
-        float* Wg = reinterpret_cast<float*>(wptr);
+        const bool first = l == 0, last = l == n_layers - 1;
+        const bool f16 = g_tc_f16 && !first && !last;
+        void* Wg = wptr;
         const int nw = 9 * 2 * CINP * NP;
         wptr += ((size_t)nw * 4 + 255) & ~(size_t)255;
-        k_tc_weights<<<(nw + 255) / 256, 256, 0, stream>>>(W, Wg, ci, co, CINP, NP);
+        float* wscale = reinterpret_cast<float*>(wptr);
+        wptr += 256;
+        if (f16) {
+            k_w_scale<<<1, 256, 0, stream>>>(W, co * ci * 9, wscale);
+            k_tc_weights_f16<<<(nw + 255) / 256, 256, 0, stream>>>(W, static_cast<__half*>(Wg), ci, co, CINP, NP,
+                                                                   wscale);
+        } else if (!last) {
+            k_tc_weights<<<(nw + 255) / 256, 256, 0, stream>>>(W, static_cast<float*>(Wg), ci, co, CINP, NP);
+        }
         if ((rc = check_launch("fdcnn_forward (weight split)"))) return rc;
         TcConv g = tc_geom(S, N_d, ci, co, n_img);
         FD_REQUIRE(n_img * g.n_tiles < (1LL << 31), "fdcnn_forward: too many images per call for the tensor-core path");
-        const size_t smem = tc_plan(g, CINP, NP);
+        const size_t smem = tc_plan(g, CINP, NP, f16);
         if (!smem) return fail_arg("fdcnn_forward: tensor-core plan does not fit shared memory");
-        const bool first = l == 0, last = l == n_layers - 1;
         const float* in = first ? nullptr : act[(l - 1) & 1];
         float* out = last ? nullptr : act[l & 1];
-        if (first) rc = launch_tc_n<1, 0, 8>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream);
+        if (first) rc = launch_tc_n<1, 0, 8, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream);
         else if (last) {
             // C_out = 2: direct FP32 convolution on the channels-last activations
             const long long nth = n_img * (long long)(((S + 3) / 4) * ((S + 3) / 4)) * (CINP / 4);
@@ -618,10 +718,18 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
             }
             rc = check_launch("fdcnn_forward (last layer)");
         } else {
-            switch (CINP) {
-                case 16: rc = launch_tc_n<0, 0, 16>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
-                case 32: rc = launch_tc_n<0, 0, 32>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
-                default: rc = launch_tc_n<0, 0, 64>(NP, g, smem, in, s_in, Wg, b, out, s_out, stream); break;
+            if (f16) {
+                switch (CINP) {
+                    case 16: rc = launch_tc_n<0, 0, 16, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                    case 32: rc = launch_tc_n<0, 0, 32, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                    default: rc = launch_tc_n<0, 0, 64, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                }
+            } else {
+                switch (CINP) {
+                    case 16: rc = launch_tc_n<0, 0, 16, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                    case 32: rc = launch_tc_n<0, 0, 32, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                    default: rc = launch_tc_n<0, 0, 64, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                }
             }
         }
         if (rc) return rc;
@@ -630,3 +738,9 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
 }
 
 }  // namespace fdpd
+
+extern "C" int fd_set_cnn_tc_precision(int mode) {
+    FD_REQUIRE(mode == 0 || mode == 1, "fd_set_cnn_tc_precision: mode=%d (0 = FP16 split, 1 = TF32 split)", mode);
+    fdpd::g_tc_f16 = mode == 0 ? 1 : 0;
+    return FD_OK;
+}

@@ -173,21 +173,31 @@ struct RunLayout {
 // (N local); window chunks left of 0 or right of N come from the partner CTA's buffers
 // (usw_r / esw_r, distributed shared memory), which hold the other half — for two halves the
 // partner is both the left and the right (circular) neighbour.
-template <int KP, int L, int M, int R, bool HALO = false>
-__device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const float* __restrict__ esw,
-                                        const float2* __restrict__ cf, int N, int rho, float2 (&out)[R],
-                                        const float2* usw_r = nullptr, const float* esw_r = nullptr) {
-    static_assert(R % 4 == 0, "run length must be a multiple of 4");
+//
+// The memory taps l are processed in chunks [L0, L1] (gmp_run_taps), each with its own envelope
+// and input windows: the registers hold the windows of one chunk only.  At the C4/C5 shape
+// (Kp = 5, L = 6, M = 3, R = 4) the whole-run windows took 4 x 20 envelope powers + 10 complex
+// inputs and the 128-register kernel spilled (272 B of stack); in two chunks the envelope
+// window is 4 x 16.  The summation order over l (and within each l) is unchanged.
+__host__ __device__ constexpr int round_up_pow2(int x, int a) { return (x + a - 1) & ~(a - 1); }
+
+template <int KP, int L, int M, int R, bool HALO, int L0, int L1>
+__device__ __forceinline__ void gmp_run_taps(const float2* __restrict__ usw, const float* __restrict__ esw,
+                                             const float2* __restrict__ cf, int N, int rho, float2 (&out)[R],
+                                             const float2* usw_r, const float* esw_r) {
     using Row = CoefRow<KP, M>;
     using Lay = RunLayout<R>;
     constexpr int NP = KP > 1 ? KP - 1 : 1;
-    constexpr int E_LO = ((L + M) + 3) & ~3;            // envelope samples before the run (chunk aligned)
-    constexpr int E_HI = ((R + M) + 3) & ~3;            // from the run start
+    // window of envelope samples m0 - E_LO .. m0 + E_HI - 1 (16-byte chunks): q = m0 + i - l +- g
+    constexpr int E_LO = round_up_pow2(L1 + M, 4);
+    constexpr int E_HI = round_up_pow2(R - L0 + M, 4);
     constexpr int E_N = E_LO + E_HI;
-    constexpr int U_LO = (L + 1) & ~1;                  // input samples before the run (chunk aligned)
-    constexpr int U_N = U_LO + R;
+    // window of inputs m0 - U_LO .. m0 + U_HI - 1: q = m0 + i - l
+    constexpr int U_LO = round_up_pow2(L1, 2);
+    constexpr int U_HI = round_up_pow2(R - L0, 2);
+    constexpr int U_N = U_LO + U_HI;
+    static_assert(E_N > 0 && U_N > 0, "empty GMP window");
     const int m0 = R * rho;
-
     float ew[NP][E_N];
     {
         const float4* e4 = reinterpret_cast<const float4*>(esw);
@@ -231,9 +241,7 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
         }
     }
 #pragma unroll
-    for (int i = 0; i < R; ++i) out[i] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int l = 0; l <= L; ++l) {
+    for (int l = L0; l <= L1; ++l) {
         const float4* row = reinterpret_cast<const float4*>(cf + l * Row::STRIDE);
         float2 G[R];
         // window index of q = m0 + i - l + delta is  i - l + delta + E_LO
@@ -264,6 +272,30 @@ __device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const fl
     }
 }
 
+// Taps per window chunk: all L + 1 at once except the largest specialised shape (Kp = 5 with
+// L >= 6, C4 / C5), which runs two chunks to stay inside 128 registers.
+template <int KP, int L, int M>
+__host__ __device__ constexpr int gmp_tap_chunk() { return (KP >= 5 && L >= 6) ? 4 : L + 1; }
+
+template <int KP, int L, int M, int R, bool HALO, int L0>
+__device__ __forceinline__ void gmp_run_chunks(const float2* __restrict__ usw, const float* __restrict__ esw,
+                                               const float2* __restrict__ cf, int N, int rho, float2 (&out)[R],
+                                               const float2* usw_r, const float* esw_r) {
+    constexpr int LC = gmp_tap_chunk<KP, L, M>();
+    constexpr int L1 = (L0 + LC - 1 < L) ? L0 + LC - 1 : L;
+    gmp_run_taps<KP, L, M, R, HALO, L0, L1>(usw, esw, cf, N, rho, out, usw_r, esw_r);
+    if constexpr (L1 < L) gmp_run_chunks<KP, L, M, R, HALO, L1 + 1>(usw, esw, cf, N, rho, out, usw_r, esw_r);
+}
+
+template <int KP, int L, int M, int R, bool HALO = false>
+__device__ __forceinline__ void gmp_run(const float2* __restrict__ usw, const float* __restrict__ esw,
+                                        const float2* __restrict__ cf, int N, int rho, float2 (&out)[R],
+                                        const float2* usw_r = nullptr, const float* esw_r = nullptr) {
+    static_assert(R % 4 == 0, "run length must be a multiple of 4");
+#pragma unroll
+    for (int i = 0; i < R; ++i) out[i] = make_float2(0.f, 0.f);
+    gmp_run_chunks<KP, L, M, R, HALO, 0>(usw, esw, cf, N, rho, out, usw_r, esw_r);
+}
 // Whole symbol: relayout of the (already scaled) IDFT output held in the FFT buffer
 // (pidx layout) into the swizzled u/e layouts, then all runs; y (global) gets R
 // contiguous complex per run via 128-bit stores.  usw aliases the FFT buffer.

@@ -26,20 +26,19 @@
 //
 // CTA = (antenna tile of 128, symbol tile, contiguous range of subcarriers); one pipeline stage
 // per subcarrier.  Warp roles (mbarrier rings, no CTA barrier in the loop):
-//   warps 0-15  epilogue: TMEM lane quadrant (w % 4) = 32 antennas x column group (w / 4) = a
-//               quarter of the symbols; sums big + small, buffers JB subcarriers in registers
-//               and writes X[n][b][j..j+JB) as 16-byte runs
-//   warps 16-23 producers: load P / s for the stage (loads issued before waiting for the
+//   warps 0-3   epilogue: TMEM lane quadrant (w % 4) = 32 antennas, all symbols of the tile; per quad of 4 subcarriers held in TMEM, sums big + small
+//               and writes X[n][b][j..j+4) as full 32-byte sectors
+//   warps 4-19  producers: load P / s for the stage (loads issued before waiting for the
 //               buffer), split, store the K-major operands, fence.proxy.async, arrive
-//   warp 24     MMA issue (one elected lane), commits to the stage's empty barrier and the TMEM
+//   warp 20     MMA issue (one elected lane), commits to the stage's empty barrier and the TMEM
 //               slot's full barrier
-// Stages: NS shared-memory buffers; TMEM: 4 slots of 128 columns (512).
+// Stages: NS shared-memory buffers; TMEM: one quad of 4 subcarriers x 128 columns (512).
 #include "common.cuh"
 #include "tcgen05.cuh"
 
 namespace fdpd {
 
-constexpr int PT_EPI = 16, PT_PROD = 8;
+constexpr int PT_EPI = 4, PT_PROD = 16;
 constexpr int PT_MMA_WARP = PT_EPI + PT_PROD;
 constexpr int PT_THREADS = 32 * (PT_MMA_WARP + 1);
 constexpr int PT_ROWS = 128;                 // rows of every operand plane (M = 128, N = 128)
@@ -68,6 +67,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld4_nowait(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void split4(float4 x, float4& hi, float4& lo) {
     hi.x = tf32_rna(x.x); lo.x = tf32_rna(x.x - hi.x);
     hi.y = tf32_rna(x.y); lo.y = tf32_rna(x.y - hi.y);
@@ -83,8 +89,7 @@ template <int HL, bool PACKED>
 __global__ void __launch_bounds__(PT_THREADS, 1)
     k_precode_tc(const float* __restrict__ P, const float2* __restrict__ s, float2* __restrict__ X, PtGeom g) {
     constexpr int NT = 64 / HL;              // symbols per tile (Bs rows = HL * 2 NT = 128)
-    constexpr int NPW = NT / 4;              // symbols per epilogue warp column group
-    constexpr int JB = HL;                   // subcarriers buffered per epilogue store (register budget)
+    constexpr int NPW = NT / (PT_EPI / 4);   // symbols per epilogue warp column group
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int plane_set = g.planes * PT_PLANE;             // bytes of one operand (all K planes)
@@ -124,49 +129,45 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
 
     if (warp >= PT_EPI && warp < PT_MMA_WARP) {
         // ---------------------------------------------------------------- producers
+        // Software-pipelined by one stage: the loads of stage i + 1 are in flight while stage i
+        // is split and stored (one stage of loads per thread left the loop latency-bound:
+        // 1.9 TB/s at C5, long-scoreboard stalls).
         const int pt = tid - 32 * PT_EPI;
         const int KQ = g.planes;             // 16-byte k-quads per row (= U / 2)
         const int UQ = U >> 2;               // u-quads
-        int buf = 0;
-        uint32_t ph = 0;
-        for (int i = 0; i < n_stages; ++i) {
-            const int j = ja + i;
-            // A rows: packed -> item (row, k-quad) one float4; plain -> item (row, u-quad), 4 float2
-            constexpr int MAXA = PACKED ? 8 : 4;   // items per thread at U <= 32 (128 rows x U/2 or U/4 quads)
+        constexpr int MAXA = PACKED ? 4 : 2; // A items per thread at U <= 32 (128 rows x U/2 or U/4 quads)
+        constexpr int PA = PACKED ? 1 : 4;   // float2 loads per plain A item
+        const int na = PACKED ? PT_ROWS * KQ : PT_ROWS * UQ;
+        const int ns_items = NT * UQ;        // symbol items (n, u-quad), <= 1 per thread
+        struct Regs {
             float4 av[MAXA];
-            const int na = PACKED ? PT_ROWS * KQ : PT_ROWS * UQ;
-            float2 pv[PACKED ? 1 : MAXA][4];
+            float2 pv[MAXA][PA];
+            float2 sv[4];
+        };
+        auto load = [&](int j, Regs& R) {
 #pragma unroll
             for (int t = 0; t < MAXA; ++t) {
                 const int it = pt + t * 32 * PT_PROD;
                 if (it >= na) break;
                 if constexpr (PACKED) {
                     const int kq = it % KQ, r = it / KQ;
-                    av[t] = (b0 + r < B) ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)j * B + b0 + r) * 2 * U) + kq)
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                    R.av[t] = (b0 + r < B) ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)j * B + b0 + r) * 2 * U) + kq)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
                 } else {
                     const int uq = it % UQ, r = it / UQ;
                     const float2* src = reinterpret_cast<const float2*>(P) + ((size_t)(b0 + r) * U + 4 * uq) * N_d + j;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        pv[t][q] = (b0 + r < B) ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
+                    for (int q = 0; q < PA; ++q)
+                        R.pv[t][q] = (b0 + r < B) ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
                 }
             }
-            // symbol rows: item (n, u-quad), 4 float2 (NT x U/4 <= 512 items: <= 2 per thread)
-            constexpr int MAXS = 2;
-            float2 sv[MAXS][4];
-            const int ns_items = NT * UQ;
+            const int su = pt % UQ, sn = pt / UQ;
+            const bool ok = pt < ns_items && n0 + sn < g.n_sym;
+            const float2* src = s + ((size_t)(n0 + sn) * U + 4 * su) * N_d + j;
 #pragma unroll
-            for (int t = 0; t < MAXS; ++t) {
-                const int it = pt + t * 32 * PT_PROD;
-                const int su = it % UQ, sn = it / UQ;
-                const bool ok = it < ns_items && n0 + sn < g.n_sym;
-                const float2* src = s + ((size_t)(n0 + sn) * U + 4 * su) * N_d + j;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) sv[t][q] = ok ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
-            }
-            if (i >= g.ns) mbar_wait(&empty[buf], ph ^ 1u);
-            unsigned char* st = sm + (size_t)buf * g.stage_bytes;
+            for (int q = 0; q < 4; ++q) R.sv[q] = ok ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
+        };
+        auto store = [&](unsigned char* st, const Regs& R) {
             unsigned char* a_hi = st;
             unsigned char* a_lo = st + plane_set;
             unsigned char* bs = st + (HL == 2 ? 2 : 1) * plane_set;
@@ -179,16 +180,16 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                     const size_t off = (size_t)kq * PT_PLANE + r * 16;
                     if constexpr (HL == 2) {
                         float4 hi, lo;
-                        split4(av[t], hi, lo);
+                        split4(R.av[t], hi, lo);
                         *reinterpret_cast<float4*>(a_hi + off) = hi;
                         *reinterpret_cast<float4*>(a_lo + off) = lo;
                     } else {
-                        *reinterpret_cast<float4*>(a_hi + off) = rna4(av[t]);
+                        *reinterpret_cast<float4*>(a_hi + off) = rna4(R.av[t]);
                     }
                 } else {
                     const int uq = it % UQ, r = it / UQ;
-                    const float4 re = make_float4(pv[t][0].x, pv[t][1].x, pv[t][2].x, pv[t][3].x);
-                    const float4 im = make_float4(pv[t][0].y, pv[t][1].y, pv[t][2].y, pv[t][3].y);
+                    const float4 re = make_float4(R.pv[t][0].x, R.pv[t][1].x, R.pv[t][2].x, R.pv[t][3].x);
+                    const float4 im = make_float4(R.pv[t][0].y, R.pv[t][1].y, R.pv[t][2].y, R.pv[t][3].y);
                     const size_t ore = (size_t)uq * PT_PLANE + r * 16, oim = (size_t)(UQ + uq) * PT_PLANE + r * 16;
                     if constexpr (HL == 2) {
                         float4 hi, lo;
@@ -204,13 +205,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                     }
                 }
             }
-#pragma unroll
-            for (int t = 0; t < MAXS; ++t) {
-                const int it = pt + t * 32 * PT_PROD;
-                if (it >= ns_items) break;
-                const int su = it % UQ, sn = it / UQ;
-                const float4 re = make_float4(sv[t][0].x, sv[t][1].x, sv[t][2].x, sv[t][3].x);
-                const float4 im = make_float4(sv[t][0].y, sv[t][1].y, sv[t][2].y, sv[t][3].y);
+            if (pt < ns_items) {
+                const int su = pt % UQ, sn = pt / UQ;
+                const float4 re = make_float4(R.sv[0].x, R.sv[1].x, R.sv[2].x, R.sv[3].x);
+                const float4 im = make_float4(R.sv[0].y, R.sv[1].y, R.sv[2].y, R.sv[3].y);
                 // row (n, 0): [Re s | -Im s];  row (n, 1): [Im s | Re s]
                 const int r0 = 2 * sn, r1 = 2 * sn + 1;
                 const size_t p1 = (size_t)su * PT_PLANE, p2 = (size_t)(UQ + su) * PT_PLANE;
@@ -234,9 +232,22 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                     *reinterpret_cast<float4*>(bs + p2 + r1 * 16) = hre;
                 }
             }
+        };
+        int buf = 0;
+        uint32_t ph = 0;
+        Regs RA, RB;
+        auto stage = [&](int i, Regs& cur, Regs& nxt) {
+            if (i + 1 < n_stages) load(ja + i + 1, nxt);
+            if (i >= g.ns) mbar_wait(&empty[buf], ph ^ 1u);
+            store(sm + (size_t)buf * g.stage_bytes, cur);
             fence_proxy_async();
             mbar_arrive(&full[buf]);
             if (++buf == g.ns) { buf = 0; ph ^= 1u; }
+        };
+        if (n_stages > 0) load(ja, RA);
+        for (int i = 0; i < n_stages; i += 2) {
+            stage(i, RA, RB);
+            if (i + 1 < n_stages) stage(i + 1, RB, RA);
         }
     } else if (warp == PT_MMA_WARP) {
         // ---------------------------------------------------------------- MMA issue
@@ -247,8 +258,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         int buf = 0;
         uint32_t ph = 0;
         for (int i = 0; i < n_stages; ++i) {
+            // TMEM holds one quad of 4 consecutive subcarriers (4 x 128 columns); the quad's first
+            // MMA waits until the epilogue has drained the previous quad
             const int slot = i & (PT_SLOTS - 1);
-            if (i >= PT_SLOTS) mbar_wait(&tempty[slot], (uint32_t)(((i / PT_SLOTS) - 1) & 1));
+            if (slot == 0 && i >= PT_SLOTS) mbar_wait(&tempty[0], (uint32_t)(((i / PT_SLOTS) - 1) & 1));
             mbar_wait(&full[buf], ph);
             tc_fence_after();
             const uint32_t sb = base + (uint32_t)buf * g.stage_bytes;
@@ -263,65 +276,61 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                     if constexpr (HL == 2) mma_tf32(d + 64, dlo + kadv, dbs + kadv, ID_HALF, 1u);
                 }
                 umma_commit(&empty[buf]);
-                umma_commit(&tfull[slot]);
+                if (slot == PT_SLOTS - 1 || i == n_stages - 1) umma_commit(&tfull[0]);
             }
             __syncwarp();
             if (++buf == g.ns) { buf = 0; ph ^= 1u; }
         }
     } else if (warp < PT_EPI) {
         // ---------------------------------------------------------------- epilogue
+        // per quad of 4 subcarriers: for 2 symbols at a time read the 4 slots' (big + small)
+        // columns and write X[n][b][j..j+4) as one 32-byte sector per (n, b) (a partially
+        // written sector costs a DRAM read-modify-write: measured 1.9x the X bytes with 16-byte runs)
         const int quad = warp & 3, grp = warp >> 2;
         const int b = b0 + quad * 32 + lane;
         const int nb = grp * NPW;            // first symbol (within the tile) of this warp
-        float2 acc[JB][NPW];
-        int jfirst = ja;
-        for (int i = 0; i < n_stages; ++i) {
-            const int slot = i & (PT_SLOTS - 1);
-            mbar_wait(&tfull[slot], (uint32_t)((i / PT_SLOTS) & 1));
+        const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16);
+        for (int q = 0; q * PT_SLOTS < n_stages; ++q) {
+            const int cnt = min(PT_SLOTS, n_stages - q * PT_SLOTS);
+            const int jfirst = ja + q * PT_SLOTS;
+            mbar_wait(&tfull[0], (uint32_t)(q & 1));
             tc_fence_after();
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)slot * PT_COLS;
-            const int jj = i % JB;
-            // columns 2n + c (c = Re / Im); HL = 2: big at 0..63, small at 64..127
+            const bool vec = cnt == 4 && ((N_d & 3) == 0) && ((jfirst & 3) == 0);
+#pragma unroll 1
+            for (int p = 0; p < NPW / 2; ++p) {
+                const int nl = nb + 2 * p;                    // symbols nl, nl + 1 of the tile
+                uint32_t r[PT_SLOTS][4], r2[PT_SLOTS][4];
 #pragma unroll
-            for (int h = 0; h < NPW / 4; ++h) {     // 8 columns = 4 symbols per TMEM load
-                float v[8];
-                tmem_ld8(ta + 2 * (nb + 4 * h), v);
-                if constexpr (HL == 2) {
-                    float w2[8];
-                    tmem_ld8(ta + 64 + 2 * (nb + 4 * h), w2);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) v[q] += w2[q];
+                for (int t = 0; t < PT_SLOTS; ++t) {
+                    tmem_ld4_nowait(ta + (uint32_t)t * PT_COLS + 2 * nl, r[t]);
+                    if constexpr (HL == 2) tmem_ld4_nowait(ta + (uint32_t)t * PT_COLS + 64 + 2 * nl, r2[t]);
                 }
+                tmem_wait_ld();
+                float v[PT_SLOTS][4];
 #pragma unroll
-                for (int t = 0; t < JB; ++t)        // compile-time register index
-                    if (t == jj)
+                for (int t = 0; t < PT_SLOTS; ++t)
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) acc[t][4 * h + q] = make_float2(v[2 * q], v[2 * q + 1]);
-            }
-            tc_fence_before();
-            mbar_arrive(&tempty[slot]);
-            const int j = ja + i;
-            if (jj == JB - 1 || i == n_stages - 1) {
-                const int cnt = jj + 1;
+                    for (int e = 0; e < 4; ++e)
+                        v[t][e] = HL == 2 ? __uint_as_float(r[t][e]) + __uint_as_float(r2[t][e]) : __uint_as_float(r[t][e]);
                 if (b < B) {
-                    const bool vec = cnt == 2 && ((((size_t)b * N_d + jfirst) & 1) == 0) && ((N_d & 1) == 0);
 #pragma unroll
-                    for (int q = 0; q < NPW; ++q) {
-                        const long long n = n0 + nb + q;
+                    for (int h = 0; h < 2; ++h) {             // v[t][2h], v[t][2h+1] = Re, Im X[nl + h][b][jfirst + t]
+                        const long long n = n0 + nl + h;
                         if (n >= g.n_sym) break;
                         float2* dst = X + ((size_t)n * B + b) * N_d + jfirst;
                         if (vec) {
-                            *reinterpret_cast<float4*>(dst) = make_float4(acc[0][q].x, acc[0][q].y, acc[1][q].x,
-                                                                          acc[1][q].y);
+                            reinterpret_cast<float4*>(dst)[0] = make_float4(v[0][2 * h], v[0][2 * h + 1], v[1][2 * h], v[1][2 * h + 1]);
+                            reinterpret_cast<float4*>(dst)[1] = make_float4(v[2][2 * h], v[2][2 * h + 1], v[3][2 * h], v[3][2 * h + 1]);
                         } else {
 #pragma unroll
-                            for (int t = 0; t < JB; ++t)
-                                if (t < cnt) dst[t] = acc[t][q];
+                            for (int t = 0; t < PT_SLOTS; ++t)
+                                if (t < cnt) dst[t] = make_float2(v[t][2 * h], v[t][2 * h + 1]);
                         }
                     }
                 }
-                jfirst = j + 1;
             }
+            tc_fence_before();
+            mbar_arrive(&tempty[0]);
         }
     }
     __syncthreads();
@@ -374,10 +383,11 @@ static int launch_precode_tc(const void* P, bool packed, const void* s, void* X,
     const long long ntiles = (n_sym + NT - 1) / NT;
     FD_REQUIRE(ntiles * g.n_btiles < 65536, "precode (tensor cores): batch too large");
     g.n_ntiles = (int)ntiles;
-    // one wave of persistent CTAs (one per SM: ~200 KB of stages, 512 TMEM columns); subcarrier ranges in multiples of the epilogue's 2-subcarrier runs
-    const int pairs = (N_d + 1) / 2;
-    int jg = std::max(1, (int)std::min<long long>(pairs, (148LL + g.n_btiles * ntiles - 1) / (g.n_btiles * ntiles)));
-    g.jper = 2 * ((pairs + jg - 1) / jg);
+    // one wave of persistent CTAs (one per SM: ~200 KB of stages, 512 TMEM columns); subcarrier
+    // ranges in multiples of the epilogue's 4-subcarrier quads
+    const int quads = (N_d + 3) / 4;
+    int jg = std::max(1, (int)std::min<long long>(quads, (148LL + g.n_btiles * ntiles - 1) / (g.n_btiles * ntiles)));
+    g.jper = 4 * ((quads + jg - 1) / jg);
     g.n_jgroups = (N_d + g.jper - 1) / g.jper;
     const size_t smem = (size_t)g.ns * g.stage_bytes + bar_bytes;
     const unsigned grid = (unsigned)(g.n_jgroups * g.n_btiles * ntiles);

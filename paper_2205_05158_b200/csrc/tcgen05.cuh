@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -22,6 +23,19 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
 __host__ __device__ constexpr uint32_t idesc_tf32_m128(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+// Instruction descriptor: D f32, A/B f16, both K-major, M = 128, N = n (K = 16 per MMA).
+__host__ __device__ constexpr uint32_t idesc_f16_m128(int n) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -71,6 +85,16 @@ __device__ __forceinline__ bool elect_one() {
         "elect.sync _|P1, 0xffffffff;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}" : "=r"(pred));
     return pred != 0;
+}
+
+// x -> (hi, lo) fp16 with x ~= hi + lo (22 significant bits; the caller pre-scales x into the
+// fp16 normal range), packed in pairs: (hi(a), hi(b)) and (lo(a), lo(b))
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 // fp32 -> tf32 (round to nearest, ties away), kept in an fp32 container

@@ -76,3 +76,107 @@ def allreduce_partial(partial: torch.Tensor, group=None) -> torch.Tensor:
         t = torch.view_as_real(partial) if partial.is_complex() else partial
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return partial
+
+
+# ============================================================================ Mode A step
+def _staged(t: torch.Tensor, host_staged: bool):
+    """The tensor a collective runs on: a real view (complex -> [..., 2]); with host staging
+    (gloo on CUDA tensors) a CPU copy that the caller copies back."""
+    r = torch.view_as_real(t) if t.is_complex() else t
+    return r.cpu() if host_staged else r
+
+
+def all_gather_into(out: torch.Tensor, local: torch.Tensor, group=None, host_staged=False, async_op=False):
+    """Mode A: rank blocks of the symbol-sharded s_tilde concatenated in rank order into the
+    preallocated out [world * n_loc][U][N_d] (torch.distributed.all_gather_into_tensor)."""
+    if world()[0] == 1:
+        out.copy_(local)
+        return None
+    if host_staged:
+        o = _staged(out, True)
+        dist.all_gather_into_tensor(o, _staged(local, True), group=group)
+        out.copy_(torch.view_as_complex(o) if out.is_complex() else o)
+        return None
+    return dist.all_gather_into_tensor(_staged(out, False), _staged(local, False), group=group, async_op=async_op)
+
+
+def reduce_scatter_into(mine: torch.Tensor, partial: torch.Tensor, group=None, host_staged=False, async_op=False):
+    """Mode A: sum the per-rank partial received signals (Eq. 5's sum over antennas)
+    and leave rank r the r-th symbol block (its own symbols) in mine [n_loc][U][N_d]
+    (torch.distributed.reduce_scatter_tensor, SUM)."""
+    if world()[0] == 1:
+        mine.copy_(partial)
+        return None
+    if host_staged:
+        m = _staged(mine, True)
+        dist.reduce_scatter_tensor(m, _staged(partial, True), op=dist.ReduceOp.SUM, group=group)
+        mine.copy_(torch.view_as_complex(m) if mine.is_complex() else m)
+        return None
+    return dist.reduce_scatter_tensor(_staged(mine, False), _staged(partial, False), op=dist.ReduceOp.SUM,
+                                      group=group, async_op=async_op)
+
+
+class AntennaShardedStep:
+    """Mode A (BASELINE configs[4] "sharded by antenna ... allreduce of per-UE
+    received subcarrier signals"), one step over a batch of world x n_per_rank symbols:
+
+      1. FD-CNN on this rank's n_per_rank symbols (the CNN does not depend on the antennas);
+      2. all_gather_into_tensor of s_tilde -> every rank holds the whole batch;
+      3. precode -> IDFT -> GMP -> receive DFT on this rank's antenna rows [b0, b0 + B_loc);
+      4. partial channel sum over the local antennas (ue_combine);
+      5. reduce_scatter_tensor (SUM) of the partial received signals: rank r gets the full
+         y_hat of its own symbols (the sum over antennas of Eq. 5, split by symbol blocks);
+      6. slicing + SER counters on the rank's symbols, int64 counters all-reduced.
+
+    The batch is cut into `micro` micro-batches: with NCCL the collectives of micro-batch k are
+    issued asynchronously and waited on just before their consumer, so the all-gather of k
+    overlaps the FD-CNN of k + 1 and the reduce-scatter of k the chain of k + 1.
+
+    `ops` supplies the per-rank compute (the CUDA kernels on GPUs; the fp64 oracle in the CPU
+    gloo tests): dpd(s, out), tx(st_all, XPA_out), combine(XPA, out), slice(yhat, idx, counts).
+    `alloc(shape)` allocates a complex buffer on the compute device.  host_staged: gloo on CUDA
+    tensors (collectives through host copies; used by the single-GPU 2-rank validation)."""
+
+    def __init__(self, ops, n_per_rank, U, N_d, alloc, micro=2, group=None, host_staged=False):
+        self.ops, self.group, self.host_staged = ops, group, host_staged
+        ws, _ = world()
+        self.ws = ws
+        self.micro = micro if (micro > 1 and n_per_rank % micro == 0) else 1
+        self.nm = n_per_rank // self.micro
+        self.n = n_per_rank
+        self.st = [alloc((self.nm, U, N_d)) for _ in range(self.micro)]
+        self.st_all = [alloc((ws * self.nm, U, N_d)) for _ in range(self.micro)]
+        self.xpa = [None] * self.micro
+        self.part = [alloc((ws * self.nm, U, N_d)) for _ in range(self.micro)]
+        self.mine = [alloc((self.nm, U, N_d)) for _ in range(self.micro)]
+        self.alloc = alloc
+
+    def step(self, s, idx, counts):
+        """s, idx: this rank's n_per_rank symbols; counts (int64[3]) receives the all-reduced
+        errors / total / near-boundary of the whole world batch.  Returns the list of the
+        micro-batches' y_hat (this rank's symbols)."""
+        nm, M = self.nm, self.micro
+        asy = not self.host_staged and self.ws > 1
+        ag = [None] * M
+        for k in range(M):                                   # CNN + async all-gather
+            self.ops.dpd(s[k * nm:(k + 1) * nm], self.st[k])
+            ag[k] = all_gather_into(self.st_all[k], self.st[k], self.group, self.host_staged, async_op=asy)
+        rs = [None] * M
+        for k in range(M):                                   # local antennas + async reduce-scatter
+            if ag[k] is not None:
+                ag[k].wait()
+            self.xpa[k] = self.ops.tx(self.st_all[k], self.xpa[k])
+            self.ops.combine(self.xpa[k], self.part[k])
+            rs[k] = reduce_scatter_into(self.mine[k], self.part[k], self.group, self.host_staged, async_op=asy)
+        for k in range(M):                                   # slicing on this rank's symbols
+            if rs[k] is not None:
+                rs[k].wait()
+            self.ops.slice(self.mine[k], idx[k * nm:(k + 1) * nm], counts)
+        if self.ws > 1:
+            if self.host_staged:
+                c = counts.cpu()
+                dist.all_reduce(c, op=dist.ReduceOp.SUM, group=self.group)
+                counts.copy_(c)
+            else:
+                dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=self.group)
+        return self.mine

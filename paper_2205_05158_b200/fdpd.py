@@ -48,6 +48,7 @@ SIGNATURES = {
     "fd_version": (_i, []),
     "fd_shutdown": (None, []),
     "fd_set_cnn_path": (_i, [_i]),
+    "fd_set_cnn_tc_precision": (_i, [_i]),
     "fd_set_chain_split": (_i, [_i]),
     "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
     "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
@@ -150,6 +151,11 @@ CNN_AUTO, CNN_SIMT, CNN_TENSOR = 0, 1, 2
 # FD_SPLIT_PRECODE_MIN_U of include/fdpd.h: from this many users the chain runs precode ->
 # chain_txrx_pre instead of the fused-prologue chain_txrx (same policy as the native runtime)
 SPLIT_PRECODE_MIN_U = 16
+
+
+def set_cnn_tc_precision(mode: int):
+    """0 = FP16 split (default), 1 = TF32 split for the tensor-core hidden layers."""
+    _check(lib().fd_set_cnn_tc_precision(int(mode)))
 
 
 def set_cnn_path(path: int):

@@ -22,6 +22,31 @@ def _free_port():
         return s.getsockname()[1]
 
 
+class OracleAntennaOps:
+    """The per-rank compute of dist.AntennaShardedStep on the fp64 oracle (CPU test stand-in for
+    chain.AntennaOps): this rank's antenna rows [b0, b0 + B_loc) of P, Hfd and the PA."""
+
+    def __init__(self, cfg, inp, b0, B_loc):
+        self.cfg, self.inp, self.b0, self.B_loc = cfg, inp, b0, B_loc
+        self.Hfd = O.channel_fd(inp["h_taps"], cfg.N_ifft, cfg.N_d)
+        self.P, self.alpha, _ = O.zf_precoder(self.Hfd, cfg.N_ifft, cfg.rho)
+
+    def dpd(self, s, out):
+        out.copy_(torch.from_numpy(O.fdcnn_forward(s.numpy(), self.inp["params"], self.cfg.chans, self.cfg.N_d)))
+
+    def tx(self, st_all, XPA=None):
+        cfg, sl = self.cfg, slice(self.b0, self.b0 + self.B_loc)
+        X = O.precode(self.P[:, sl, :], st_all.numpy())
+        return O.gmp_pa(O.ofdm_modulate(X, cfg.N_ifft), self.inp["coef"][sl], cfg.orders, cfg.L, cfg.M)
+
+    def combine(self, y, out):
+        out.copy_(torch.from_numpy(O.ue_receive(y, self.Hfd[:, :, self.b0:self.b0 + self.B_loc], self.cfg.N_d)))
+
+    def slice(self, yhat, idx, counts):
+        _, c = O.slice_ser(yhat.numpy(), self.alpha, idx.numpy(), self.cfg.M_qam)
+        counts += torch.from_numpy(c)
+
+
 def _worker(rank, world, port, mode, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -29,7 +54,19 @@ def _worker(rank, world, port, mode, q):
     from paper_2205_05158_b200 import dist as D
     try:
         cfg = configs.C1
-        if mode == "S":
+        if mode == "A_step":
+            per = 4
+            syms = D.symbol_range(per, rank)
+            inp_all = gen.make_inputs(cfg, range(per * world))
+            inp = gen.make_inputs(cfg, syms)
+            b0, B_loc = D.antenna_shard(cfg.B, world, rank)
+            ops = OracleAntennaOps(cfg, inp_all, b0, B_loc)
+            step = D.AntennaShardedStep(ops, per, cfg.U, cfg.N_d,
+                                        alloc=lambda sh: torch.zeros(sh, dtype=torch.complex128), micro=2)
+            counts = torch.zeros(3, dtype=torch.int64)
+            mine = step.step(torch.from_numpy(inp["s"].astype(np.complex128)), torch.from_numpy(inp["idx"]), counts)
+            q.put((rank, (np.concatenate([m.numpy() for m in mine]), counts.numpy())))
+        elif mode == "S":
             per = 3
             inp = gen.make_inputs(cfg, D.symbol_range(per, rank))
             out = O.run_config(cfg, inp)
@@ -84,6 +121,20 @@ def test_antenna_mode_allgather_and_partial_sum():
         st, yhat = res[r]
         assert np.max(np.abs(st - full["s_tilde"])) < 1e-12
         assert np.max(np.abs(yhat - full["yhat"])) < 1e-12 * max(1.0, np.max(np.abs(full["yhat"])))
+
+
+def test_antenna_sharded_step_matches_unsharded():
+    """dist.AntennaShardedStep (Mode A, two micro-batches) over 2 gloo ranks: all_gather_into_tensor of
+    s_tilde, local antennas, reduce_scatter_tensor of the partial received signals, counter all-reduce.
+    Each rank's y_hat (its own symbols) and the world counters equal the unsharded oracle."""
+    res = _run("A_step")
+    cfg = configs.C1
+    full = O.run_config(cfg, gen.make_inputs(cfg, range(8)))
+    for r in (0, 1):
+        yhat, counts = res[r]
+        want = full["yhat"][4 * r:4 * r + 4]
+        assert np.max(np.abs(yhat - want)) < 1e-12 * max(1.0, np.max(np.abs(want)))
+        assert np.array_equal(counts, full["counts"])
 
 
 def test_split_covers_everything():

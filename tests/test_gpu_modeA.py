@@ -1,0 +1,41 @@
+"""Mode A (antenna sharding; BASELINE configs[4]) on the CUDA path, validated on
+one GPU: two torchrun ranks on cuda:0 with gloo host-staged collectives (tools/modeA_check.py).
+Each rank's y_hat must match the single-GPU all-antenna step within 1e-6 relative L2 (only the
+order of the antenna sum differs), and the world SER counters must agree (errors within the
+near-boundary band)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("cfg,per,math", [("C2", 4, "simt"), ("C2", 4, "fp32tc"), ("C5", 2, "fp32tc"),
+                                          ("C4", 3, "fp32tc")])
+def test_mode_a_two_ranks_one_gpu(cfg, per, math, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tools", "modeA_check.py"), cfg, str(per), math]
+    env = dict(os.environ, MODEA_OUT=str(tmp_path / "modeA"))
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(open(tmp_path / f"modeA.{r}.json").read()) for r in range(2)]
+    for d in lines:
+        assert d["yhat_rel_l2_vs_1rank"] < 1e-6, d
+        a, b = d["counts_modeA"], d["counts_1rank"]
+        assert a[1] == b[1] == 2 * per * {"C2": 4 * 600, "C4": 16 * 3300, "C5": 32 * 3300}[cfg]
+        assert abs(a[0] - b[0]) <= max(a[2], b[2]), d

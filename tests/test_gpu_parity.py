@@ -249,13 +249,14 @@ def test_combine_ser_ragged(F, n, B, U, Nd):
     assert rel(host(yhat), want) < TOL
     assert rel(host(F.ue_combine(dev(XPA), dev(h))), want) < TOL
     dec_o, c_o = O.slice_ser(want, alpha, idx, M_qam)
-    near = np.zeros(want.shape, bool)
-    _, cn = O.slice_ser(want, alpha, idx, M_qam)
-    mism = host(dec).astype(np.int64) != dec_o.astype(np.int64)
+    _, near = _near_mask(want, alpha, M_qam)
+    dg = host(dec)
+    assert np.array_equal(dg[~near], dec_o[~near])          # element by element outside the 1e-4 band
     c = host(counts)
     assert c[1] == n * U * Nd
-    assert mism.sum() <= cn[2] + c[2]
-    assert abs(int(c[0]) - int(c_o[0])) <= cn[2] + c[2]
+    err_gpu = int((dg != idx).sum())
+    assert c[0] == err_gpu
+    assert abs(err_gpu - int(c_o[0])) <= int(near.sum())
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
@@ -483,30 +484,57 @@ def test_end_to_end(F, name, fused):
     _, near = _near_mask(o["yhat"], o["alpha"], cfg.M_qam)
     assert np.array_equal(dec[pick][~near], o["dec"][~near])
     assert counts[1] == cfg.n_sym * cfg.U * cfg.N_d
-    if cfg.n_sym <= 4:
-        assert abs(int(counts[0]) - int(o["counts"][0])) <= int(near.sum())
+    err_g = int((dec[pick] != inp["idx"][pick]).sum())          # SER errors of the compared symbols
+    assert abs(err_g - int(o["counts"][0])) <= int(near.sum())
+    assert counts[0] == int((dec != inp["idx"]).sum())
 
 
-@pytest.mark.parametrize("name,nsym,pick", [("C3", 8, 5), ("C4", 8, 5), ("C5", 8, 5), ("C3", 512, 509),
-                                           ("C4", 128, 125), ("C5", 32, 29)])
+def _decision_report(name, dec_g, o, eps_band):
+    """Decision parity at the north star's fixed 1e-4 band and at the A25 band: every decision
+    outside the A25 band is identical; the raw north-star mismatches (outside 1e-4) are
+    printed with their boundary distances and must all lie inside the A25 band."""
+    cfg = configs.get(name)
+    z, near4 = _near_mask(o["yhat"], o["alpha"], cfg.M_qam, 1e-4)
+    _, near_b = _near_mask(o["yhat"], o["alpha"], cfg.M_qam, eps_band)
+    mism = dec_g != o["dec"]
+    raw = mism & ~near4
+    cst = 1.0 / np.sqrt(2.0 * (cfg.M_qam - 1) / 3.0)
+    dist = []
+    for i in np.argwhere(raw):
+        zz = z[tuple(i)]
+        d = min(abs(v / cst - 2.0 * np.round(v / cst / 2.0)) * cst for v in (zz.real, zz.imag))
+        dist.append(float(d))
+    print(f"{name}: decisions {mism.size}, mismatches {int(mism.sum())}, outside the north-star 1e-4 band "
+          f"{int(raw.sum())} (boundary distances {sorted(dist)[:8]}), A25 band {eps_band:.3g}")
+    assert not (mism & ~near_b).any()
+    assert int(raw.sum()) <= max(2, mism.size // 10000)
+
+
+@pytest.mark.parametrize("name,nsym,pick", [("C3", 8, [5]), ("C4", 8, [5]), ("C5", 8, [5]), ("C3", 512, [0, 509]),
+                                           ("C4", 128, [0, 125]), ("C5", 32, [3, 29])])
 def test_end_to_end_large(F, name, nsym, pick):
     """The large configurations through the whole step on their own paths: tensor-core CNN
-    with the FP32 last layer, the tiled precode + chain_txrx_pre (U >= 16), the N = 8192
+    with the FP32 last layer, the precode + chain_txrx_pre (U >= 16), the N = 8192
     256-thread / N = 16384 cluster-split chain, the staged-tile channel sum.  Small batches
-    and the bench's batches (C3 512, C4 128, C5 32 symbols per step); one symbol of the batch
-    (in the last 8-symbol tile for the bench batches) against the oracle."""
+    and the bench's batches (C3 512, C4 128, C5 32 symbols per step); one or two symbols of
+    the batch (one in the last 8-symbol tile) against the oracle: every stage output at 2e-5,
+    decisions (north-star band and A25 band, _decision_report) and the SER error count of the
+    compared symbols."""
     cfg = configs.get(name)
     inp = gen.make_inputs(cfg, range(nsym))
     ch, st, y, yhat, counts, dec = _gpu_chain(F, cfg, inp)
-    pick = [pick]
     o = O.run_config(cfg, gen.make_inputs(cfg, pick))
     assert abs(ch.alpha / o["alpha"] - 1) < 1e-6
     assert rel(st[pick], o["s_tilde"]) < TOL
     assert rel(y[pick], o["y"]) < TOL
     assert rel(yhat[pick], o["yhat"]) < TOL
-    _, near = _near_mask(o["yhat"], o["alpha"], cfg.M_qam, _decision_eps(o["yhat"], o["alpha"]))
-    assert np.array_equal(dec[pick][~near], o["dec"][~near])
+    eps_band = _decision_eps(o["yhat"], o["alpha"])
+    _decision_report(name, dec[pick], o, eps_band)
+    _, near_b = _near_mask(o["yhat"], o["alpha"], cfg.M_qam, eps_band)
+    err_g = int((dec[pick] != inp["idx"][pick]).sum())
+    assert abs(err_g - int(o["counts"][0])) <= int(near_b.sum())
     assert counts[1] == nsym * cfg.U * cfg.N_d
+    assert counts[0] == int((dec != inp["idx"]).sum())
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "P"])

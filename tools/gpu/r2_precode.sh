@@ -1,0 +1,5 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_precode_tc.py -x -q 2>&1 | tail -15 > gpurun_out/r2_precode_tests.log
+STAGES=precode,precode_fp32tc,precode_tf32 timeout 300 python tools/stage_bench.py C5 32 10 > gpurun_out/r2_stage_precode_c5.json 2>&1
+STAGES=precode,precode_fp32tc,precode_tf32 timeout 300 python tools/stage_bench.py C3 512 10 > gpurun_out/r2_stage_precode_c3.json 2>&1
+STAGES=precode,precode_fp32tc,precode_tf32 timeout 300 python tools/stage_bench.py C4 128 10 > gpurun_out/r2_stage_precode_c4.json 2>&1

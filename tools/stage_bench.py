@@ -36,6 +36,7 @@ def main():
     params = torch.from_numpy(inp["params"]).to(dev)
     B, U, N, Nd = cfg.B, cfg.U, cfg.N_ifft, cfg.N_d
     X = fdpd.precode(P, s)
+    Ppk = fdpd.precode_pack(P) if U % 4 == 0 and U <= 32 else None
     x = fdpd.ofdm_modulate(X, N)
     y = fdpd.gmp_pa(x, coef, cfg.orders, cfg.L, cfg.M)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -62,13 +63,20 @@ def main():
                           2 * 9 * sum(a * b for a, b in zip(cfg.chans[:-1], cfg.chans[1:])) *
                           int(np.ceil(np.sqrt(Nd))) ** 2 * U * n),
         "precode": (lambda: fdpd.precode(P, s, out=X), c8 * (B * U * Nd + n * U * Nd + n * B * Nd), 8 * B * U * Nd * n),
+        "precode_fp32tc": (lambda: fdpd.precode_packed(Ppk, s, out=X, math=fdpd.MATH_FP32_TC),
+                           c8 * (B * U * Nd + n * U * Nd + n * B * Nd), 8 * B * U * Nd * n),
+        "precode_tf32": (lambda: fdpd.precode_packed(Ppk, s, out=X, math=fdpd.MATH_TF32),
+                         c8 * (B * U * Nd + n * U * Nd + n * B * Nd), 8 * B * U * Nd * n),
         "ofdm_modulate": (lambda: fdpd.ofdm_modulate(X, N, out=x), c8 * n * B * (Nd + N), 5 * N * np.log2(N) * B * n),
         "gmp_pa": (lambda: fdpd.gmp_pa(x, coef, cfg.orders, cfg.L, cfg.M, out=y), c8 * 2 * n * B * N, gmp_c * N * B * n),
         "ue_receive_ser": (lambda: fdpd.ue_receive_ser(y, h_fd, alpha, idx, cfg.M_qam),
                            c8 * (n * B * N + U * B * Nd + n * U * Nd) + 2 * n * U * Nd,
                            (5 * N * np.log2(N) + 8 * U * Nd) * B * n),
     }
+    only = os.environ.get("STAGES")
     for k, (fn, nbytes, flops) in stages.items():
+        if (only and k not in only.split(",")) or (Ppk is None and "tc" in k or Ppk is None and "tf32" in k):
+            continue
         ms = timed(fn)
         gbs = nbytes / (ms * 1e-3) / 1e9
         tfs = flops / (ms * 1e-3) / 1e12
