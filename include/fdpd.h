@@ -284,6 +284,12 @@ int ue_slice_ser(const void* yhat, float alpha, const uint16_t* tx_idx, int M_qa
  *   yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j];  n_sym <= 65535 per call. */
 int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, int B_loc, int U, int N_d,
                int accumulate, cudaStream_t stream);
+/* Channel-sum implementation (process-wide): 0 = auto (default) — for 9 <= U <= 32 (and no
+ * AWGN, one channel realisation, 16-byte aligned yhat) the sum runs on the tensor cores
+ * (tcgen05 kind::tf32, per-subcarrier real GEMM with K = 2 B_loc, FP32-accurate hi/lo split on
+ * both operands, four products), else the FP32 SIMT kernels; 1 = always FP32 SIMT.
+ * FD_ERR_ARG for other modes. */
+int fd_set_combine_path(int mode);
 /* ue_combine (accumulate = 0) fused with ue_slice_ser. */
 int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
                    uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d,

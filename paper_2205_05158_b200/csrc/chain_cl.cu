@@ -106,7 +106,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
             for (int r = 0; r < 16; ++r) usm[pidx(16 * j + r)] = X[r];
         }
         __syncthreads();
-        fft_run<LOG2NL, +1, 1>(usm, v, tw_l, tid);
+        fft_run<LOG2NL, +1, 1>(usm, v, tw_l, tid, reinterpret_cast<float2*>(esm));   // xs (in esm) is dead after pass 0
     } else {
         constexpr int R0 = pass_radix<LOG2NL>(0);
 #pragma unroll
@@ -163,7 +163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
                 v[q * R0 + r] = c ? cmul(csub(y0, y1), __ldg(tw_g + pos)) : cadd(y0, y1);
             }
     }
-    fft_run<LOG2NL, -1>(usm, v, tw_l, tid);
+    fft_run<LOG2NL, -1>(usm, v, tw_l, tid, reinterpret_cast<float2*>(esm));       // e (esm) is dead after the GMP
     float2* xo = XPA + nb * N_d + c;
     for (int jl = tid; jl < NdL; jl += T) xo[2 * jl] = cscale(usm[pidx(data_to_bin(jl, NL, NdL))], sc);
 }

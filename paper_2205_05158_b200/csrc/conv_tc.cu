@@ -133,8 +133,13 @@ struct TcRoles {
     static constexpr int LOAD_THREADS = 32 * LOAD, EPI_THREADS = 32 * EPI;
 };
 
+// K chunk = 32 input channels for both precisions: with the fp16 split a 64-channel layer's
+// 9 taps x 2 chunks of weights (144 KB) stay resident in shared memory next to two 33 KB A
+// chunks (measured: streaming the weight slices from L2 every tile bound the 64 -> 64 layer,
+// tensor pipe 35 % busy); with the TF32 split (288 KB) they are streamed through a ring.
 __host__ __device__ constexpr int tc_ck(int cinp, bool f16) {
-    return f16 ? (cinp >= 64 ? 64 : cinp) : (cinp >= 32 ? 32 : cinp);
+    (void)f16;
+    return cinp >= 32 ? 32 : cinp;
 }
 
 template <int CINP, int NP, int IN_MODE, int OUT_MODE, bool F16>

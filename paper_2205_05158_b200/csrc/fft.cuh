@@ -189,11 +189,11 @@ __host__ __device__ constexpr int tw_table_len(int N) {
     return len;
 }
 
-template <int R, int DIR, int VPT, int T, int N, int TWOFF = 0>
+template <int R, int DIR, int VPT, int T, int N, int TWOFF = 0, int Q0 = 0, int Q1 = VPT / R>
 __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT], int Ns, const float2* __restrict__ tw,
                                                    int tid) {
 #pragma unroll
-    for (int q = 0; q < VPT / R; ++q) {
+    for (int q = Q0; q < Q1; ++q) {
         const int j = tid + q * T;
         const int k = j & (Ns - 1);
         if (R == 16 && TWOFF > 0 && Ns > 1) pass_twiddle_tab16<DIR>(v, q * R, k, Ns, tw + TWOFF);
@@ -209,21 +209,57 @@ __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT],
 // layout (pass_pos with R = pass_radix(0)); P > 0: reading the previous pass from sm.
 // With PEND = n_passes the transform (unnormalised) is left in sm in natural order.
 // Ends with __syncthreads().
+//
+// scr (optional, T x VPT/2 complex of free shared memory): a pass reads all of its inputs before
+// the barrier that precedes its in-place writes, so VPT complex values per thread are live across
+// that barrier — 64 registers at VPT = 32 (N = 8192 over 256 threads), which spilled the
+// 128-register chain kernel.  With scr the second half of the inputs is parked in shared memory
+// (thread-private slots [i][tid], conflict-free) and reloaded after the first half's butterflies.
 template <int LOG2N, int DIR, int P = 0, int PEND = n_passes<LOG2N>()>
 __device__ __forceinline__ void fft_run(float2* sm, float2 (&v)[(1 << LOG2N) / fft_threads<LOG2N>()],
-                                        const float2* __restrict__ tw, int tid) {
+                                        const float2* __restrict__ tw, int tid, float2* scr = nullptr) {
     constexpr int N = 1 << LOG2N;
     constexpr int T = fft_threads<LOG2N>();
     constexpr int VPT = N / T;
     constexpr int R = pass_radix<LOG2N>(P);
+    constexpr int QN = VPT / R;
+    constexpr int TWOFF = (R == 16 && P > 0) ? tw_pass_off(N, P) : 0;
+    if constexpr (P > 0 && QN >= 2 && QN % 2 == 0) {
+        if (scr != nullptr) {
+            constexpr int H = VPT / 2;
+            // second half: straight from the pass buffer into the parking slots (8 in flight),
+            // then the first half into registers
+#pragma unroll
+            for (int c0 = H; c0 < VPT; c0 += 8) {
+                float2 t[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int x = c0 + e;
+                    t[e] = sm[pidx(pass_pos<R, VPT, T, N>(tid, x / R, x % R))];
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) scr[(c0 + e - H) * T + tid] = t[e];
+                asm volatile("" ::: "memory");
+            }
+#pragma unroll
+            for (int x = 0; x < H; ++x) v[x] = sm[pidx(pass_pos<R, VPT, T, N>(tid, x / R, x % R))];
+            __syncthreads();
+            pass_compute_store<R, DIR, VPT, T, N, TWOFF, 0, QN / 2>(sm, v, pass_ns<LOG2N>(P), tw, tid);
+#pragma unroll
+            for (int i = 0; i < H; ++i) v[H + i] = scr[i * T + tid];
+            pass_compute_store<R, DIR, VPT, T, N, TWOFF, QN / 2, QN>(sm, v, pass_ns<LOG2N>(P), tw, tid);
+            __syncthreads();
+            if constexpr (P + 1 < PEND) fft_run<LOG2N, DIR, P + 1, PEND>(sm, v, tw, tid, scr);
+            return;
+        }
+    }
     if constexpr (P > 0) {
         pass_load_smem<R, VPT, T, N>(sm, v, tid);
         __syncthreads();
     }
-    constexpr int TWOFF = (R == 16 && P > 0) ? tw_pass_off(N, P) : 0;
     pass_compute_store<R, DIR, VPT, T, N, TWOFF>(sm, v, pass_ns<LOG2N>(P), tw, tid);
     __syncthreads();
-    if constexpr (P + 1 < PEND) fft_run<LOG2N, DIR, P + 1, PEND>(sm, v, tw, tid);
+    if constexpr (P + 1 < PEND) fft_run<LOG2N, DIR, P + 1, PEND>(sm, v, tw, tid, scr);
 }
 
 // ---------------------------------------------------------------- pruned radix-16 passes

@@ -43,7 +43,7 @@ constexpr int PT_MMA_WARP = PT_EPI + PT_PROD;
 constexpr int PT_THREADS = 32 * (PT_MMA_WARP + 1);
 constexpr int PT_ROWS = 128;                 // rows of every operand plane (M = 128, N = 128)
 constexpr int PT_PLANE = (PT_ROWS + 1) * 16; // bytes per 16-byte K chunk (4 tf32) plane, +1 row: conflict-free stores
-constexpr int PT_SLOTS = 4, PT_COLS = 128;   // TMEM accumulator ring
+constexpr int PT_SLOTS = 4, PT_COLS = 64;    // subcarriers per TMEM quad, columns per subcarrier (N = 64)
 
 struct PtGeom {
     int U, B, N_d;
@@ -88,7 +88,7 @@ __device__ __forceinline__ float4 rna4(float4 x) {
 template <int HL, bool PACKED>
 __global__ void __launch_bounds__(PT_THREADS, 1)
     k_precode_tc(const float* __restrict__ P, const float2* __restrict__ s, float2* __restrict__ X, PtGeom g) {
-    constexpr int NT = 64 / HL;              // symbols per tile (Bs rows = HL * 2 NT = 128)
+    constexpr int NT = 32;                   // symbols per tile (Bs rows 2 NT per hi / lo half)
     constexpr int NPW = NT / (PT_EPI / 4);   // symbols per epilogue warp column group
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -96,21 +96,21 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)g.ns * g.stage_bytes);
     uint64_t* full = bars;                   // [ns]
     uint64_t* empty = bars + g.ns;           // [ns]
-    uint64_t* tfull = empty + g.ns;          // [4]
-    uint64_t* tempty = tfull + PT_SLOTS;     // [4]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + PT_SLOTS);
+    uint64_t* tfull = empty + g.ns;          // [2] quad buffers
+    uint64_t* tempty = tfull + 2;            // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     if (tid == 0) {
         for (int i = 0; i < g.ns; ++i) {
             mbar_init(&full[i], 32 * PT_PROD);
             mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < PT_SLOTS; ++i) {
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 32 * PT_EPI);
         }
     }
-    if (warp == 0) tmem_alloc(tmem_slot, PT_SLOTS * PT_COLS);
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -144,28 +144,37 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
             float2 pv[MAXA][PA];
             float2 sv[4];
         };
+        // per-thread item geometry, fixed over the stages (no integer divisions in the loop)
+        constexpr int QSTEP = 32 * PT_PROD;  // item stride between a thread's items
+        const int Q = PACKED ? KQ : UQ;      // quads per operand row
+        int a_row[MAXA];                     // operand row r of item t (< 0: no item); its quad is
+#pragma unroll                               //   it - r Q (a multiply, no division in the loop)
+        for (int t = 0; t < MAXA; ++t) {
+            const int it = pt + t * QSTEP;
+            a_row[t] = it < na ? it / Q : -1;
+        }
+        auto a_quad = [&](int t) { return pt + t * QSTEP - a_row[t] * Q; };
+        const bool s_item = pt < ns_items;
+        const int s_u = s_item ? pt % UQ : 0, s_n = s_item ? pt / UQ : 0;
+        const bool s_ok = s_item && n0 + s_n < g.n_sym;
+        const float2* s_src = s + ((size_t)(n0 + (s_ok ? s_n : 0)) * U + 4 * s_u) * N_d;
         auto load = [&](int j, Regs& R) {
 #pragma unroll
             for (int t = 0; t < MAXA; ++t) {
-                const int it = pt + t * 32 * PT_PROD;
-                if (it >= na) break;
+                const int r = a_row[t];
+                if (r < 0) break;
+                const bool ok = b0 + r < B;
                 if constexpr (PACKED) {
-                    const int kq = it % KQ, r = it / KQ;
-                    R.av[t] = (b0 + r < B) ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)j * B + b0 + r) * 2 * U) + kq)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                    R.av[t] = ok ? __ldg(reinterpret_cast<const float4*>(P + ((size_t)j * B + b0 + r) * 2 * U) + a_quad(t))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
                 } else {
-                    const int uq = it % UQ, r = it / UQ;
-                    const float2* src = reinterpret_cast<const float2*>(P) + ((size_t)(b0 + r) * U + 4 * uq) * N_d + j;
+                    const float2* src = reinterpret_cast<const float2*>(P) + ((size_t)(b0 + r) * U + 4 * a_quad(t)) * N_d + j;
 #pragma unroll
-                    for (int q = 0; q < PA; ++q)
-                        R.pv[t][q] = (b0 + r < B) ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
+                    for (int q = 0; q < PA; ++q) R.pv[t][q] = ok ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
                 }
             }
-            const int su = pt % UQ, sn = pt / UQ;
-            const bool ok = pt < ns_items && n0 + sn < g.n_sym;
-            const float2* src = s + ((size_t)(n0 + sn) * U + 4 * su) * N_d + j;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) R.sv[q] = ok ? __ldg(src + (size_t)q * N_d) : make_float2(0.f, 0.f);
+            for (int q = 0; q < 4; ++q) R.sv[q] = s_ok ? __ldg(s_src + (size_t)q * N_d + j) : make_float2(0.f, 0.f);
         };
         auto store = [&](unsigned char* st, const Regs& R) {
             unsigned char* a_hi = st;
@@ -173,11 +182,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
             unsigned char* bs = st + (HL == 2 ? 2 : 1) * plane_set;
 #pragma unroll
             for (int t = 0; t < MAXA; ++t) {
-                const int it = pt + t * 32 * PT_PROD;
-                if (it >= na) break;
+                const int r = a_row[t];
+                if (r < 0) break;
                 if constexpr (PACKED) {
-                    const int kq = it % KQ, r = it / KQ;
-                    const size_t off = (size_t)kq * PT_PLANE + r * 16;
+                    const size_t off = (size_t)a_quad(t) * PT_PLANE + r * 16;
                     if constexpr (HL == 2) {
                         float4 hi, lo;
                         split4(R.av[t], hi, lo);
@@ -187,10 +195,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                         *reinterpret_cast<float4*>(a_hi + off) = rna4(R.av[t]);
                     }
                 } else {
-                    const int uq = it % UQ, r = it / UQ;
                     const float4 re = make_float4(R.pv[t][0].x, R.pv[t][1].x, R.pv[t][2].x, R.pv[t][3].x);
                     const float4 im = make_float4(R.pv[t][0].y, R.pv[t][1].y, R.pv[t][2].y, R.pv[t][3].y);
-                    const size_t ore = (size_t)uq * PT_PLANE + r * 16, oim = (size_t)(UQ + uq) * PT_PLANE + r * 16;
+                    const int aq = a_quad(t);
+                    const size_t ore = (size_t)aq * PT_PLANE + r * 16, oim = (size_t)(UQ + aq) * PT_PLANE + r * 16;
                     if constexpr (HL == 2) {
                         float4 hi, lo;
                         split4(re, hi, lo);
@@ -205,13 +213,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                     }
                 }
             }
-            if (pt < ns_items) {
-                const int su = pt % UQ, sn = pt / UQ;
+            if (s_item) {
                 const float4 re = make_float4(R.sv[0].x, R.sv[1].x, R.sv[2].x, R.sv[3].x);
                 const float4 im = make_float4(R.sv[0].y, R.sv[1].y, R.sv[2].y, R.sv[3].y);
                 // row (n, 0): [Re s | -Im s];  row (n, 1): [Im s | Re s]
-                const int r0 = 2 * sn, r1 = 2 * sn + 1;
-                const size_t p1 = (size_t)su * PT_PLANE, p2 = (size_t)(UQ + su) * PT_PLANE;
+                const int r0 = 2 * s_n, r1 = 2 * s_n + 1;
+                const size_t p1 = (size_t)s_u * PT_PLANE, p2 = (size_t)(UQ + s_u) * PT_PLANE;
                 if constexpr (HL == 2) {
                     float4 hi, lo;
                     split4(re, hi, lo);
@@ -252,31 +259,45 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     } else if (warp == PT_MMA_WARP) {
         // ---------------------------------------------------------------- MMA issue
         const uint32_t base = smem_u32(sm);
-        constexpr uint32_t ID_FULL = idesc_tf32_m128(128);
-        constexpr uint32_t ID_HALF = idesc_tf32_m128(64);
+        constexpr uint32_t ID64 = idesc_tf32_m128(64);
         const int ksteps = g.planes / 2;     // K = 8 per MMA = two 16-byte planes
         int buf = 0;
         uint32_t ph = 0;
         for (int i = 0; i < n_stages; ++i) {
-            // TMEM holds one quad of 4 consecutive subcarriers (4 x 128 columns); the quad's first
-            // MMA waits until the epilogue has drained the previous quad
-            const int slot = i & (PT_SLOTS - 1);
-            if (slot == 0 && i >= PT_SLOTS) mbar_wait(&tempty[0], (uint32_t)(((i / PT_SLOTS) - 1) & 1));
+            // TMEM: two quad buffers of 4 subcarriers x 64 columns; the first MMA of quad q waits
+            // until the epilogue has drained quad q - 2
+            const int slot = i & (PT_SLOTS - 1), q = i / PT_SLOTS, qb = q & 1;
+            if (slot == 0 && q >= 2) mbar_wait(&tempty[qb], (uint32_t)(((q >> 1) - 1) & 1));
             mbar_wait(&full[buf], ph);
             tc_fence_after();
             const uint32_t sb = base + (uint32_t)buf * g.stage_bytes;
             const uint64_t dhi = umma_desc(sb, PT_PLANE, 128);
             const uint64_t dlo = umma_desc(sb + plane_set, PT_PLANE, 128);
             const uint64_t dbs = umma_desc(sb + (HL == 2 ? 2 : 1) * plane_set, PT_PLANE, 128);
-            const uint32_t d = tmem + (uint32_t)slot * PT_COLS;
+            const uint64_t dbs_lo = dbs + (uint64_t)((64u * 16u) >> 4);         // rows 64..127: s_lo
+            const uint32_t d = tmem + (uint32_t)qb * (PT_SLOTS * PT_COLS) + (uint32_t)slot * PT_COLS;
             if (elect_one()) {
-                for (int k = 0; k < ksteps; ++k) {
-                    const uint64_t kadv = (uint64_t)((2u * k * PT_PLANE) >> 4);
-                    mma_tf32(d, dhi + kadv, dbs + kadv, ID_FULL, k > 0 ? 1u : 0u);
-                    if constexpr (HL == 2) mma_tf32(d + 64, dlo + kadv, dbs + kadv, ID_HALF, 1u);
+                if constexpr (HL == 2) {
+                    // one accumulator: the two small products first, the large A_hi s_hi last, so
+                    // the tensor core's round-toward-zero accumulation acts on the full sum only
+                    // in the last K steps (bias ~ K/8 ulp of X instead of 3 K/8)
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t kadv = (uint64_t)((2u * k * PT_PLANE) >> 4);
+                        mma_tf32(d, dlo + kadv, dbs + kadv, ID64, k > 0 ? 1u : 0u);
+                        mma_tf32(d, dhi + kadv, dbs_lo + kadv, ID64, 1u);
+                    }
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t kadv = (uint64_t)((2u * k * PT_PLANE) >> 4);
+                        mma_tf32(d, dhi + kadv, dbs + kadv, ID64, 1u);
+                    }
+                } else {
+                    for (int k = 0; k < ksteps; ++k) {
+                        const uint64_t kadv = (uint64_t)((2u * k * PT_PLANE) >> 4);
+                        mma_tf32(d, dhi + kadv, dbs + kadv, ID64, k > 0 ? 1u : 0u);
+                    }
                 }
                 umma_commit(&empty[buf]);
-                if (slot == PT_SLOTS - 1 || i == n_stages - 1) umma_commit(&tfull[0]);
+                if (slot == PT_SLOTS - 1 || i == n_stages - 1) umma_commit(&tfull[qb]);
             }
             __syncwarp();
             if (++buf == g.ns) { buf = 0; ph ^= 1u; }
@@ -293,25 +314,23 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         for (int q = 0; q * PT_SLOTS < n_stages; ++q) {
             const int cnt = min(PT_SLOTS, n_stages - q * PT_SLOTS);
             const int jfirst = ja + q * PT_SLOTS;
-            mbar_wait(&tfull[0], (uint32_t)(q & 1));
+            const int qb = q & 1;
+            mbar_wait(&tfull[qb], (uint32_t)((q >> 1) & 1));
             tc_fence_after();
             const bool vec = cnt == 4 && ((N_d & 3) == 0) && ((jfirst & 3) == 0);
 #pragma unroll 1
             for (int p = 0; p < NPW / 2; ++p) {
                 const int nl = nb + 2 * p;                    // symbols nl, nl + 1 of the tile
-                uint32_t r[PT_SLOTS][4], r2[PT_SLOTS][4];
+                uint32_t r[PT_SLOTS][4];
 #pragma unroll
-                for (int t = 0; t < PT_SLOTS; ++t) {
-                    tmem_ld4_nowait(ta + (uint32_t)t * PT_COLS + 2 * nl, r[t]);
-                    if constexpr (HL == 2) tmem_ld4_nowait(ta + (uint32_t)t * PT_COLS + 64 + 2 * nl, r2[t]);
-                }
+                for (int t = 0; t < PT_SLOTS; ++t)
+                    tmem_ld4_nowait(ta + (uint32_t)qb * (PT_SLOTS * PT_COLS) + (uint32_t)t * PT_COLS + 2 * nl, r[t]);
                 tmem_wait_ld();
                 float v[PT_SLOTS][4];
 #pragma unroll
                 for (int t = 0; t < PT_SLOTS; ++t)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        v[t][e] = HL == 2 ? __uint_as_float(r[t][e]) + __uint_as_float(r2[t][e]) : __uint_as_float(r[t][e]);
+                    for (int e = 0; e < 4; ++e) v[t][e] = __uint_as_float(r[t][e]);
                 if (b < B) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {             // v[t][2h], v[t][2h+1] = Re, Im X[nl + h][b][jfirst + t]
@@ -330,13 +349,13 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[0]);
+            mbar_arrive(&tempty[qb]);
         }
     }
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, PT_SLOTS * PT_COLS);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -367,7 +386,7 @@ static int launch_precode_tc(const void* P, bool packed, const void* s, void* X,
     FD_REQUIRE(U % 4 == 0 && U <= 32, "precode (tensor cores): U=%d must be a multiple of 4 and <= 32", U);
     FD_REQUIRE(aligned16(P) && aligned8(s) && aligned16(X), "precode (tensor cores): P / X 16-byte, s 8-byte aligned");
     const int HL = math == FD_MATH_TF32 ? 1 : 2;
-    const int NT = 64 / HL;
+    const int NT = 32;
     PtGeom g{};
     g.U = U;
     g.B = B;
@@ -375,7 +394,7 @@ static int launch_precode_tc(const void* P, bool packed, const void* s, void* X,
     g.n_sym = n_sym;
     g.planes = U / 2;
     g.stage_bytes = (HL + 1) * g.planes * PT_PLANE;
-    const size_t bar_bytes = 8 * (2 * 8 + 2 * PT_SLOTS) + 16;
+    const size_t bar_bytes = 8 * (2 * 8 + 4) + 16;
     const size_t limit = 227 * 1024;
     g.ns = (int)std::min<size_t>(8, (limit - bar_bytes) / (size_t)g.stage_bytes);
     FD_REQUIRE(g.ns >= 2, "precode (tensor cores): U=%d too large", U);

@@ -1,6 +1,7 @@
 // rx.cu — evaluation side of the hot path: receive DFT at the data bins,
 // FD channel sum over antennas (Eqs. 4-5), QAM slicing and SER.
 #include "fft.cuh"
+#include "tcgen05.cuh"
 
 namespace fdpd {
 
@@ -102,6 +103,40 @@ __global__ void k_slice(const float2* __restrict__ yhat, const uint16_t* __restr
         ++cnt;
     }
     add_counts(counts, err, near, cnt);
+}
+
+#include "combine_tc.cuh"
+
+// Tensor-core channel sum for 9 <= U <= 32 (combine_tc.cuh); process-wide switch
+// (fd_set_combine_path): 0 = auto (tensor cores where they apply), 1 = FP32 SIMT kernels.
+static int g_combine_simt = 0;
+
+static bool launch_combine_tc(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d,
+                              long long n_sym, int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
+                              const SliceParams& sp, bool ser, cudaStream_t st) {
+    if (g_combine_simt || U < 9 || U > 32 || !aligned16(yhat)) return false;
+    CtGeom g{};
+    g.B = B;
+    g.U = U;
+    g.UP = U <= 16 ? 16 : 32;
+    g.N_d = N_d;
+    g.n_sym = n_sym;
+    g.n_ntiles = (int)((n_sym + 31) / 32);
+    g.nchunks = (B + CT_KB - 1) / CT_KB;
+    const int quads = (N_d + 3) / 4;
+    const int groups = std::max(1, std::min(quads, (148 + g.n_ntiles - 1) / g.n_ntiles));
+    g.qper = (quads + groups - 1) / groups;
+    g.n_qgroups = (quads + g.qper - 1) / g.qper;
+    const size_t smem = (size_t)CT_NS * CT_STAGE + 8 * (2 * CT_NS + 4) + 16;
+    const unsigned grid = (unsigned)(g.n_qgroups * g.n_ntiles);
+    if (ser) {
+        cudaFuncSetAttribute(k_combine_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_combine_tc<true><<<grid, CT_THREADS, smem, st>>>(XPA, hfd, yhat, accumulate, idx, dec, counts, sp, g);
+    } else {
+        cudaFuncSetAttribute(k_combine_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_combine_tc<false><<<grid, CT_THREADS, smem, st>>>(XPA, hfd, yhat, accumulate, idx, dec, counts, sp, g);
+    }
+    return true;
 }
 
 // ============================================================================ channel sum (+ slicing)
@@ -366,6 +401,8 @@ static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, i
                            int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
                            const SliceParams& sp, const Impair& imp, cudaStream_t st) {
     if (imp.h_stride == 0 && imp.alpha_dev == nullptr) {
+        if (!AWGN && launch_combine_tc(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, SER, st))
+            return;
         auto go = [&](auto kern, int ns) {
             dim3 g((N_d + 127) / 128, (unsigned)((n_sym + ns - 1) / ns));
             kern<<<g, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, imp);
@@ -602,3 +639,9 @@ int ue_combine_ser_ps(const void* XPA, const void* h_fd_all, void* yhat, const f
 }
 
 }  // extern "C"
+
+extern "C" int fd_set_combine_path(int mode) {
+    FD_REQUIRE(mode == 0 || mode == 1, "fd_set_combine_path: mode=%d (0 = auto, 1 = FP32 SIMT)", mode);
+    fdpd::g_combine_simt = mode;
+    return FD_OK;
+}

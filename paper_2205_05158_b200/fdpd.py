@@ -50,6 +50,7 @@ SIGNATURES = {
     "fd_set_cnn_path": (_i, [_i]),
     "fd_set_cnn_tc_precision": (_i, [_i]),
     "fd_set_chain_split": (_i, [_i]),
+    "fd_set_combine_path": (_i, [_i]),
     "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
     "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
     "fdcnn_paper_workspace_bytes": (_sz, [_i, _ll, _i, _i]),
@@ -151,6 +152,11 @@ CNN_AUTO, CNN_SIMT, CNN_TENSOR = 0, 1, 2
 # FD_SPLIT_PRECODE_MIN_U of include/fdpd.h: from this many users the chain runs precode ->
 # chain_txrx_pre instead of the fused-prologue chain_txrx (same policy as the native runtime)
 SPLIT_PRECODE_MIN_U = 16
+
+
+def set_combine_path(mode: int):
+    """0 = auto (tensor cores for 9 <= U <= 32), 1 = FP32 SIMT kernels."""
+    _check(lib().fd_set_combine_path(int(mode)))
 
 
 def set_cnn_tc_precision(mode: int):
