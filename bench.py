@@ -264,6 +264,7 @@ def run_ours(args, cfg):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     fdpd.lib()
+    fdpd.set_combine_path(1 if args.combine == "simt" else 0)
     n = batch_of(cfg, args)
     symbols = D.symbol_range(n, rank)          # Mode S, weak scaling
     inp = gen.make_inputs(cfg, symbols)
@@ -648,6 +649,8 @@ def main():
     ap.add_argument("--split-precode", action="store_true", help="precode kernel + chain_txrx_pre")
     ap.add_argument("--precode-math", default="simt", choices=["simt", "tf32", "fp32tc"],
                     help="split-path precode: FP32 SIMT, TF32 tensor cores, or FP32-accurate split-TF32 tensor cores")
+    ap.add_argument("--combine", default="auto", choices=["auto", "simt"],
+                    help="channel sum: auto (tensor cores for 9 <= U <= 32) or the FP32 SIMT kernels")
     ap.add_argument("--mode", default="auto", choices=["auto", "symbol", "antenna"],
                     help="multi-GPU partitioning: symbol batches (Mode S) or antennas (Mode A); auto = antenna "
                          "for C5 at N > 1 (BASELINE configs[4]), else symbol")

@@ -169,6 +169,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+// L2 prefetch of the line holding p (no register, no completion tracking).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // One-thread bulk copy global -> shared (TMA engine, UBLKCP), completion counted on bar.
 // dst, src 16-byte aligned; bytes a multiple of 16.
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -33,8 +33,17 @@ namespace fdpd {
 
 constexpr int TC_M = 128;
 
+// Split-fp16 activation layout (ACT16, written by every layer's epilogue in the FP16 mode and
+// read by the next layer): per image C/4 planes [c][hl][gq] (K chunk c of CK channels, hi / lo
+// half, 8-channel group gq), each PP pixels x 16 bytes (8 fp16 values of x * 2^12) with TC_GLO
+// zero guard pixels before pixel 0 and zeros after the last computed pixel.  A K chunk of a
+// tile's A operand is then 2 CK / 8 contiguous pixel ranges, one per plane, copied into the
+// shared-memory planes with cp.async.bulk as they are (no producer threads, no split).
+constexpr int TC_GLO = 8;
+
 struct TcConv {
     int S, Wp, P, N_d;        // image side, haloed side, haloed pixels, symbols per image
+    int PP;                   // ACT16 plane length in pixels (guards included)
     int q_begin, q_end;       // computed pixel range [Wp, Wp + S Wp) (rows 1..S)
     int n_tiles;              // tiles per image
     int A_px, PL;             // staged pixels per tile, plane stride in bytes
@@ -124,26 +133,32 @@ __global__ void k_tc_weights_f16(const float* __restrict__ W, __half* __restrict
 // The first layer (IN_MODE 1: one K step per tap, C_out tanh per pixel) is bound by its
 // epilogue's dependent tanh chains at two warps per scheduler, so it runs 16 epilogue warps
 // (four column groups per TMEM lane quadrant) where C_out >= 32.
-template <int IN_MODE, int NP>
+// TMA_A (hidden layers in the FP16 mode): the A operand arrives by cp.async.bulk from the
+// ACT16 layout, so one producer warp (one elected lane) replaces the eight load / split warps.
+template <int IN_MODE, int NP, bool TMA_A = false>
 struct TcRoles {
     static constexpr int EPI = (IN_MODE == 1 && NP >= 32) ? 16 : 8;
-    static constexpr int LOAD = 8;
+    static constexpr int LOAD = TMA_A ? 1 : 8;
     static constexpr int MMA_WARP = EPI + LOAD, W_WARP = MMA_WARP + 1;
     static constexpr int THREADS = 32 * (W_WARP + 1);
     static constexpr int LOAD_THREADS = 32 * LOAD, EPI_THREADS = 32 * EPI;
 };
 
 // K chunk = 32 input channels for both precisions: with the fp16 split a 64-channel layer's
-// 9 taps x 2 chunks of weights (144 KB) stay resident in shared memory next to two 33 KB A
+// 9 taps x 2 chunks of weights (144 KB) stay resident in shared memory next to two 32 KB A
 // chunks (measured: streaming the weight slices from L2 every tile bound the 64 -> 64 layer,
-// tensor pipe 35 % busy); with the TF32 split (288 KB) they are streamed through a ring.
+// tensor pipe 35 % busy; 16-channel chunks with four A buffers measured slower, 0.94 vs
+// 0.77 ms per C5 layer of 32 symbols); with the TF32 split (288 KB) they are streamed through
+// a ring.
 __host__ __device__ constexpr int tc_ck(int cinp, bool f16) {
     (void)f16;
     return cinp >= 32 ? 32 : cinp;
 }
 
+// OUT_MODE: 0 = tanh, fp32 channels-last; 1 = residual s_out (C_out = 2); 2 = tanh, ACT16.
+// IN_MODE 0 with F16 reads ACT16 (TMA); IN_MODE 0 without F16 reads fp32 channels-last.
 template <int CINP, int NP, int IN_MODE, int OUT_MODE, bool F16>
-__global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
+__global__ void __launch_bounds__(TcRoles<IN_MODE, NP, IN_MODE == 0 && F16>::THREADS, 1)
     k_conv_tc(const float* __restrict__ act_in, const float2* __restrict__ s_in, const void* __restrict__ Wg,
               const float* __restrict__ bias, const float* __restrict__ wscale, float* __restrict__ act_out,
               float2* __restrict__ s_out, TcConv g) {
@@ -161,7 +176,8 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
     // the A_lo MMA reads only the first NP rows of B (W_hi): A_lo W_lo (~2^-22 relative) is
     // dropped and the MMA reads 25 % fewer shared-memory bytes
     constexpr uint32_t IDESC_LO = F16 ? idesc_f16_m128(NP) : idesc_tf32_m128(NP);
-    using Roles = TcRoles<IN_MODE, NP>;
+    constexpr bool TMA_A = IN_MODE == 0 && F16;
+    using Roles = TcRoles<IN_MODE, NP, TMA_A>;
     constexpr int TC_EPI_WARPS = Roles::EPI, TC_LOAD_WARPS = Roles::LOAD;
     constexpr int TC_MMA_WARP = Roles::MMA_WARP, TC_W_WARP = Roles::W_WARP;
     constexpr int TC_LOAD_THREADS = Roles::LOAD_THREADS, TC_EPI_THREADS = Roles::EPI_THREADS;
@@ -185,7 +201,7 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
             mbar_init(&acc_empty[i], TC_EPI_THREADS);
         }
         for (int i = 0; i < g.na; ++i) {
-            mbar_init(&a_full[i], TC_LOAD_THREADS);
+            mbar_init(&a_full[i], TMA_A ? 1 : TC_LOAD_THREADS);
             mbar_init(&a_empty[i], 1);
         }
         for (int i = 0; i < g.ws; ++i) {
@@ -213,46 +229,37 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
         uint32_t ph = 0;
         int img = (int)blockIdx.x / g.n_tiles, t = (int)blockIdx.x - img * g.n_tiles;
         const int dimg = (int)gridDim.x / g.n_tiles, dt = (int)gridDim.x - dimg * g.n_tiles;
+        if constexpr (TMA_A) {
+            // one lane: per (tile, K chunk) the chunk's 2 GC planes, A_px pixels each, from ACT16
+            const uint4* a16 = reinterpret_cast<const uint4*>(act_in);
+            const uint32_t plane_bytes = (uint32_t)g.A_px * 16u;
+            for (int i = 0; i < my_tiles; ++i) {
+                const int qa = t * TC_M - 1;              // q0 - Wp - 1 with q0 = Wp + t TC_M
+                for (int c = 0; c < NCH; ++c, ++n_staged) {
+                    if (n_staged >= g.na) mbar_wait(&a_empty[buf], ph ^ 1u);
+                    if (elect_one()) {
+                        unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
+                        mbar_arrive_expect_tx(&a_full[buf], 2u * GC * plane_bytes);
+                        const uint4* src = a16 + ((size_t)img * (CINP / 4) + (size_t)c * 2 * GC) * g.PP + TC_GLO + qa;
+#pragma unroll
+                        for (int pl = 0; pl < 2 * GC; ++pl)
+                            tma_bulk_g2s(ab + (size_t)pl * g.PL, src + (size_t)pl * g.PP, plane_bytes, &a_full[buf]);
+                    }
+                    __syncwarp();
+                    if (++buf == g.na) { buf = 0; ph ^= 1u; }
+                }
+                img += dimg;
+                t += dt;
+                if (t >= g.n_tiles) { t -= g.n_tiles; ++img; }
+            }
+        } else
         for (int i = 0; i < my_tiles; ++i) {
             const int q0 = g.q_begin + t * TC_M;
             const int qa = q0 - g.Wp - 1;
             for (int c = 0; c < NCH; ++c, ++n_staged) {
                 if (n_staged >= g.na) mbar_wait(&a_empty[buf], ph ^ 1u);
                 unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
-                if constexpr (IN_MODE == 0 && F16) {
-                    // 8 channels (two fp32 float4) -> 16 bytes of fp16 hi and 16 bytes of lo
-                    const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP) + c * (CK / 4);
-                    constexpr int PB = 4;
-                    const int ne = g.A_px * GC;
-                    for (int e0 = lt; e0 < ne; e0 += PB * TC_LOAD_THREADS) {
-                        float4 x[PB][2];
-#pragma unroll
-                        for (int k = 0; k < PB; ++k) {
-                            const int e = e0 + k * TC_LOAD_THREADS;
-                            const int p = e / GC, gq = e - p * GC;
-                            const int pos = qa + p;
-                            x[k][0] = x[k][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                            if (e < ne && pos >= 0 && pos < g.P) {
-                                x[k][0] = __ldg(src + (size_t)pos * G + 2 * gq);
-                                x[k][1] = __ldg(src + (size_t)pos * G + 2 * gq + 1);
-                            }
-                        }
-#pragma unroll
-                        for (int k = 0; k < PB; ++k) {
-                            const int e = e0 + k * TC_LOAD_THREADS;
-                            if (e >= ne) break;
-                            const int p = e / GC, gq = e - p * GC;
-                            constexpr float S = TC_ACT_SCALE;
-                            uint4 hi, lo;
-                            split_f16x2(x[k][0].x * S, x[k][0].y * S, hi.x, lo.x);
-                            split_f16x2(x[k][0].z * S, x[k][0].w * S, hi.y, lo.y);
-                            split_f16x2(x[k][1].x * S, x[k][1].y * S, hi.z, lo.z);
-                            split_f16x2(x[k][1].z * S, x[k][1].w * S, hi.w, lo.w);
-                            *reinterpret_cast<uint4*>(ab + (size_t)gq * g.PL + p * 16) = hi;
-                            *reinterpret_cast<uint4*>(ab + (size_t)(GC + gq) * g.PL + p * 16) = lo;
-                        }
-                    }
-                } else if constexpr (IN_MODE == 0) {
+                if constexpr (IN_MODE == 0) {
                     const float4* src = reinterpret_cast<const float4*>(act_in + (size_t)img * g.P * CINP) + c * GC;
                     // PB independent 16-byte loads in flight per thread before any split / store
                     constexpr int PB = 8;
@@ -409,7 +416,47 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP>::THREADS, 1)
             const int prow = pos / g.Wp, pcol = pos - prow * g.Wp;
             const bool interior = pos < g.q_end && pcol >= 1 && pcol <= g.S;
             const float dscale = bsm[NP];
-            if constexpr (OUT_MODE == 0) {
+            if constexpr (OUT_MODE == 2) {
+                // ACT16: the next layer's K chunks (CKO channels) -> planes [c][hl][gq] of 8 channels
+                constexpr int CKO = tc_ck(NP, true), GCO = CKO / 8, NPL = NP / 4;
+                uint4* o = reinterpret_cast<uint4*>(act_out) + (size_t)img * NPL * g.PP + TC_GLO + pos;
+                constexpr int HC = NP / NGRP;
+#pragma unroll
+                for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 8) {
+                    float v[8], w[8], v2[8], w2[8];
+                    tmem_ld8(tbase + c0, v);
+                    tmem_ld8(tbase + NP + c0, w);
+                    tmem_ld8(tbase + 2 * NP + c0, v2);
+                    tmem_ld8(tbase + 3 * NP + c0, w2);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        v[j] = interior ? TC_ACT_SCALE * tanhf(((v[j] + v2[j]) + (w[j] + w2[j])) * dscale + bsm[c0 + j])
+                                        : 0.f;
+                    uint4 hi, lo;
+                    split_f16x2(v[0], v[1], hi.x, lo.x);
+                    split_f16x2(v[2], v[3], hi.y, lo.y);
+                    split_f16x2(v[4], v[5], hi.z, lo.z);
+                    split_f16x2(v[6], v[7], hi.w, lo.w);
+                    const int pl = (c0 / CKO) * 2 * GCO + (c0 % CKO) / 8;
+                    if (pos < g.q_end) {
+                        o[(size_t)pl * g.PP] = hi;
+                        o[(size_t)(pl + GCO) * g.PP] = lo;
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&acc_empty[acc]);
+                // guards + halo row 0 (pixels -TC_GLO .. Wp - 1) from the first tile, halo row S + 1
+                // and everything after it (pixels q_end .. PP - TC_GLO - 1) from the last tile
+                for (int side = 0; side < 2; ++side) {
+                    if (t != (side ? g.n_tiles - 1 : 0)) continue;
+                    const int a = side ? TC_GLO + g.q_end : 0, len = side ? g.PP - a : TC_GLO + g.Wp;
+                    uint4* z = reinterpret_cast<uint4*>(act_out) + (size_t)img * NPL * g.PP + a;
+                    for (int e = tid; e < NPL * len; e += TC_EPI_THREADS) {
+                        const int pl = e / len;
+                        z[(size_t)pl * g.PP + (e - pl * len)] = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                }
+            } else if constexpr (OUT_MODE == 0) {
                 float* o = act_out + ((size_t)img * g.P + pos) * NP;
                 constexpr int HC = NP / NGRP;         // columns per warp (>= 8)
 #pragma unroll
@@ -579,6 +626,8 @@ static TcConv tc_geom(int S, int N_d, int Cin, int Cout, long long n_img) {
     g.n_tiles = (S * g.Wp + TC_M - 1) / TC_M;
     g.A_px = (TC_M + 2 * g.Wp + 2 + 7) & ~7;
     g.PL = (g.A_px + 1) * 16;   // one spare row: the 4-channel groups of a pixel hit distinct banks
+    // ACT16 planes: guards, then every pixel a tile's A range can touch (up to (n_tiles - 1) TC_M + A_px - 2)
+    g.PP = (TC_GLO + std::max(g.P, (g.n_tiles - 1) * TC_M + g.A_px) + 8 + 7) & ~7;
     g.Cin = Cin;
     g.Cout = Cout;
     g.n_img = n_img;
@@ -633,7 +682,7 @@ static int launch_tc_na(const TcConv& g, size_t smem, const float* act_in, const
     auto kern = k_conv_tc<CINP, NP, IN_MODE, OUT_MODE, F16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, dev = 0, nsm = 148;
-    constexpr int THREADS = TcRoles<IN_MODE, NP>::THREADS;
+    constexpr int THREADS = TcRoles<IN_MODE, NP, IN_MODE == 0 && F16>::THREADS;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -660,7 +709,8 @@ static int g_tc_f16 = 1;
 size_t fdcnn_tc_workspace_bytes(const int* chans, int n_layers, long long n_sym, int U, int N_d) {
     int S = 1;
     while (S * S < N_d) ++S;
-    const size_t P = (size_t)(S + 2) * (S + 2);
+    // activations: P pixels x C fp32 (TF32 mode) or C / 4 ACT16 planes of PP pixels x 16 B
+    const size_t P = (size_t)tc_geom(S, N_d, 2, 2, 1).PP;
     int cmax = 0;
     for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
     const size_t one = (((size_t)n_sym * U * P * cmax * 4) + 255) & ~(size_t)255;
@@ -675,7 +725,7 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
     int S = 1;
     while (S * S < N_d) ++S;
     const long long n_img = n_sym * U;
-    const size_t P = (size_t)(S + 2) * (S + 2);
+    const size_t P = (size_t)tc_geom(S, N_d, 2, 2, 1).PP;
     int cmax = 0;
     for (int l = 1; l < n_layers; ++l) cmax = chans[l] > cmax ? chans[l] : cmax;
     const size_t one = (((size_t)n_img * P * cmax * 4) + 255) & ~(size_t)255;
@@ -711,8 +761,16 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
         if (!smem) return fail_arg("fdcnn_forward: tensor-core plan does not fit shared memory");
         const float* in = first ? nullptr : act[(l - 1) & 1];
         float* out = last ? nullptr : act[l & 1];
-        if (first) rc = launch_tc_n<1, 0, 8, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream);
-        else if (last) {
+        // FP16 mode: every intermediate activation in the ACT16 layout (first layer's epilogue
+        // splits, hidden layers stage A by TMA, the last layer reads hi + lo)
+        // FP16 mode: the activations between two tensor-core layers are in the ACT16 layout
+        // (the producing epilogue splits, the consumer stages A by TMA); the input of the last
+        // layer (FP32 direct convolution) stays fp32 channels-last
+        const bool next_f16 = g_tc_f16 && l + 1 < n_layers - 1;
+        if (first) {
+            rc = next_f16 ? launch_tc_n<1, 2, 8, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream)
+                          : launch_tc_n<1, 0, 8, false>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream);
+        } else if (last) {
             // C_out = 2: direct FP32 convolution on the channels-last activations
             const long long nth = n_img * (long long)(((S + 3) / 4) * ((S + 3) / 4)) * (CINP / 4);
             const unsigned blocks = (unsigned)((nth + 255) / 256);
@@ -723,7 +781,13 @@ int fdcnn_tc_forward(const float* params, const int* chans, int n_layers, const 
             }
             rc = check_launch("fdcnn_forward (last layer)");
         } else {
-            if (f16) {
+            if (f16 && next_f16) {
+                switch (CINP) {
+                    case 16: rc = launch_tc_n<0, 2, 16, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                    case 32: rc = launch_tc_n<0, 2, 32, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                    default: rc = launch_tc_n<0, 2, 64, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
+                }
+            } else if (f16) {
                 switch (CINP) {
                     case 16: rc = launch_tc_n<0, 0, 16, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;
                     case 32: rc = launch_tc_n<0, 0, 32, true>(NP, g, smem, in, s_in, Wg, b, wscale, out, s_out, stream); break;

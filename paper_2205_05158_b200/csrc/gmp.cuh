@@ -174,11 +174,9 @@ struct RunLayout {
 // (usw_r / esw_r, distributed shared memory), which hold the other half — for two halves the
 // partner is both the left and the right (circular) neighbour.
 //
-// The memory taps l are processed in chunks [L0, L1] (gmp_run_taps), each with its own envelope
-// and input windows: the registers hold the windows of one chunk only.  At the C4/C5 shape
-// (Kp = 5, L = 6, M = 3, R = 4) the whole-run windows took 4 x 20 envelope powers + 10 complex
-// inputs and the 128-register kernel spilled (272 B of stack); in two chunks the envelope
-// window is 4 x 16.  The summation order over l (and within each l) is unchanged.
+// The memory taps l can be processed in chunks [L0, L1] (gmp_run_taps), each with its own
+// envelope and input windows, so the registers hold the windows of one chunk only (see
+// gmp_tap_chunk).  The summation order over l (and within each l) is the same either way.
 __host__ __device__ constexpr int round_up_pow2(int x, int a) { return (x + a - 1) & ~(a - 1); }
 
 template <int KP, int L, int M, int R, bool HALO, int L0, int L1>
@@ -272,10 +270,15 @@ __device__ __forceinline__ void gmp_run_taps(const float2* __restrict__ usw, con
     }
 }
 
-// Taps per window chunk: all L + 1 at once except the largest specialised shape (Kp = 5 with
-// L >= 6, C4 / C5), which runs two chunks to stay inside 128 registers.
+// Taps per window chunk: all L + 1 at once.  (Two chunks of 4 taps at the C4 / C5 shape
+// halved the envelope window held in registers, but recomputing the envelope powers per chunk
+// cost more than the spills it removed once the FFT passes parked their inputs in shared memory:
+// C5 chain 5.99 ms with one chunk vs 6.16 ms with two; -DFD_GMP_TAP_CHUNK=4 rebuilds the latter.)
+#ifndef FD_GMP_TAP_CHUNK
+#define FD_GMP_TAP_CHUNK 0
+#endif
 template <int KP, int L, int M>
-__host__ __device__ constexpr int gmp_tap_chunk() { return (KP >= 5 && L >= 6) ? 4 : L + 1; }
+__host__ __device__ constexpr int gmp_tap_chunk() { return FD_GMP_TAP_CHUNK > 0 ? FD_GMP_TAP_CHUNK : L + 1; }
 
 template <int KP, int L, int M, int R, bool HALO, int L0>
 __device__ __forceinline__ void gmp_run_chunks(const float2* __restrict__ usw, const float* __restrict__ esw,

@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfdpd.so")
+# FDPD_LIB: an alternative build of the same library (tools/ A/B experiments of compile-time variants)
+LIB_PATH = os.environ.get("FDPD_LIB") or os.path.join(_HERE, "libfdpd.so")
 
 FD_OK, FD_ERR_ARG, FD_ERR_NUMERIC, FD_ERR_CUDA = 0, 2, 3, 4
 

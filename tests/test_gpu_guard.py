@@ -1,0 +1,237 @@
+"""Memory-safety and race checks of every kernel family through the C ABI, standing in for
+compute-sanitizer, which this GPU pool does not allow:
+
+  * guard bands: every output and workspace the caller passes sits inside a larger buffer
+    whose head and tail are filled with a sentinel bit pattern; after the call the sentinels
+    must be intact (an out-of-bounds store of any kernel — a TMA bulk copy, a tile epilogue,
+    a halo-zeroing loop, a counter — changes them);
+  * determinism: the same call repeated on the same inputs gives bit-identical outputs (a
+    missing barrier / mbarrier wait in a warp-specialised pipeline, or a shared-memory race,
+    shows up as run-to-run differences);
+  * tiny and ragged shapes that still take each kernel's real code path.
+Parity itself is in test_gpu_parity / test_gpu_precode_tc / test_gpu_combine_tc."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from workload import configs, gen
+
+pytestmark = pytest.mark.gpu
+
+GUARD = 4096                      # sentinel bytes before and after every guarded buffer
+SENT = 0x7FA5A5A5                 # a NaN payload no kernel writes
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2205_05158_b200 import fdpd
+    fdpd.lib()
+    return fdpd
+
+
+class Guarded:
+    """A tensor of `shape` / `dtype` carved out of an int32 buffer with sentinel guard bands."""
+
+    def __init__(self, shape, dtype, fill=None):
+        nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        self.nbytes = nbytes
+        n_words = (2 * GUARD + ((nbytes + 15) // 16) * 16) // 4
+        self.raw = torch.full((n_words,), SENT, dtype=torch.int32, device="cuda")
+        body = self.raw.view(torch.uint8)[GUARD:GUARD + nbytes]
+        self.t = body.view(dtype).view(shape) if nbytes else torch.empty(shape, dtype=dtype, device="cuda")
+        if fill is not None and nbytes:
+            self.t.copy_(fill)
+
+    def check(self, what=""):
+        torch.cuda.synchronize()
+        head = self.raw[: GUARD // 4]
+        tail_start = (GUARD + ((self.nbytes + 15) // 16) * 16) // 4
+        tail = self.raw[tail_start:]
+        assert bool((head == SENT).all()), f"{what}: write before the buffer"
+        assert bool((tail == SENT).all()), f"{what}: write past the buffer"
+        # bytes between nbytes and the 16-byte rounding belong to the tail guard too
+        pad = self.raw.view(torch.uint8)[GUARD + self.nbytes:GUARD + ((self.nbytes + 15) // 16) * 16]
+        want = torch.tensor([SENT], dtype=torch.int32).view(torch.uint8).repeat(8).to("cuda")
+        off = (GUARD + self.nbytes) % 4
+        assert bool((pad == want[off:off + pad.numel()]).all()), f"{what}: write into the padding"
+
+
+def cr(rng, *shape, scale=1.0):
+    x = scale * (rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+    return torch.from_numpy(x.astype(np.complex64)).to("cuda")
+
+
+def repeat_equal(fn, n=3):
+    """fn() -> tensor (or tuple); n runs must be bit-identical."""
+    ref = [t.clone() for t in _as_tuple(fn())]
+    for _ in range(n - 1):
+        got = _as_tuple(fn())
+        for a, b in zip(ref, got):
+            assert torch.equal(a.view(torch.uint8) if a.is_complex() else a, b.view(torch.uint8) if b.is_complex() else b)
+
+
+def _as_tuple(x):
+    return x if isinstance(x, tuple) else (x,)
+
+
+# ============================================================================ a1
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("chans,N_d,nsym,U", [((2, 64, 64, 64, 64, 2), 3300, 1, 2),
+                                             ((2, 32, 32, 32, 2), 1200, 2, 3),
+                                             ((2, 16, 32, 64, 2), 500, 3, 2),
+                                             ((2, 16, 16, 2), 600, 5, 4),
+                                             ((2, 32, 2), 2, 3, 1)])
+def test_guard_fdcnn_tensor(F, prec, chans, N_d, nsym, U):
+    rng = np.random.default_rng(N_d + nsym)
+    n_par = sum(co * ci * 9 + co for ci, co in zip(chans[:-1], chans[1:]))
+    params = torch.from_numpy((0.05 * rng.standard_normal(n_par)).astype(np.float32)).cuda()
+    s = cr(rng, nsym, U, N_d, scale=0.7)
+    F.set_cnn_path(F.CNN_TENSOR)
+    F.set_cnn_tc_precision(prec)
+    try:
+        need = F.lib().fdcnn_workspace_bytes(F._ints(chans), len(chans) - 1, nsym, U, N_d)
+        ws = Guarded((need,), torch.uint8)
+        out = Guarded((nsym, U, N_d), torch.complex64)
+        repeat_equal(lambda: F.fdcnn_forward(params, chans, s, out=out.t, workspace=ws.t))
+        out.check("fdcnn_forward out")
+        ws.check("fdcnn_forward workspace")
+    finally:
+        F.set_cnn_path(F.CNN_AUTO)
+        F.set_cnn_tc_precision(0)
+
+
+@pytest.mark.parametrize("name,nsym", [("C1", 3), ("C2", 5)])
+def test_guard_fdcnn_fused(F, name, nsym):
+    cfg = configs.get(name)
+    inp = gen.make_inputs(cfg, range(nsym))
+    params = torch.from_numpy(inp["params"]).cuda()
+    s = torch.from_numpy(inp["s"]).cuda()
+    need = F.lib().fdcnn_workspace_bytes(F._ints(cfg.chans), len(cfg.chans) - 1, nsym, cfg.U, cfg.N_d)
+    ws = Guarded((need,), torch.uint8)
+    out = Guarded(tuple(s.shape), torch.complex64)
+    repeat_equal(lambda: F.fdcnn_forward(params, cfg.chans, s, out=out.t, workspace=ws.t))
+    out.check("fdcnn out")
+    ws.check("fdcnn workspace")
+
+
+# ============================================================================ a3
+@pytest.mark.parametrize("math", [0, 1, 2])
+@pytest.mark.parametrize("n,B,U,Nd", [(33, 130, 32, 38), (2, 40, 12, 70), (65, 64, 4, 600), (1, 8, 4, 36)])
+def test_guard_precode(F, math, n, B, U, Nd):
+    if math and U % 4:
+        pytest.skip("tensor-core precode needs U % 4 == 0")
+    rng = np.random.default_rng(n + B)
+    P, s = cr(rng, B, U, Nd), cr(rng, n, U, Nd)
+    X = Guarded((n, B, Nd), torch.complex64)
+    repeat_equal(lambda: F.precode(P, s, out=X.t, math=math))
+    X.check("precode")
+    if math:
+        Ppk = Guarded((Nd, B, 2 * U), torch.float32)
+        F.precode_pack(P, out=Ppk.t)
+        Ppk.check("precode_pack")
+        X2 = Guarded((n, B, Nd), torch.complex64)
+        repeat_equal(lambda: F.precode_packed(Ppk.t, s, out=X2.t, math=math))
+        X2.check("precode_packed")
+        assert torch.equal(X.t, X2.t)
+
+
+# ============================================================================ a4-a6 fused chains
+@pytest.mark.parametrize("name,n,B", [("C1", 3, None), ("C2", 2, 5), ("C3", 1, 3), ("C5", 1, 2)])
+def test_guard_chain(F, name, n, B):
+    cfg = configs.get(name)
+    B = B or cfg.B
+    rng = np.random.default_rng(5)
+    inp = gen.make_inputs(cfg, range(n))
+    coef = torch.from_numpy(inp["coef"][:B]).cuda()
+    X = cr(rng, n, B, cfg.N_d, scale=0.05)
+    y = Guarded((n, B, cfg.N_ifft), torch.complex64)
+    XPA = Guarded((n, B, cfg.N_d), torch.complex64)
+    repeat_equal(lambda: F.chain_txrx_pre(X, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft, y=y.t, XPA=XPA.t))
+    y.check("chain_txrx_pre y")
+    XPA.check("chain_txrx_pre XPA")
+    if cfg.U <= 8:
+        P = cr(rng, B, cfg.U, cfg.N_d, scale=0.1)
+        st = cr(rng, n, cfg.U, cfg.N_d)
+        y2 = Guarded((n, B, cfg.N_ifft), torch.complex64)
+        XPA2 = Guarded((n, B, cfg.N_d), torch.complex64)
+        repeat_equal(lambda: F.chain_txrx(P, st, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft, y=y2.t, XPA=XPA2.t))
+        y2.check("chain_txrx y")
+        XPA2.check("chain_txrx XPA")
+        y3 = Guarded((n, B, cfg.N_ifft), torch.complex64)
+        repeat_equal(lambda: F.chain_tx(P, st, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft, out=y3.t))
+        y3.check("chain_tx")
+
+
+@pytest.mark.parametrize("N,Nd", [(128, 36), (4096, 600), (16384, 3300), (16, 8)])
+def test_guard_stages(F, N, Nd):
+    rng = np.random.default_rng(N)
+    X = cr(rng, 2, 3, Nd)
+    x = Guarded((2, 3, N), torch.complex64)
+    repeat_equal(lambda: F.ofdm_modulate(X, N, out=x.t))
+    x.check("ofdm_modulate")
+    cfg = configs.C2
+    coef = torch.from_numpy(gen.make_inputs(cfg, [0])["coef"][:3]).cuda()
+    y = Guarded((2, 3, N), torch.complex64)
+    repeat_equal(lambda: F.gmp_pa(x.t, coef, cfg.orders, cfg.L, cfg.M, out=y.t))
+    y.check("gmp_pa")
+
+
+# ============================================================================ a6 channel sum
+@pytest.mark.parametrize("simt", [0, 1])
+@pytest.mark.parametrize("n,B,U,Nd", [(2, 40, 32, 70), (33, 20, 12, 38), (5, 64, 4, 600), (70, 17, 9, 6)])
+def test_guard_combine(F, simt, n, B, U, Nd):
+    rng = np.random.default_rng(n * B)
+    XPA, h = cr(rng, n, B, Nd), cr(rng, U, B, Nd)
+    idx = torch.from_numpy(rng.integers(0, 256, (n, U, Nd)).astype(np.uint16)).cuda()
+    F.set_combine_path(simt)
+    try:
+        yh = Guarded((n, U, Nd), torch.complex64)
+        dec = Guarded((n, U, Nd), torch.uint16)
+        cnt = Guarded((3,), torch.int64)
+
+        def run():
+            cnt.t.zero_()
+            F.ue_combine_ser(XPA, h, 3.0, idx, 256, yhat=yh.t, counts=cnt.t, dec=dec.t)
+            return yh.t, dec.t, cnt.t
+        repeat_equal(run)
+        for g, w in ((yh, "yhat"), (dec, "dec"), (cnt, "counts")):
+            g.check("ue_combine_ser " + w)
+        assert int(cnt.t[1]) == n * U * Nd
+        yh2 = Guarded((n, U, Nd), torch.complex64)
+        repeat_equal(lambda: F.ue_combine(XPA, h, out=yh2.t))
+        yh2.check("ue_combine")
+    finally:
+        F.set_combine_path(0)
+
+
+# ============================================================================ a2, runtime
+def test_guard_zf(F):
+    cfg = configs.C5
+    taps = torch.from_numpy(np.ascontiguousarray(gen.make_inputs(cfg, [0])["h_taps"][:, :, :40])).cuda()
+    repeat_equal(lambda: F.zf_precoder_build(taps, 256, 70, 0.3)[:2])
+
+
+def test_guard_step_c1_native_and_redraw(F):
+    """The whole C1 step through the Python plan, the native runtime and the redraw path,
+    twice each, bit-identical."""
+    from paper_2205_05158_b200.chain import Chain, Shapes
+    cfg = configs.C1
+    inp = gen.make_inputs(cfg, range(4))
+    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device="cuda", max_batch=4)
+    s, idx = torch.from_numpy(inp["s"]).cuda(), torch.from_numpy(inp["idx"]).cuda()
+
+    def step():
+        c = torch.zeros(3, dtype=torch.int64, device="cuda")
+        yh, _, _ = ch.step(s, idx, counts=c)
+        return yh.clone(), c
+    repeat_equal(step)
+    taps = torch.from_numpy(gen.channel_taps_per_symbol(cfg, list(range(4)))).cuda()
+
+    def redraw():
+        c = torch.zeros(3, dtype=torch.int64, device="cuda")
+        yh, _, _ = ch.step_redraw(s, idx, taps, counts=c)
+        return yh.clone(), c
+    repeat_equal(redraw)

@@ -105,11 +105,23 @@ def test_fdcnn_forward(F, name, nsym):
 
 @pytest.fixture
 def cnn_path(F):
-    yield F.set_cnn_path
+    def set_path(p):
+        F.set_cnn_path(p)
+        F.set_cnn_tc_precision(0)
+
+    def set_named(name):
+        """simt | tensor (FP16-split hidden layers, ACT16 activations) | tensor_tf32 (TF32 split)."""
+        set_path(F.CNN_SIMT if name == "simt" else F.CNN_TENSOR)
+        if name == "tensor_tf32":
+            F.set_cnn_tc_precision(1)
+
+    set_path.named = set_named
+    yield set_path
     F.set_cnn_path(F.CNN_AUTO)
+    F.set_cnn_tc_precision(0)
 
 
-@pytest.mark.parametrize("path", ["simt", "tensor"])
+@pytest.mark.parametrize("path", ["simt", "tensor", "tensor_tf32"])
 @pytest.mark.parametrize("chans,N_d,nsym,U", [((2, 16, 16, 2), 600, 37, 4),      # C2 shape, many tiles / CTA
                                              ((2, 32, 32, 32, 2), 1200, 3, 8),  # C3
                                              ((2, 64, 64, 64, 64, 2), 3300, 1, 4),  # C5 widths (streamed W)
@@ -117,8 +129,8 @@ def cnn_path(F):
                                              ((2, 16, 2), 37, 9, 2),             # no hidden-to-hidden layer, S = 7
                                              ((2, 32, 2), 2, 4, 1)])             # S = 2: one partial tile
 def test_fdcnn_paths(F, cnn_path, path, chans, N_d, nsym, U):
-    """Tensor-core (3xTF32 tcgen05) and SIMT FD-CNN paths against the fp64 oracle."""
-    cnn_path(F.CNN_SIMT if path == "simt" else F.CNN_TENSOR)
+    """Tensor-core (FP16 / TF32 split tcgen05) and SIMT FD-CNN paths against the fp64 oracle."""
+    cnn_path.named(path)
     rng = np.random.default_rng(len(chans) * 1000 + N_d)
     s = crandn(rng, nsym, U, N_d, scale=0.7)
     n_par = sum(co * ci * 9 + co for ci, co in zip(chans[:-1], chans[1:]))
@@ -129,18 +141,18 @@ def test_fdcnn_paths(F, cnn_path, path, chans, N_d, nsym, U):
     assert rel(got - s, want - s) < 1e-4
 
 
-@pytest.mark.parametrize("path", ["simt", "tensor"])
+@pytest.mark.parametrize("path", ["simt", "tensor", "tensor_tf32"])
 @pytest.mark.parametrize("seed", range(8))
 def test_fdcnn_random_shapes(F, cnn_path, path, seed):
     """Seeded random networks / image sizes on both CNN paths (tensor path: hidden widths in
     {16, 32, 64}; SIMT path: any width) against the fp64 oracle."""
     rng = np.random.default_rng(7000 + seed)
     depth = int(rng.integers(1, 5))
-    widths = [16, 32, 64] if path == "tensor" else [3, 8, 16, 20, 32]
+    widths = [16, 32, 64] if path != "simt" else [3, 8, 16, 20, 32]
     chans = (2,) + tuple(int(rng.choice(widths)) for _ in range(depth)) + (2,)
     N_d = 2 * int(rng.integers(1, 300))
     U, nsym = int(rng.integers(1, 5)), int(rng.integers(1, 4))
-    cnn_path(F.CNN_SIMT if path == "simt" else F.CNN_TENSOR)
+    cnn_path.named(path)
     s = crandn(rng, nsym, U, N_d, scale=0.7)
     n_par = sum(co * ci * 9 + co for ci, co in zip(chans[:-1], chans[1:]))
     params = (0.05 * rng.standard_normal(n_par)).astype(np.float32)
