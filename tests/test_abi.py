@@ -89,7 +89,13 @@ def test_workspace_queries(lib):
         act = 2 * 4 * 16 * 8 * 32 * 35 * 35                  # C3: per-layer, two activation buffers
         assert act < lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200) < act + (1 << 20)   # + transposed weights
         assert lib.fd_set_cnn_path(2) == 0                               # tensor cores
-        act = 2 * 4 * 16 * 8 * 32 * 37 * 37                  # channels-last, zero halo (S + 2)^2
+        # two activation buffers of PP pixels x 32 channels x 4 B per image: PP = the split-fp16
+        # plane length (conv_tc.cu tc_geom: 8 guard pixels + (n_tiles - 1) * 128 + A_px + 8, rounded
+        # to 8) >= the (S + 2)^2 haloed pixels of the TF32 mode's channels-last layout
+        S, Wp = 35, 37
+        n_tiles, A_px = (S * Wp + 127) // 128, (128 + 2 * Wp + 2 + 7) & ~7
+        PP = (8 + max(Wp * Wp, (n_tiles - 1) * 128 + A_px) + 8 + 7) & ~7
+        act = 2 * 4 * 16 * 8 * 32 * PP
         wsplit = 4 * 9 * 2 * (8 * 32 + 32 * 32 * 2 + 32 * 16)   # hi/lo weight images, padded
         tc_bytes = lib.fdcnn_workspace_bytes(ch, 4, 16, 8, 1200)
         assert act + wsplit <= tc_bytes < act + wsplit + 4096
