@@ -264,7 +264,7 @@ def run_ours(args, cfg):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     fdpd.lib()
-    fdpd.set_combine_path(1 if args.combine == "simt" else 0)
+    fdpd.set_combine_path({"auto": 0, "simt": 1, "tc": 2}[args.combine])
     n = batch_of(cfg, args)
     symbols = D.symbol_range(n, rank)          # Mode S, weak scaling
     inp = gen.make_inputs(cfg, symbols)
@@ -456,8 +456,9 @@ def run_ours(args, cfg):
         "config": dict(config_dict(cfg, ws, n), impairments=bool(args.impair),
                        channel=("per-symbol redraw, ZF in the step" if args.redraw else
                                 "one realisation per run, ZF before timing"),
-                       precode=("tensor cores, " + args.precode_math if split and args.precode_math != "simt"
-                                else ("FP32 SIMT kernel" if split else "fused into the chain kernel"))),
+                       precode=("tensor cores, " + ch.precode_math if split and ch.precode_math != "simt"
+                                else ("FP32 SIMT kernel" if split else "fused into the chain kernel")),
+                       channel_sum={"auto": "FP32 SIMT (auto)", "simt": "FP32 SIMT", "tc": "tensor cores"}[args.combine]),
         "roofline": {"kernel": kern, "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "traffic": measured_traffic(cfg, n, args),
@@ -521,7 +522,7 @@ def run_antenna(args, cfg):
     symbols = D.symbol_range(n, rank)
     inp = gen.make_inputs(cfg, symbols)
     b0, B_loc = D.antenna_shard(cfg.B, ws, rank)
-    math = args.precode_math if args.precode_math != "simt" else "simt"
+    math = args.precode_math
     t0 = time.perf_counter()
     ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], device=dev,
                max_batch=ws * n // micro, b0=b0, B_loc=B_loc, precode_math=math)
@@ -647,10 +648,10 @@ def main():
     ap.add_argument("--impair", action="store_true", help="PA clip + noise, AWGN, imperfect CSI (NEXT f3)")
     ap.add_argument("--redraw", action="store_true", help="per-symbol channel redraw, ZF on the hot path (NEXT f4)")
     ap.add_argument("--split-precode", action="store_true", help="precode kernel + chain_txrx_pre")
-    ap.add_argument("--precode-math", default="simt", choices=["simt", "tf32", "fp32tc"],
+    ap.add_argument("--precode-math", default="auto", choices=["auto", "simt", "tf32", "fp32tc"],
                     help="split-path precode: FP32 SIMT, TF32 tensor cores, or FP32-accurate split-TF32 tensor cores")
-    ap.add_argument("--combine", default="auto", choices=["auto", "simt"],
-                    help="channel sum: auto (tensor cores for 9 <= U <= 32) or the FP32 SIMT kernels")
+    ap.add_argument("--combine", default="auto", choices=["auto", "simt", "tc"],
+                    help="channel sum: auto (= the FP32 SIMT kernels), simt, or tc (tensor cores for 9 <= U <= 32)")
     ap.add_argument("--mode", default="auto", choices=["auto", "symbol", "antenna"],
                     help="multi-GPU partitioning: symbol batches (Mode S) or antennas (Mode A); auto = antenna "
                          "for C5 at N > 1 (BASELINE configs[4]), else symbol")

@@ -284,11 +284,11 @@ int ue_slice_ser(const void* yhat, float alpha, const uint16_t* tx_idx, int M_qa
  *   yhat[n][u][j] (+)= sum_b h_fd[u][b][j] XPA[n][b][j];  n_sym <= 65535 per call. */
 int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, int B_loc, int U, int N_d,
                int accumulate, cudaStream_t stream);
-/* Channel-sum implementation (process-wide): 0 = auto (default) — for 9 <= U <= 32 (and no
- * AWGN, one channel realisation, 16-byte aligned yhat) the sum runs on the tensor cores
- * (tcgen05 kind::tf32, per-subcarrier real GEMM with K = 2 B_loc, FP32-accurate hi/lo split on
- * both operands, four products), else the FP32 SIMT kernels; 1 = always FP32 SIMT.
- * FD_ERR_ARG for other modes. */
+/* Channel-sum implementation (process-wide): 0 = auto (default) = the FP32 SIMT kernels
+ * (measured faster at C4 / C5); 1 = FP32 SIMT; 2 = tensor cores where they apply — 9 <= U <= 32,
+ * no AWGN, one channel realisation, 16-byte aligned yhat (tcgen05 kind::tf32, per-subcarrier
+ * real GEMM with K = 2 B_loc, FP32-accurate hi/lo split on both operands, four products),
+ * else SIMT.  FD_ERR_ARG for other modes. */
 int fd_set_combine_path(int mode);
 /* ue_combine (accumulate = 0) fused with ue_slice_ser. */
 int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
@@ -325,7 +325,10 @@ typedef struct fd_chain fd_chain;
 
 /* Copies the HOST arrays h_taps [T][U][B] complex64, coef [B][n_coef] complex64 and
  * params (float) to the device, builds the ZF precoder (zf_precoder_build; synchronises)
- * and reserves buffers for batches of up to max_batch symbols. */
+ * and reserves buffers for batches of up to max_batch symbols.  A step is fdcnn_forward ->
+ * chain_txrx (U < FD_SPLIT_PRECODE_MIN_U) or precode -> chain_txrx_pre (the precode on the
+ * tensor cores, FD_MATH_FP32_TC on a precode_pack'ed P, where U % 4 == 0 and U <= 32; else
+ * FD_MATH_FP32) -> ue_combine_ser. */
 int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_taps, const void* coef,
                     const float* params, long long max_batch, cudaStream_t stream);
 float fd_chain_alpha(const fd_chain* chain);

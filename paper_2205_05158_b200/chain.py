@@ -42,10 +42,11 @@ class Shapes:
 
 class Chain:
     def __init__(self, shapes: Shapes, h_taps, coef, params, device="cuda", max_batch=1, b0=0, B_loc=None,
-                 impair=None, precode_math="simt"):
+                 impair=None, precode_math="auto"):
         """impair (NEXT f3, optional): dict with clip, pa_noise_std, awgn_n0, csi_eta, noise_key, h_err.
         precode_math (split path): "simt" FP32 SIMT, "tf32" TF32 tensor cores, "fp32tc" FP32-accurate
-        split-TF32 tensor cores (the latter two on the precode_pack'ed precoder)."""
+        split-TF32 tensor cores (the latter two on the precode_pack'ed precoder); "auto" = fdpd.auto_precode_math
+        (fp32tc where the tensor-core kernel applies: the split path with U % 4 == 0, U <= 32)."""
         self.sh = shapes
         self.device = torch.device(device)
         dev = self.device
@@ -68,8 +69,8 @@ class Chain:
         else:
             self.h_fd, self.P, self.alpha = fdpd.zf_precoder_build(self.h_taps, shapes.N_ifft, shapes.N_d,
                                                                    shapes.rho, b0=b0, B_loc=self.B_loc)
-        self.precode_math = precode_math
-        self.Ppk = fdpd.precode_pack(self.P) if precode_math != "simt" else None
+        self.precode_math = fdpd.auto_precode_math(shapes.U) if precode_math == "auto" else precode_math
+        self.Ppk = fdpd.precode_pack(self.P) if self.precode_math != "simt" else None
         self.reserve(max_batch)
 
     def _imp(self, sym0):

@@ -26,6 +26,8 @@
 // Layers: IN_MODE 1 reads the complex symbols (2 real channels, padded to K = 8);
 // OUT_MODE 0 writes tanh(D + b) channels-last with a zero halo; OUT_MODE 1 (Cout = 2,
 // N padded to 16) writes the residual s_out = s_in + D + b on the first N_d pixels.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tcgen05.cuh"
 
@@ -52,6 +54,7 @@ struct TcConv {
     int ws, na;               // weight ring slots (9 = all taps resident), A buffers
     int off_a, off_bias, off_bar;   // smem byte offsets (weights at 0)
     int tmem_cols;
+    int dbg;                  // experiments only (FDPD_TC_DBG): 1 = every TMA A copy reads tile 0 of image 0
 };
 
 // Weights W[co][ci][3][3] -> per tap [ci/4][n][4] with n < 2 NP: rows n < NP hold hi(W[n]),
@@ -240,7 +243,8 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP, IN_MODE == 0 && F16>::THR
                     if (elect_one()) {
                         unsigned char* ab = sm + g.off_a + (size_t)buf * abytes;
                         mbar_arrive_expect_tx(&a_full[buf], 2u * GC * plane_bytes);
-                        const uint4* src = a16 + ((size_t)img * (CINP / 4) + (size_t)c * 2 * GC) * g.PP + TC_GLO + qa;
+                        const uint4* src = (g.dbg & 1) ? a16 + (size_t)c * 2 * GC * g.PP + TC_GLO - 1
+                                                       : a16 + ((size_t)img * (CINP / 4) + (size_t)c * 2 * GC) * g.PP + TC_GLO + qa;
 #pragma unroll
                         for (int pl = 0; pl < 2 * GC; ++pl)
                             tma_bulk_g2s(ab + (size_t)pl * g.PL, src + (size_t)pl * g.PP, plane_bytes, &a_full[buf]);
@@ -631,6 +635,11 @@ static TcConv tc_geom(int S, int N_d, int Cin, int Cout, long long n_img) {
     g.Cin = Cin;
     g.Cout = Cout;
     g.n_img = n_img;
+    static const int dbg = [] {
+        const char* e = getenv("FDPD_TC_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    g.dbg = dbg;
     return g;
 }
 
@@ -663,6 +672,15 @@ static size_t tc_plan(TcConv& g, int CINP, int NP, bool f16) {
         return bytes;
     };
     size_t r;
+    // experiment switch (FDPD_TC_WRING=<ws>): stream the weights through a ring of ws slices
+    // and give the freed shared memory to A buffers
+    static const int wring = [] {
+        const char* e = getenv("FDPD_TC_WRING");
+        return e ? atoi(e) : 0;
+    }();
+    if (wring > 0 && wring < NW)
+        for (int na = 6; na >= 2; --na)
+            if ((r = take(wring, na))) return r;
     for (int na = 4; na >= 2; --na)
         if ((r = take(NW, na))) return r;
     for (int na = 4; na >= 2; --na)

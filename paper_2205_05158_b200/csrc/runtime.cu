@@ -20,6 +20,7 @@ struct fd_chain {
     float* params = nullptr;
     float2 *s = nullptr, *s_tilde = nullptr, *y = nullptr, *XPA = nullptr, *yhat = nullptr;
     float2* X = nullptr;   // precoded spectrum [cap][B][N_d] when U >= FD_SPLIT_PRECODE_MIN_U
+    float* Ppk = nullptr;  // precode_pack'ed P for the tensor-core precode (split path, U % 4 == 0, U <= 32)
     uint16_t* idx = nullptr;
     long long* counts = nullptr;
     void* ws_cnn = nullptr;
@@ -68,7 +69,7 @@ int dalloc(T** p, size_t n) {
 void release(fd_chain* c) {
     if (!c) return;
     void* ptrs[] = {c->h_taps, c->coef, c->h_fd, c->P, c->params, c->s, c->s_tilde, c->y,
-                    c->XPA, c->yhat, c->idx, c->counts, c->ws_cnn, c->ws_zf, c->X};
+                    c->XPA, c->yhat, c->idx, c->counts, c->ws_cnn, c->ws_zf, c->X, c->Ppk};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (cudaEvent_t e : c->ev_in)
@@ -118,7 +119,8 @@ int run_chunk(fd_chain* c, const void* s, const uint16_t* tx_idx, long long s0, 
     if (c->X) {
         // many users: tiled precode kernel, then the chain on the precoded spectrum
         float2* X = c->X + s0 * pb;
-        rc = precode(c->P, st, X, n, d.B, d.U, d.N_d, FD_MATH_FP32, stream);
+        rc = c->Ppk ? precode_packed(c->Ppk, st, X, n, d.B, d.U, d.N_d, FD_MATH_FP32_TC, stream)
+                    : precode(c->P, st, X, n, d.B, d.U, d.N_d, FD_MATH_FP32, stream);
         if (rc) return rc;
         rc = chain_txrx_pre(X, c->coef, c->y + s0 * py, XPA, d.orders, d.n_orders, d.L, d.M, n, d.B, d.N_d, d.N_ifft,
                             nullptr, stream);
@@ -181,6 +183,12 @@ int fd_chain_create(fd_chain** out, const fd_chain_desc* desc, const void* h_tap
     // a2: ZF precoder, once per channel realisation (synchronises)
     FD_TRY(zf_precoder_build(c->h_taps, d.T, d.U, d.B, d.N_ifft, d.N_d, d.rho, 0, d.B, c->h_fd, c->P, &c->alpha,
                              c->ws_zf, zf_workspace_bytes(d.N_d), stream));
+    // split path: the FP32-accurate tensor-core precode where it applies (same policy as the
+    // binding's auto_precode_math), on the precoder packed once per channel realisation
+    if (d.U >= FD_SPLIT_PRECODE_MIN_U && d.U % 4 == 0 && d.U <= 32) {
+        FD_TRY(dalloc(&c->Ppk, precode_pack_bytes(d.B, d.U, d.N_d) / sizeof(float)));
+        FD_TRY(precode_pack(c->P, c->Ppk, d.B, d.U, d.N_d, stream));
+    }
     FD_TRY(ensure_batch(c, max_batch));
 #undef FD_TRY
     bool ok = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&

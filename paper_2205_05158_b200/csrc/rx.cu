@@ -108,13 +108,15 @@ __global__ void k_slice(const float2* __restrict__ yhat, const uint16_t* __restr
 #include "combine_tc.cuh"
 
 // Tensor-core channel sum for 9 <= U <= 32 (combine_tc.cuh); process-wide switch
-// (fd_set_combine_path): 0 = auto (tensor cores where they apply), 1 = FP32 SIMT kernels.
-static int g_combine_simt = 0;
+// (fd_set_combine_path): 0 = auto = the FP32 SIMT kernels (measured faster: C5 0.645 vs 0.80 ms
+// per 32 symbols, both latency-bound on their loads), 1 = FP32 SIMT, 2 = tensor cores where
+// they apply.
+static int g_combine_mode = 0;
 
 static bool launch_combine_tc(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d,
                               long long n_sym, int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
                               const SliceParams& sp, bool ser, cudaStream_t st) {
-    if (g_combine_simt || U < 9 || U > 32 || !aligned16(yhat)) return false;
+    if (g_combine_mode != 2 || U < 9 || U > 32 || !aligned16(yhat)) return false;
     CtGeom g{};
     g.B = B;
     g.U = U;
@@ -641,7 +643,8 @@ int ue_combine_ser_ps(const void* XPA, const void* h_fd_all, void* yhat, const f
 }  // extern "C"
 
 extern "C" int fd_set_combine_path(int mode) {
-    FD_REQUIRE(mode == 0 || mode == 1, "fd_set_combine_path: mode=%d (0 = auto, 1 = FP32 SIMT)", mode);
-    fdpd::g_combine_simt = mode;
+    FD_REQUIRE(mode >= 0 && mode <= 2, "fd_set_combine_path: mode=%d (0 = auto, 1 = FP32 SIMT, 2 = tensor cores)",
+               mode);
+    fdpd::g_combine_mode = mode;
     return FD_OK;
 }

@@ -156,7 +156,7 @@ SPLIT_PRECODE_MIN_U = 16
 
 
 def set_combine_path(mode: int):
-    """0 = auto (tensor cores for 9 <= U <= 32), 1 = FP32 SIMT kernels."""
+    """0 = auto (the FP32 SIMT kernels), 1 = FP32 SIMT, 2 = tensor cores for 9 <= U <= 32."""
     _check(lib().fd_set_combine_path(int(mode)))
 
 
@@ -321,6 +321,13 @@ def make_impairments(clip=0.0, pa_noise_std=0.0, awgn_n0=0.0, csi_eta=0.0, noise
 # ----------------------------------------------------------------------------- a3-a5
 MATH_FP32, MATH_TF32, MATH_FP32_TC = 0, 1, 2
 MATH = {"simt": MATH_FP32, "fp32": MATH_FP32, "tf32": MATH_TF32, "fp32tc": MATH_FP32_TC}
+
+
+def auto_precode_math(U: int) -> str:
+    """The precode of the split path (U >= SPLIT_PRECODE_MIN_U): FP32-accurate tensor cores where
+    they apply (U % 4 == 0, U <= 32; measured C5 0.47 vs 0.61 ms per 32 symbols), else FP32 SIMT —
+    the same policy as the native runtime (fd_chain_create)."""
+    return "fp32tc" if U >= SPLIT_PRECODE_MIN_U and U % 4 == 0 and U <= 32 else "simt"
 
 
 def precode(P, s, out=None, math=MATH_FP32):

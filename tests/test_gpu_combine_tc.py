@@ -1,5 +1,5 @@
 """GPU parity of the tensor-core channel sum (Eq. 5) with fused slicing / SER
-through the C ABI (ue_combine, ue_combine_ser; fd_set_combine_path 0 = auto -> tensor cores for
+through the C ABI (ue_combine, ue_combine_ser; fd_set_combine_path 2 = tensor cores for
 9 <= U <= 32) against the fp64 oracle einsum + slicer: y_hat at 2e-5, decisions identical
 outside the 1e-4 band element by element, SER counters equal to the decisions; the SIMT kernel
 (fd_set_combine_path(1)) agrees to 2e-5; accumulate mode adds onto y_hat."""
@@ -64,7 +64,7 @@ def test_combine_ser_tc(F, n, B, U, Nd):
     alpha = float(np.sqrt(np.mean(np.abs(want) ** 2)))                 # z at unit scale
     idx = rng.integers(0, M_qam, size=(n, U, Nd)).astype(np.uint16)
     d_idx = dev(idx.astype(np.int32), torch.int32).to(torch.uint16)
-    F.set_combine_path(0)
+    F.set_combine_path(2)
     dec = torch.zeros((n, U, Nd), dtype=torch.uint16, device="cuda")
     yhat, counts, _ = F.ue_combine_ser(dev(XPA), dev(h), alpha, d_idx, M_qam, dec=dec)
     y = yhat.cpu().numpy()
@@ -78,7 +78,7 @@ def test_combine_ser_tc(F, n, B, U, Nd):
     # the SIMT kernel on the same inputs
     F.set_combine_path(1)
     y_simt = F.ue_combine(dev(XPA), dev(h)).cpu().numpy()
-    F.set_combine_path(0)
+    F.set_combine_path(2)
     assert rel(y, y_simt) < TOL
     # ue_combine (no slicing) and accumulate
     y2 = F.ue_combine(dev(XPA), dev(h))

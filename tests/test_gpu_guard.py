@@ -180,13 +180,13 @@ def test_guard_stages(F, N, Nd):
 
 
 # ============================================================================ a6 channel sum
-@pytest.mark.parametrize("simt", [0, 1])
+@pytest.mark.parametrize("mode", [2, 1])
 @pytest.mark.parametrize("n,B,U,Nd", [(2, 40, 32, 70), (33, 20, 12, 38), (5, 64, 4, 600), (70, 17, 9, 6)])
-def test_guard_combine(F, simt, n, B, U, Nd):
+def test_guard_combine(F, mode, n, B, U, Nd):
     rng = np.random.default_rng(n * B)
     XPA, h = cr(rng, n, B, Nd), cr(rng, U, B, Nd)
     idx = torch.from_numpy(rng.integers(0, 256, (n, U, Nd)).astype(np.uint16)).cuda()
-    F.set_combine_path(simt)
+    F.set_combine_path(mode)
     try:
         yh = Guarded((n, U, Nd), torch.complex64)
         dec = Guarded((n, U, Nd), torch.uint16)

@@ -549,6 +549,49 @@ def test_end_to_end_large(F, name, nsym, pick):
     assert counts[0] == int((dec != inp["idx"]).sum())
 
 
+TOL_TF32 = 2e-3          # north star: "<= 2e-3 (TF32 tensor-core precoding)"
+EPS_TF32 = 5e-3          # SURVEY §8(c) reading A22: TF32 moves z by ~3e-4, so the band is scaled to 5e-3
+
+
+@pytest.mark.parametrize("nsym,pick", [(8, [5]), (512, [0, 509])])
+def test_end_to_end_c3_tf32_precode(F, nsym, pick):
+    """BASELINE configs[2]: C3 with the "TF32 tensor-core precoding variant reported separately"
+    (precode on tcgen05 kind::tf32, one pass, then chain_txrx_pre; bench --split-precode
+    --precode-math tf32).  Against the fp64 oracle: s_tilde at the FP32 bar (the CNN is
+    unchanged), the precoded / PA / received signals at the TF32 bar 2e-3, and decisions
+    identical outside the A22 band (5e-3), the mismatches inside it printed with their boundary
+    distances (north-star band 1e-4 reported)."""
+    from paper_2205_05158_b200.chain import Chain, Shapes
+    cfg = configs.C3
+    inp = gen.make_inputs(cfg, range(nsym))
+    ch = Chain(Shapes.from_config(cfg), inp["h_taps"], inp["coef"], inp["params"], max_batch=nsym,
+               precode_math="tf32")
+    ch.split_precode = True
+    s, idx = dev(inp["s"]), dev(inp["idx"], torch.uint16)
+    dec = torch.zeros(idx.shape, dtype=torch.uint16, device="cuda")
+    yhat, counts, _ = ch.step(s, idx, dec=dec)
+    torch.cuda.synchronize()
+    st, X, y, yh, dg, c = (host(ch.s_tilde[:nsym]), host(ch.X[:nsym]), host(ch.y[:nsym]), host(yhat), host(dec),
+                           host(counts))
+    o = O.run_config(cfg, gen.make_inputs(cfg, pick))
+    assert rel(st[pick], o["s_tilde"]) < TOL
+    e_X, e_y, e_yh = rel(X[pick], o["X"]), rel(y[pick], o["y"]), rel(yh[pick], o["yhat"])
+    print(f"C3 TF32 precode: rel-L2 X {e_X:.2e}, y {e_y:.2e}, yhat {e_yh:.2e}")
+    assert 1e-6 < e_X < TOL_TF32                       # TF32 class, not FP32
+    assert e_y < TOL_TF32 and e_yh < TOL_TF32
+    z, near4 = _near_mask(o["yhat"], o["alpha"], cfg.M_qam, 1e-4)
+    _, near_b = _near_mask(o["yhat"], o["alpha"], cfg.M_qam, EPS_TF32)
+    mism = dg[pick] != o["dec"]
+    cst = 1.0 / np.sqrt(2.0 * (cfg.M_qam - 1) / 3.0)
+    dist = sorted(min(abs(v / cst - 2.0 * np.round(v / cst / 2.0)) * cst for v in (z[tuple(i)].real, z[tuple(i)].imag))
+                  for i in np.argwhere(mism))
+    print(f"C3 TF32 decisions {mism.size}: mismatches {int(mism.sum())} (outside 1e-4: {int((mism & ~near4).sum())}),"
+          f" boundary distances {[round(d, 6) for d in dist[:10]]}")
+    assert not (mism & ~near_b).any()
+    assert c[1] == nsym * cfg.U * cfg.N_d
+    assert c[0] == int((dg != inp["idx"]).sum())
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "P"])
 def test_invariant_zero_cnn_linear_pa(F, name):
     cfg = configs.get(name)

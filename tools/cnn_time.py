@@ -30,7 +30,10 @@ def main():
         n_par = sum(co * ci * 9 + co for ci, co in zip(cfg.chans[:-1], cfg.chans[1:]))
         params = torch.randn(n_par, device="cuda", generator=g) * 0.05
         out = {}
-        for path, code in (("simt", fdpd.CNN_SIMT), ("tensor", fdpd.CNN_TENSOR)):
+        paths = (("simt", fdpd.CNN_SIMT), ("tensor", fdpd.CNN_TENSOR))
+        if os.environ.get("CNN_TIME_TENSOR_ONLY"):
+            paths = paths[1:]
+        for path, code in paths:
             fdpd.set_cnn_path(code)
             o = torch.empty_like(s)
             ws = None
@@ -49,9 +52,11 @@ def main():
                 ts.append(e0.elapsed_time(e1))
             out[path] = (float(np.median(ts)), o.clone())
         fdpd.set_cnn_path(fdpd.CNN_AUTO)
-        d = (out["simt"][1] - out["tensor"][1]).abs().pow(2).sum().sqrt() / out["simt"][1].abs().pow(2).sum().sqrt()
+        d = float("nan")
+        if "simt" in out:
+            d = (out["simt"][1] - out["tensor"][1]).abs().pow(2).sum().sqrt() / out["simt"][1].abs().pow(2).sum().sqrt()
         f = flops(cfg.chans, cfg.U, cfg.N_d, n)
-        print(json.dumps({"config": name, "n_sym": n, "simt_ms": round(out["simt"][0], 4),
+        print(json.dumps({"config": name, "n_sym": n, "simt_ms": round(out["simt"][0], 4) if "simt" in out else None,
                           "tensor_ms": round(out["tensor"][0], 4),
                           "tensor_tflops": round(f / out["tensor"][0] / 1e9, 1),
                           "rel_simt_vs_tensor": float(d)}))

@@ -110,6 +110,7 @@ def case_combine_tc():
     for (n, B, U, Nd) in ((2, 40, 32, 70), (33, 20, 12, 38)):
         XPA, h = cr(rng, n, B, Nd), cr(rng, U, B, Nd)
         idx = torch.from_numpy(rng.integers(0, 256, (n, U, Nd)).astype(np.uint16)).to(DEV)
+        fdpd.set_combine_path(2)
         fdpd.ue_combine(XPA, h)
         fdpd.ue_combine_ser(XPA, h, 1.0, idx, 256)
         fdpd.set_combine_path(1)
