@@ -86,6 +86,19 @@ __global__ void k_tc_weights(const float* __restrict__ W, float* __restrict__ Wg
 // keep an absolute error <= 2^-37 instead of 2^-22 relative: negligible against the sums.
 constexpr float TC_ACT_SCALE = 4096.f;
 
+// tanh for the tensor-core epilogues: tanh x = (e - 1) / (e + 1), e = 2^(2 x log2 e) with
+// ex2.approx (relative error ~2^-22) and a fast reciprocal, |x| clamped to 9 (tanh 9 = 1 - 3e-8):
+// 6 branch-free instructions against tanhf's ~20 with divergent paths, which bound the epilogue
+// warps (measured: tanhf's FFMA / FADD / BSSY / BSYNC were half of the 64 -> 64 layer's warp
+// samples).  Error: absolute <= ~2e-7 for every x (e - 1 cancels near 0, where tanh ~ x), i.e.
+// below the ~2.4e-7 relative resolution of the split-fp16 activations the next layer reads.
+__device__ __forceinline__ float tanh_fast(float x) {
+    const float xc = fminf(fmaxf(x, -9.f), 9.f);
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(xc * 2.8853900817779268f));
+    return __fdividef(e - 1.f, e + 1.f);
+}
+
 __global__ void k_w_scale(const float* __restrict__ W, int n, float* __restrict__ scale) {
     __shared__ float red[32];
     float m = 0.f;
@@ -352,6 +365,56 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP, IN_MODE == 0 && F16>::THR
         const uint64_t wdesc0 = umma_desc(sm_base, 2 * NP * 16, 128);
         int cslot = 0, buf = 0;
         uint32_t cph = 0, aph = 0;
+        if (resident) {
+            // Resident weights: after the first tile's weight waits, a chunk is one elected lane
+            // issuing its 9 taps x KSC x 2 MMAs in a straight line (descriptors = loop-invariant
+            // bases + compile-time offsets).  Measured: with a per-tap elect / syncwarp and the
+            // per-tap descriptor arithmetic the MMA warp's own instruction stream bound the
+            // 64 -> 64 layer (tensor-core smem pipe 64 % busy, the TMA producer waiting for buffers).
+            uint64_t toff[9];
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) toff[tap] = (uint64_t)((tap / 3) * WP + (tap % 3));
+            for (int i = 0; i < my_tiles; ++i) {
+                const int acc = i & 1;
+                if (i >= 2) mbar_wait(&acc_empty[acc], (uint32_t)(((i >> 1) - 1) & 1));
+                const uint32_t d = tmem + (uint32_t)acc * (4 * NP);
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) {
+                    mbar_wait(&a_full[buf], aph);
+                    if (i == 0)
+                        for (int tap = 0; tap < 9; ++tap) mbar_wait(&wfull[c * 9 + tap], 0u);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t abase = adesc0 + (uint64_t)(((uint32_t)buf * abytes) >> 4);
+                        const uint64_t wbase = wdesc0 + (uint64_t)(((uint32_t)(c * 9) * WCB) >> 4);
+#pragma unroll
+                        for (int tap = 0; tap < 9; ++tap) {
+                            const uint64_t at = abase + toff[tap];
+                            const uint64_t wb = wbase + (uint64_t)((tap * WCB) >> 4);
+                            const uint32_t dt = d + (tap >= 5 ? 2u * NP : 0u);   // tap groups, see below
+#pragma unroll
+                            for (int k = 0; k < KSC; ++k) {
+                                const uint64_t ahi = at + (uint64_t)(2u * k * PL16);
+                                const uint64_t alo = ahi + (uint64_t)(GC * PL16);
+                                const uint64_t b = wb + (uint64_t)(2 * k * 2 * NP);
+                                const uint32_t accum = (c | k) != 0 || (tap != 0 && tap != 5) ? 1u : 0u;
+                                if constexpr (F16) {
+                                    mma_f16(dt, ahi, b, IDESC, accum);
+                                    mma_f16(dt + NP, alo, b, IDESC_LO, 1u);
+                                } else {
+                                    mma_tf32(dt, ahi, b, IDESC, accum);
+                                    mma_tf32(dt + NP, alo, b, IDESC_LO, 1u);
+                                }
+                            }
+                        }
+                        umma_commit(&a_empty[buf]);
+                        if (c == NCH - 1) umma_commit(&acc_full[acc]);
+                    }
+                    __syncwarp();
+                    if (++buf == g.na) { buf = 0; aph ^= 1u; }
+                }
+            }
+        } else
         for (int i = 0; i < my_tiles; ++i) {
             const int acc = i & 1;
             if (i >= 2) mbar_wait(&acc_empty[acc], (uint32_t)(((i >> 1) - 1) & 1));
@@ -432,10 +495,15 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP, IN_MODE == 0 && F16>::THR
                     tmem_ld8(tbase + NP + c0, w);
                     tmem_ld8(tbase + 2 * NP + c0, v2);
                     tmem_ld8(tbase + 3 * NP + c0, w2);
+                    // halo / pad pixels: x 0 (a multiply, not a per-element branch: the ternary
+                    // compiled to a BSSY / BSYNC region with the bias load inside, per element)
+                    const float4 b0 = *reinterpret_cast<const float4*>(bsm + c0);
+                    const float4 b1 = *reinterpret_cast<const float4*>(bsm + c0 + 4);
+                    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    const float keep = interior ? TC_ACT_SCALE : 0.f;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        v[j] = interior ? TC_ACT_SCALE * tanhf(((v[j] + v2[j]) + (w[j] + w2[j])) * dscale + bsm[c0 + j])
-                                        : 0.f;
+                        v[j] = keep * tanh_fast(((v[j] + v2[j]) + (w[j] + w2[j])) * dscale + bb[j]);
                     uint4 hi, lo;
                     split_f16x2(v[0], v[1], hi.x, lo.x);
                     split_f16x2(v[2], v[3], hi.y, lo.y);
@@ -470,9 +538,13 @@ __global__ void __launch_bounds__(TcRoles<IN_MODE, NP, IN_MODE == 0 && F16>::THR
                     tmem_ld8(tbase + NP + c0, w);          //           A_hi W_lo + A_lo W_hi
                     tmem_ld8(tbase + 2 * NP + c0, v2);     // taps 5-8
                     tmem_ld8(tbase + 3 * NP + c0, w2);
+                    const float4 b0 = *reinterpret_cast<const float4*>(bsm + c0);
+                    const float4 b1 = *reinterpret_cast<const float4*>(bsm + c0 + 4);
+                    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    const float keep = interior ? 1.f : 0.f;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        v[j] = interior ? tanhf(((v[j] + v2[j]) + (w[j] + w2[j])) * dscale + bsm[c0 + j]) : 0.f;
+                        v[j] = keep * tanh_fast(((v[j] + v2[j]) + (w[j] + w2[j])) * dscale + bb[j]);
                     if (pos < g.q_end) {
                         reinterpret_cast<float4*>(o + c0)[0] = make_float4(v[0], v[1], v[2], v[3]);
                         reinterpret_cast<float4*>(o + c0)[1] = make_float4(v[4], v[5], v[6], v[7]);
