@@ -288,6 +288,7 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     fdpd.lib()
     fdpd.set_combine_path({"auto": 0, "simt": 1, "tc": 2}[args.combine])
+    fdpd.set_gmp_path({"auto": 0, "simt": 1, "tc": 2}[args.gmp])
     n = batch_of(cfg, args)
     symbols = D.symbol_range(n, rank)          # Mode S, weak scaling
     inp = gen.make_inputs(cfg, symbols)
@@ -544,6 +545,8 @@ def run_antenna(args, cfg):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     fdpd.lib()
+    fdpd.set_combine_path({"auto": 0, "simt": 1, "tc": 2}[args.combine])
+    fdpd.set_gmp_path({"auto": 0, "simt": 1, "tc": 2}[args.gmp])
     n = batch_of(cfg, args)
     micro = 2 if n % 2 == 0 else 1
     symbols = D.symbol_range(n, rank)
@@ -679,6 +682,8 @@ def main():
                     help="split-path precode: FP32 SIMT, TF32 tensor cores, or FP32-accurate split-TF32 tensor cores")
     ap.add_argument("--combine", default="auto", choices=["auto", "simt", "tc"],
                     help="channel sum: auto (= the FP32 SIMT kernels), simt, or tc (tensor cores for 9 <= U <= 32)")
+    ap.add_argument("--gmp", default="auto", choices=["auto", "simt", "tc"],
+                    help="GMP of the N = 16384 cluster chain: auto, FP32 SIMT, or tensor cores (C4 / C5 shape)")
     ap.add_argument("--mode", default="auto", choices=["auto", "symbol", "antenna"],
                     help="multi-GPU partitioning: symbol batches (Mode S) or antennas (Mode A); auto = antenna "
                          "for C5 at N > 1 (BASELINE configs[4]), else symbol")

@@ -20,14 +20,19 @@
 // again a contiguous-around-DC set of N_d / 2 local bins, with local data index jl <->
 // global data index j = 2 jl + c, so the pruned local transforms of chain.cuh apply as is.
 #include <cooperative_groups.h>
+#include <cuda_bf16.h>
 
 #include "chain.cuh"
+#include "tcgen05.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace fdpd {
 
-template <int LOG2NL, int KP, int L, int M, int RS, int PZ>
+#include "gmp_tc.cuh"
+
+// TCG: the GMP on the tensor cores (gmp_tc.cuh; the C4 / C5 shape at N_L = 8192 only).
+template <int LOG2NL, int KP, int L, int M, int RS, int PZ, bool TCG = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(), fft_min_blocks<LOG2NL>())
     k_chain_cl(const float2* __restrict__ P, const float2* __restrict__ s, const float2* __restrict__ coef,
                float2* __restrict__ y, float2* __restrict__ XPA, const float2* __restrict__ tw_l,
@@ -54,7 +59,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
 
     // ---- precode (Eq. 1) of this CTA's data bins: local jl <-> global j = 2 jl + c
     float2* xs = reinterpret_cast<float2*>(esm);
-    stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
+    if constexpr (!TCG) stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
     if (imp.precoded) {
         const float2* Xr = P + nb * N_d + c;
         for (int jl = tid; jl < NdL; jl += T) xs[jl] = __ldg(Xr + 2 * jl);
@@ -137,18 +142,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     }
     cl.sync();                                   // the partner has read our Y
     using Lay = RunLayout<RS>;
+    if constexpr (TCG) {
 #pragma unroll
-    for (int j = 0; j < VPT; ++j) {
-        const int i = tid + T * j;
-        usm[Lay::u_phys(i)] = v[j];
-        esm[Lay::e_phys(i)] = fmaf(v[j].x, v[j].x, v[j].y * v[j].y);
+        for (int j = 0; j < VPT; ++j) usm[tid + T * j] = v[j];          // natural order
+    } else {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int i = tid + T * j;
+            usm[Lay::u_phys(i)] = v[j];
+            esm[Lay::e_phys(i)] = fmaf(v[j].x, v[j].x, v[j].y * v[j].y);
+        }
     }
     cl.sync();                                   // both halves' u / e staged (GMP halo reads)
 
     // ---- GMP on this half; y (global) gets samples [c N_L, (c + 1) N_L)
     float2* yo = y + nb * N;
-    gmp_runs_symbol<KP, L, M, RS, false, true>(usm, esm, cf, NL, yo + (size_t)c * NL, tid, T, nullptr, im, nbase,
-                                               cl.map_shared_rank(usm, c ^ 1), cl.map_shared_rank(esm, c ^ 1));
+    if constexpr (TCG) {
+        static_assert(T == 256, "gmp_tc_half runs 256 threads");
+        gmp_tc_half<KP, L, M>(usm, cl.map_shared_rank(usm, c ^ 1), coef + (size_t)b * d.n_coef, cf, d.n_coef,
+                              reinterpret_cast<unsigned char*>(esm), NL, yo + (size_t)c * NL, tid, im, nbase);
+    } else {
+        gmp_runs_symbol<KP, L, M, RS, false, true>(usm, esm, cf, NL, yo + (size_t)c * NL, tid, T, nullptr, im, nbase,
+                                                   cl.map_shared_rank(usm, c ^ 1), cl.map_shared_rank(esm, c ^ 1));
+    }
     cl.sync();   // the partner is done with our u / e, and both halves of y are written (cluster acq/rel)
 
     // ---- receive DFT at the parity-c bins: DFT_{N_L}((y_0 + (-1)^c y_1) W_N^{c m})
@@ -168,7 +184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     for (int jl = tid; jl < NdL; jl += T) xo[2 * jl] = cscale(usm[pidx(data_to_bin(jl, NL, NdL))], sc);
 }
 
-template <int LOG2NL, int KP, int L, int M, int RS, int PZ>
+template <int LOG2NL, int KP, int L, int M, int RS, int PZ, bool TCG = false>
 static int launch_cl_one(const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
                          long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp, cudaStream_t st) {
     constexpr int NL = 1 << LOG2NL;
@@ -177,18 +193,30 @@ static int launch_cl_one(const float2* P, const float2* s, const float2* coef, f
     if (!tw_l || !tw_g) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
     const ChainSmem lay = chain_smem(NL, N_d / 2, d, false);
     if (lay.bytes > 227 * 1024) return fail_arg("chain_cl: shared-memory footprint %d B too large", lay.bytes);
-    set_smem(k_chain_cl<LOG2NL, KP, L, M, RS, PZ>, lay.bytes);
-    k_chain_cl<LOG2NL, KP, L, M, RS, PZ><<<(unsigned)(2 * n_sym * B), fft_threads<LOG2NL>(), lay.bytes, st>>>(
+    if constexpr (TCG) {
+        if (lay.off_cf - lay.off_e < GT_BYTES) return fail_arg("chain_cl: tensor-core GMP needs %d B of scratch", GT_BYTES);
+    }
+    set_smem(k_chain_cl<LOG2NL, KP, L, M, RS, PZ, TCG>, lay.bytes);
+    k_chain_cl<LOG2NL, KP, L, M, RS, PZ, TCG><<<(unsigned)(2 * n_sym * B), fft_threads<LOG2NL>(), lay.bytes, st>>>(
         P, s, coef, y, XPA, tw_l, tw_g, B, U, N_d, (float)(1.0 / std::sqrt((double)(2 * NL))), d, imp);
     return check_launch("chain_txrx (cluster split)");
 }
+
+// GMP implementation of the cluster chain (fd_set_gmp_path): 0 = auto (the tensor cores where
+// they apply: the C4 / C5 shape at N = 16384), 1 = FP32 SIMT, 2 = tensor cores where they apply.
+static int g_gmp_path = 1;
 
 template <int LOG2NL, int PZ>
 static int cl_variant(int variant, const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
                       long long n_sym, int B, int U, int N_d, const GmpDesc& d, const Impair& imp, cudaStream_t st) {
     switch (variant) {
         case 2: return launch_cl_one<LOG2NL, 4, 4, 2, 4, PZ>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
-        case 3: return launch_cl_one<LOG2NL, 5, 6, 3, 4, PZ>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+        case 3:
+            if constexpr (LOG2NL == 13) {
+                if (g_gmp_path != 1)
+                    return launch_cl_one<LOG2NL, 5, 6, 3, 4, PZ, true>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
+            }
+            return launch_cl_one<LOG2NL, 5, 6, 3, 4, PZ>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
         default: return -1;
     }
 }
@@ -217,6 +245,12 @@ int launch_chain_cluster(int log2n, int variant, const float2* P, const float2* 
 }
 
 }  // namespace fdpd
+
+extern "C" int fd_set_gmp_path(int mode) {
+    FD_REQUIRE(mode >= 0 && mode <= 2, "fd_set_gmp_path: mode=%d (0 = auto, 1 = FP32 SIMT, 2 = tensor cores)", mode);
+    fdpd::g_gmp_path = mode;
+    return FD_OK;
+}
 
 extern "C" int fd_set_chain_split(int mode) {
     FD_REQUIRE(mode == 0 || mode == 1, "fd_set_chain_split: mode=%d (0 = auto, 1 = off)", mode);

@@ -86,9 +86,23 @@ const float2* twiddle_table(int N, cudaStream_t stream) {
     return w;
 }
 
+// Test support: fill the whole shared memory of every SM with a pattern (uninitialised-read
+// detection: a kernel whose output changes after this ran reads shared memory it never wrote).
+__global__ void k_poison_smem(uint32_t pattern, int words) {
+    extern __shared__ uint32_t sw[];
+    for (int i = threadIdx.x; i < words; i += blockDim.x) sw[i] = pattern;
+}
+
 }  // namespace fdpd
 
 extern "C" {
+
+int fd_debug_poison_smem(unsigned pattern, cudaStream_t stream) {
+    const int bytes = 227 * 1024;
+    cudaFuncSetAttribute(fdpd::k_poison_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    fdpd::k_poison_smem<<<4 * 148, 1024, bytes, stream>>>(pattern, bytes / 4);
+    return fdpd::check_launch("fd_debug_poison_smem");
+}
 
 const char* fd_last_error(void) { return fdpd::g_err.c_str(); }
 

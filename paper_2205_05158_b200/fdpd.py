@@ -51,6 +51,8 @@ SIGNATURES = {
     "fd_set_cnn_path": (_i, [_i]),
     "fd_set_cnn_tc_precision": (_i, [_i]),
     "fd_set_chain_split": (_i, [_i]),
+    "fd_set_gmp_path": (_i, [_i]),
+    "fd_debug_poison_smem": (_i, [C.c_uint, _vp]),
     "fd_set_combine_path": (_i, [_i]),
     "fdcnn_workspace_bytes": (_sz, [_ip, _i, _ll, _i, _i]),
     "fdcnn_forward": (_i, [_vp, _ip, _i, _vp, _vp, _vp, _sz, _ll, _i, _i, _vp]),
@@ -177,6 +179,18 @@ def qam_map(idx, M_qam, out=None):
     out = torch.empty(idx.shape, dtype=torch.complex64, device=idx.device) if out is None else out
     _check(lib().qam_map(_ptr(idx), _ptr(out), idx.numel(), int(M_qam), _stream(idx)))
     return out
+
+
+def set_gmp_path(mode: int):
+    """GMP of the N = 16384 cluster chain (include/fdpd.h fd_set_gmp_path): 0 = auto, 1 = FP32 SIMT,
+    2 = tensor cores (C4 / C5 GMP shape).  Process-wide."""
+    _check(lib().fd_set_gmp_path(int(mode)))
+
+
+def debug_poison_smem(pattern: int):
+    """Test support (include/fdpd.h fd_debug_poison_smem): shared memory of every SM := pattern."""
+    _check(lib().fd_debug_poison_smem(int(pattern) & 0xFFFFFFFF,
+                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
 
 def set_chain_split(mode: int):

@@ -5,9 +5,12 @@ compute-sanitizer, which this GPU pool does not allow:
     whose head and tail are filled with a sentinel bit pattern; after the call the sentinels
     must be intact (an out-of-bounds store of any kernel — a TMA bulk copy, a tile epilogue,
     a halo-zeroing loop, a counter — changes them);
-  * determinism: the same call repeated on the same inputs gives bit-identical outputs (a
-    missing barrier / mbarrier wait in a warp-specialised pipeline, or a shared-memory race,
-    shows up as run-to-run differences);
+  * determinism: the same call repeated on the same inputs gives bit-identical outputs, with the
+    shared memory of every SM poisoned with a different pattern before each repeat
+    (fd_debug_poison_smem): a missing barrier / mbarrier wait in a warp-specialised pipeline, a
+    shared-memory race, a read of shared memory the kernel never wrote, or a live mbarrier whose
+    memory is reused (this found one: the tensor-core GMP's barriers under the receive DFT's
+    scratch) shows up as run-to-run differences;
   * tiny and ragged shapes that still take each kernel's real code path.
 Parity itself is in test_gpu_parity / test_gpu_precode_tc / test_gpu_combine_tc."""
 import numpy as np
@@ -64,10 +67,17 @@ def cr(rng, *shape, scale=1.0):
     return torch.from_numpy(x.astype(np.complex64)).to("cuda")
 
 
+POISON = (0x00000000, 0x7FC0DEAD, 0x4E6E6B28, 0xFFFFFFFF)
+
+
 def repeat_equal(fn, n=3):
-    """fn() -> tensor (or tuple); n runs must be bit-identical."""
+    """fn() -> tensor (or tuple); n runs, shared memory poisoned differently before each, must be
+    bit-identical."""
+    from paper_2205_05158_b200 import fdpd
+    fdpd.debug_poison_smem(POISON[0])
     ref = [t.clone() for t in _as_tuple(fn())]
-    for _ in range(n - 1):
+    for i in range(n - 1):
+        fdpd.debug_poison_smem(POISON[1 + i % 3])
         got = _as_tuple(fn())
         for a, b in zip(ref, got):
             assert torch.equal(a.view(torch.uint8) if a.is_complex() else a, b.view(torch.uint8) if b.is_complex() else b)
@@ -139,7 +149,8 @@ def test_guard_precode(F, math, n, B, U, Nd):
 
 
 # ============================================================================ a4-a6 fused chains
-@pytest.mark.parametrize("name,n,B", [("C1", 3, None), ("C2", 2, 5), ("C3", 1, 3), ("C5", 1, 2)])
+@pytest.mark.parametrize("name,n,B", [("C1", 3, None), ("C2", 2, 5), ("C3", 1, 3), ("C5", 1, 2), ("C5", 4, 40),
+                                      ("C4", 2, 24)])
 def test_guard_chain(F, name, n, B):
     cfg = configs.get(name)
     B = B or cfg.B
@@ -152,6 +163,16 @@ def test_guard_chain(F, name, n, B):
     repeat_equal(lambda: F.chain_txrx_pre(X, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft, y=y.t, XPA=XPA.t))
     y.check("chain_txrx_pre y")
     XPA.check("chain_txrx_pre XPA")
+    if cfg.N_ifft == 16384:                   # the tensor-core GMP of the cluster chain
+        F.set_gmp_path(2)
+        try:
+            y4 = Guarded((n, B, cfg.N_ifft), torch.complex64)
+            XPA4 = Guarded((n, B, cfg.N_d), torch.complex64)
+            repeat_equal(lambda: F.chain_txrx_pre(X, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft, y=y4.t, XPA=XPA4.t))
+            y4.check("chain_txrx_pre (tensor-core GMP) y")
+            XPA4.check("chain_txrx_pre (tensor-core GMP) XPA")
+        finally:
+            F.set_gmp_path(0)
     if cfg.U <= 8:
         P = cr(rng, B, cfg.U, cfg.N_d, scale=0.1)
         st = cr(rng, n, cfg.U, cfg.N_d)

@@ -93,6 +93,9 @@ def case_chain_cl():
     coef = torch.from_numpy(inp["coef"][:2]).to(DEV)
     X = cr(rng, 1, 2, cfg.N_d, scale=0.3)
     fdpd.chain_txrx_pre(X, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+    fdpd.set_gmp_path(2)
+    fdpd.chain_txrx_pre(X, coef, cfg.orders, cfg.L, cfg.M, cfg.N_ifft)
+    fdpd.set_gmp_path(0)
 
 
 def case_precode_tc():
