@@ -220,8 +220,8 @@ int chain_txrx_ex(const void* P, const void* s_tilde, const void* coef, void* y,
  * step across the pair, DSMEM exchange).  mode 0 = auto (default), 1 = never (single-CTA kernel).
  * Process-wide; returns FD_ERR_ARG for other modes. */
 int fd_set_chain_split(int mode);
-/* GMP implementation of the cluster-split chain (process-wide): 0 = auto, 1 = FP32 SIMT
- * (default), 2 = the tensor cores where they apply — the C4 / C5 shape (orders {1,3,5,7,9},
+/* GMP implementation of the cluster-split chain (process-wide): 0 = auto (default; = FP32 SIMT,
+ * measured faster), 1 = FP32 SIMT, 2 = the tensor cores where they apply — the C4 / C5 shape (orders {1,3,5,7,9},
  * L = 6, M = 3) at N_ifft = 16384: Eq. 9's feature contraction G_l(q) = sum_{d,k} C_l[d][k]
  * e_{q+d}^k as shifted-row MMAs, tf32 hi + bf16 lo envelope powers against tf32 hi + lo
  * coefficients (FP32-accurate, no range scaling).  FD_ERR_ARG for other modes. */

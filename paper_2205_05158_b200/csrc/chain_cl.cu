@@ -160,7 +160,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     if constexpr (TCG) {
         static_assert(T == 256, "gmp_tc_half runs 256 threads");
         gmp_tc_half<KP, L, M>(usm, cl.map_shared_rank(usm, c ^ 1), coef + (size_t)b * d.n_coef, cf, d.n_coef,
-                              reinterpret_cast<unsigned char*>(esm), NL, yo + (size_t)c * NL, tid, im, nbase);
+                              reinterpret_cast<unsigned char*>(esm),
+                              reinterpret_cast<const unsigned char*>(cl.map_shared_rank(esm, c ^ 1)), NL,
+                              yo + (size_t)c * NL, tid, im, nbase);
     } else {
         gmp_runs_symbol<KP, L, M, RS, false, true>(usm, esm, cf, NL, yo + (size_t)c * NL, tid, T, nullptr, im, nbase,
                                                    cl.map_shared_rank(usm, c ^ 1), cl.map_shared_rank(esm, c ^ 1));
@@ -202,9 +204,10 @@ static int launch_cl_one(const float2* P, const float2* s, const float2* coef, f
     return check_launch("chain_txrx (cluster split)");
 }
 
-// GMP implementation of the cluster chain (fd_set_gmp_path): 0 = auto (the tensor cores where
-// they apply: the C4 / C5 shape at N = 16384), 1 = FP32 SIMT, 2 = tensor cores where they apply.
-static int g_gmp_path = 1;
+// GMP implementation of the cluster chain (fd_set_gmp_path): 0 = auto (= FP32 SIMT: the
+// tensor-core GMP is correct but measured slower), 1 = FP32 SIMT, 2 = tensor cores
+// where they apply (the C4 / C5 shape at N = 16384).
+static int g_gmp_path = 0;
 
 template <int LOG2NL, int PZ>
 static int cl_variant(int variant, const float2* P, const float2* s, const float2* coef, float2* y, float2* XPA,
@@ -213,7 +216,7 @@ static int cl_variant(int variant, const float2* P, const float2* s, const float
         case 2: return launch_cl_one<LOG2NL, 4, 4, 2, 4, PZ>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
         case 3:
             if constexpr (LOG2NL == 13) {
-                if (g_gmp_path != 1)
+                if (g_gmp_path == 2)
                     return launch_cl_one<LOG2NL, 5, 6, 3, 4, PZ, true>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);
             }
             return launch_cl_one<LOG2NL, 5, 6, 3, 4, PZ>(P, s, coef, y, XPA, n_sym, B, U, N_d, d, imp, st);

@@ -21,40 +21,53 @@
 // 6 MMAs per 128 samples against ~205 FFMA2 per sample on the FP32 pipe.  The constant term
 // a_{1,l} (order 1, power 0) is added in the epilogue.
 //
-// Per CTA (its N_L samples) in chunks of 256 (two M = 128 tiles), all 256 threads, software-
-// pipelined over two feature buffers and two TMEM accumulators (MMA(k + 1) runs while the
-// threads finish chunk k and build the features of chunk k + 2):
-//   1. features of samples [q0 - 4, q0 + 261): the tf32 buffer Fp (row r = hi(q), q = q0 - 4 + r;
-//      the MMA's second K plane is the next row: descriptor LBO = 16 B) and the bf16 buffer Fq
-//      (row r = lo(q), lo(q + 1); second K plane two rows on: LBO = 32 B) — one 16-byte row per
-//      sample and buffer; samples outside [0, N_L) are the partner CTA's (distributed shared
-//      memory; the symbol is circular, A13);
-//   2. one thread issues the 12 MMAs into the chunk's TMEM accumulator (two tiles x 32 columns)
-//      and commits to the chunk's mbarrier;
-//   3. thread = sample: G_l = D[2l + c] + D[16 + 2l + c] + a_{1,l}, z_l = u_q G_l (packed FP32);
-//   4. y_q = sum_l z_l(q - l): shuffles inside the warp's 32 samples, the previous group's last
+// Per CTA (its N_L samples) in chunks of 512 (four M = 128 tiles), all 256 threads, with two
+// TMEM accumulators so that the MMAs of chunk k + 1 run under the epilogue of chunk k:
+//   1. (after MMA(k) completed) features of chunk k + 1, samples [q0 - 4, q0 + 517): the tf32
+//      buffer Fp (row r = hi(q), q = q0 - 4 + r; the MMA's second K plane is the next row:
+//      descriptor LBO = 16 B) and the bf16 buffer Fq (row r = lo(q), lo(q + 1); second K plane
+//      two rows on: LBO = 32 B) — one 16-byte row per sample and buffer; samples outside
+//      [0, N_L) are the partner CTA's (distributed shared memory; the symbol is circular, A13);
+//   2. lane 0 of warps 0..3 issues tile j = warp's 6 MMAs of chunk k + 1 into its accumulator and
+//      commits (the chunk's mbarrier counts the four commits);
+//   3. thread = sample (two 32-sample groups per warp): G_l = D[2l + c] + D[16 + 2l + c] + a_{1,l},
+//      z_l = u_q G_l;
+//   4. y_q = sum_l z_l(q - l): shuffles inside each group of 32 samples, the previous group's last
 //      six samples through a small shared-memory carry (the first group of the half takes the
 //      partner's last six samples, evaluated on the FP32 pipe before the loop).
 // (Included inside namespace fdpd by chain_cl.cu.)
 #pragma once
 
-constexpr int GT_CH = 256;                         // samples per chunk (two M = 128 tiles)
+constexpr int GT_CH = 512;                         // samples per chunk (four M = 128 tiles)
+constexpr int GT_TILES = GT_CH / 128;
+constexpr int GT_GROUPS = GT_CH / 32;              // 32-sample groups per chunk
 constexpr int GT_R = GT_CH + 8;                    // feature rows per chunk
 constexpr int GT_BUF = GT_R * 16;                  // bytes of one feature buffer (one 16-byte row per sample)
-constexpr int GT_FP = 0;                           // tf32 hi features [2 chunks]
-constexpr int GT_FQ = GT_FP + 2 * GT_BUF;          // bf16 lo features [2 chunks]
-constexpr int GT_B1 = GT_FQ + 2 * GT_BUF;          // 4 x [32 rows][2 planes] tf32 coefficients
+constexpr int GT_FP = 0;                           // tf32 hi features
+constexpr int GT_FQ = GT_FP + GT_BUF;              // bf16 lo features
+constexpr int GT_B1 = GT_FQ + GT_BUF;              // 4 x [32 rows][2 planes] tf32 coefficients
 constexpr int GT_B1_MAT = 2 * 32 * 16;
 constexpr int GT_B2 = GT_B1 + 4 * GT_B1_MAT;       // 2 x [16 rows][2 planes] bf16 coefficients
 constexpr int GT_B2_MAT = 2 * 16 * 16;
-constexpr int GT_ZC = GT_B2 + 2 * GT_B2_MAT;       // carries: [2][8 groups][6 taps l = 1..6][6] float2
-constexpr int GT_A0 = GT_ZC + 2 * 8 * 6 * 6 * 8;   // a_{1,l}, l = 0..6 (float2)
+constexpr int GT_ZC = GT_B2 + 2 * GT_B2_MAT;       // carries: [2][groups][6 taps l = 1..6][6] float2
+constexpr int GT_A0 = GT_ZC + 2 * GT_GROUPS * 6 * 6 * 8;   // a_{1,l}, l = 0..6 (float2)
 constexpr int GT_BAR = GT_A0 + 8 * 8;              // 2 mbarriers + TMEM address
 constexpr int GT_BYTES = GT_BAR + 32;
+constexpr int GT_TMEM = 2 * GT_TILES * 32;         // two accumulators x four tiles x 32 columns
 
 // Instruction descriptor: D f32, A / B bf16, K-major, M = 128, N = n (kind::f16, K = 16).
 __host__ __device__ constexpr uint32_t idesc_bf16_m128(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+// Round a finite fp32 to tf32 (nearest, ties away) with two integer ops (cvt.rna.tf32.f32 also
+// checks for inf / NaN: four instructions; the envelope powers and coefficients are finite).
+__device__ __forceinline__ float tf32_fin(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
@@ -94,15 +107,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int KP, int L, int M>
 __device__ void gmp_tc_half(const float2* __restrict__ usm, const float2* __restrict__ usm_r,
                             const float2* __restrict__ cg, float2* __restrict__ cs, int n_coef,
-                            unsigned char* __restrict__ sm, int NL, float2* __restrict__ y, int tid,
-                            const Impair* im, unsigned long long nbase) {
+                            unsigned char* __restrict__ sm, const unsigned char* __restrict__ sm_r, int NL,
+                            float2* __restrict__ y, int tid, const Impair* im, unsigned long long nbase) {
     static_assert(KP == 5 && L == 6 && M == 3, "tensor-core GMP: the C4 / C5 shape only");
     constexpr int T = 256;
     const int warp = tid >> 5, lane = tid & 31;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + GT_BAR);          // [2]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + GT_BAR + 16);
     float2* zc = reinterpret_cast<float2*>(sm + GT_ZC);
-    float2* a0 = reinterpret_cast<float2*>(sm + GT_A0);
     auto u_at = [&](int q) -> float2 {     // circular over the two halves
         return q < 0 ? usm_r[q + NL] : (q >= NL ? usm_r[q - NL] : usm[q]);
     };
@@ -119,8 +131,8 @@ __device__ void gmp_tc_half(const float2* __restrict__ usm, const float2* __rest
             if (l <= L && d <= M) {
                 const float2 cc = gmp_tc_coef<KP, L, M>(cs, l, d, k);
                 const float x = c ? cc.y : cc.x;
-                const float hi = tf32_rna(x);
-                v = n < 16 ? hi : tf32_rna(x - hi);
+                const float hi = tf32_fin(x);
+                v = n < 16 ? hi : tf32_fin(x - hi);
             }
             // K-major core-matrix layout: plane kk / 4, row n, element kk % 4
             b1[(size_t)s1 * (GT_B1_MAT / 4) + (kk >> 2) * (32 * 4) + n * 4 + (kk & 3)] = v;
@@ -136,137 +148,143 @@ __device__ void gmp_tc_half(const float2* __restrict__ usm, const float2* __rest
             }
             b2[(size_t)s2 * (GT_B2_MAT / 2) + (kk >> 3) * (16 * 8) + n * 8 + (kk & 7)] = __float2bfloat16_rn(v);
         }
-        if (tid <= L) a0[tid] = cs[tid];                       // a_{1,l}
-        // the partner's last six samples (q = -6 .. -1): z_l(q) = u_q G_l(q) for l = 1..6 on the
-        // FP32 pipe, as the carry of the group before chunk 0 (zc[1][7])
-        if (tid < 6 * L) {
-            const int i = tid / L, l = tid % L + 1, q = -6 + i;
-            float ew[2 * M + 1];
-#pragma unroll
-            for (int d = -M; d <= M; ++d) {
-                const float2 uu = u_at(q + d);
-                ew[d + M] = fmaf(uu.x, uu.x, uu.y * uu.y);
-            }
-            float2 G = cs[l];                                 // a_{1,l}
-#pragma unroll
-            for (int d = -M; d <= M; ++d) {
-                float ek = 1.f;
-#pragma unroll
-                for (int k = 1; k < KP; ++k) {
-                    ek *= ew[d + M];
-                    const float2 cc = gmp_tc_coef<KP, L, M>(cs, l, d, k);
-                    G.x = fmaf(cc.x, ek, G.x);
-                    G.y = fmaf(cc.y, ek, G.y);
-                }
-            }
-            zc[((1 * 8 + 7) * 6 + (l - 1)) * 6 + i] = cmul(u_at(q), G);
-        }
         if (tid == 0) {
-            mbar_init(&bar[0], 1);
-            mbar_init(&bar[1], 1);
+            mbar_init(&bar[0], GT_TILES);                 // one commit per tile
+            mbar_init(&bar[1], GT_TILES);
         }
-        if (warp == 0) tmem_alloc(tslot, 128);
+        if (warp == 0) tmem_alloc(tslot, GT_TMEM);
     }
     const uint32_t sbase = smem_u32(sm);
     constexpr uint32_t ID1 = idesc_tf32_m128(32), ID2 = idesc_bf16_m128(16);
     const int nch = NL / GT_CH;
+    uint4* const fp = reinterpret_cast<uint4*>(sm + GT_FP);
+    uint2* const fq = reinterpret_cast<uint2*>(sm + GT_FQ);
 
-    // features of chunk ch into buffer ch & 1
+    // features of chunk ch: sample rs <-> q = q0 - 4 + rs writes Fp row rs, Fq row rs (first
+    // half) and Fq row rs - 1 (second half)
+    auto feature = [&](int rs, float2 uu) {
+        const float e1 = fmaf(uu.x, uu.x, uu.y * uu.y), e2 = e1 * e1, e3 = e2 * e1, e4 = e2 * e2;
+        const float h1 = tf32_fin(e1), h2 = tf32_fin(e2), h3 = tf32_fin(e3), h4 = tf32_fin(e4);
+        const uint2 lv = make_uint2(bf16x2_bits(e1 - h1, e2 - h2), bf16x2_bits(e3 - h3, e4 - h4));
+        if (rs < GT_R) {
+            fp[rs] = make_uint4(__float_as_uint(h1), __float_as_uint(h2), __float_as_uint(h3), __float_as_uint(h4));
+            fq[2 * rs] = lv;
+        }
+        if (rs >= 1) fq[2 * rs - 1] = lv;
+    };
     auto features = [&](int ch) {
-        const int q0 = ch * GT_CH;
-        const bool edge = ch == 0 || ch == nch - 1;
-        uint4* fp = reinterpret_cast<uint4*>(sm + GT_FP + (ch & 1) * GT_BUF);
-        uint2* fq = reinterpret_cast<uint2*>(sm + GT_FQ + (ch & 1) * GT_BUF);
-        for (int rs = tid; rs < GT_R + 1; rs += T) {
-            const int q = q0 - 4 + rs;
-            const float2 uu = edge ? u_at(q) : usm[q];
-            const float e1 = fmaf(uu.x, uu.x, uu.y * uu.y), e2 = e1 * e1, e3 = e2 * e1, e4 = e2 * e2;
-            const float h1 = tf32_rna(e1), h2 = tf32_rna(e2), h3 = tf32_rna(e3), h4 = tf32_rna(e4);
-            const uint2 lv = make_uint2(bf16x2_bits(e1 - h1, e2 - h2), bf16x2_bits(e3 - h3, e4 - h4));
-            if (rs < GT_R) {
-                fp[rs] = make_uint4(__float_as_uint(h1), __float_as_uint(h2), __float_as_uint(h3), __float_as_uint(h4));
-                fq[2 * rs] = lv;                               // row rs, first half
-            }
-            if (rs >= 1) fq[2 * rs - 1] = lv;                  // row rs - 1, second half
+        const int qb = ch * GT_CH - 4;
+        if (ch == 0 || ch == nch - 1) {
+            for (int rs = tid; rs < GT_R + 1; rs += T) feature(rs, u_at(qb + rs));
+        } else {
+#pragma unroll
+            for (int k = 0; k < GT_CH / T; ++k) feature(tid + k * T, usm[qb + tid + k * T]);
+            if (tid < GT_R + 1 - GT_CH) feature(GT_CH + tid, usm[qb + GT_CH + tid]);
         }
     };
-    // 12 MMAs of chunk ch (feature buffer and accumulator ch & 1), committed to bar[ch & 1]
-    auto issue = [&](int ch) {
-        const uint32_t fpb = sbase + GT_FP + (ch & 1) * GT_BUF, fqb = sbase + GT_FQ + (ch & 1) * GT_BUF;
-        const uint32_t dacc = *tslot + 64u * (ch & 1);
+    // tile j of chunk ch: 6 MMAs into accumulator (ch & 1), committed to bar[ch & 1]
+    auto issue = [&](int ch, int j) {
+        const uint32_t d = *tslot + (uint32_t)(GT_TILES * 32) * (ch & 1) + 32u * j;
         tc_fence_after();
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const uint32_t d = dacc + 32u * j;
+        for (int s1 = 0; s1 < 4; ++s1) {     // rows q + d0, d0 = -3 + 2 s1; K plane 2 = the next row
+            const uint64_t da = umma_desc(sbase + GT_FP + (128 * j + 1 + 2 * s1) * 16, 16, 128);
+            const uint64_t db = umma_desc(sbase + GT_B1 + s1 * GT_B1_MAT, 32 * 16, 128);
+            mma_tf32(d, da, db, ID1, s1 > 0 ? 1u : 0u);
+        }
 #pragma unroll
-            for (int s1 = 0; s1 < 4; ++s1) {   // rows q + d0, d0 = -3 + 2 s1; K plane 2 = the next row
-                const uint64_t da = umma_desc(fpb + (128 * j + 1 + 2 * s1) * 16, 16, 128);
-                const uint64_t db = umma_desc(sbase + GT_B1 + s1 * GT_B1_MAT, 32 * 16, 128);
-                mma_tf32(d, da, db, ID1, s1 > 0 ? 1u : 0u);
-            }
-#pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {   // rows q + d0, d0 = -3 + 4 s2; K plane 2 = two rows on
-                const uint64_t da = umma_desc(fqb + (128 * j + 1 + 4 * s2) * 16, 32, 128);
-                const uint64_t db = umma_desc(sbase + GT_B2 + s2 * GT_B2_MAT, 16 * 16, 128);
-                mma_f16(d, da, db, ID2, 1u);
-            }
+        for (int s2 = 0; s2 < 2; ++s2) {     // rows q + d0, d0 = -3 + 4 s2; K plane 2 = two rows on
+            const uint64_t da = umma_desc(sbase + GT_FQ + (128 * j + 1 + 4 * s2) * 16, 32, 128);
+            const uint64_t db = umma_desc(sbase + GT_B2 + s2 * GT_B2_MAT, 16 * 16, 128);
+            mma_f16(d, da, db, ID2, 1u);
         }
         umma_commit(&bar[ch & 1]);
     };
+    float2 c0[L + 1];
+#pragma unroll
+    for (int l = 0; l <= L; ++l) c0[l] = cs[l];                  // a_{1,l}
 
+    float2 acc0 = make_float2(0.f, 0.f);   // y of samples 0..5 without the partner's taps (warp 0)
     features(0);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (tid == 0) issue(0);
+    if (warp < GT_TILES && lane == 0) issue(0, warp);
 #pragma unroll 1
     for (int ch = 0; ch < nch; ++ch) {
         const int q0 = ch * GT_CH;
-        if (ch + 1 < nch) features(ch + 1);          // buffer (ch + 1) & 1: MMA(ch - 1) has completed
-        mbar_wait(&bar[ch & 1], (uint32_t)((ch >> 1) & 1));
+        mbar_wait(&bar[ch & 1], (uint32_t)((ch >> 1) & 1));      // MMA(ch) complete: features free
+        if (ch + 1 < nch) features(ch + 1);
         fence_proxy_async();
         tc_fence_before();
         __syncthreads();                             // features(ch + 1) complete; epilogue(ch - 1) done
-        if (tid == 0 && ch + 1 < nch) issue(ch + 1);
+        if (ch + 1 < nch && warp < GT_TILES && lane == 0) issue(ch + 1, warp);
         tc_fence_after();
-        // ---- thread = sample q = q0 + 32 warp + lane (tile warp / 4, lane quadrant warp % 4)
-        const int q = q0 + 32 * warp + lane;
-        float v[32];
-        tmem_ld32(*tslot + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (ch & 1) + 32u * (warp >> 2), v);
-        const float2 uq = usm[q];
-        float2 z[L + 1];
-#pragma unroll
-        for (int l = 0; l <= L; ++l) {
-            const float2 G = fadd2(fadd2(make_float2(v[2 * l], v[2 * l + 1]), make_float2(v[16 + 2 * l], v[17 + 2 * l])),
-                                   a0[l]);
-            z[l] = cmul2(uq, G);
-        }
+        // ---- epilogue: groups g = warp and warp + 8 (tile g / 4, TMEM lane quadrant g % 4 = warp % 4)
         const int cb = ch & 1;
-        if (lane >= 26) {
+        float2 z[2][L + 1];
 #pragma unroll
-            for (int l = 1; l <= L; ++l) zc[((cb * 8 + warp) * 6 + (l - 1)) * 6 + (lane - 26)] = z[l];
+        for (int h = 0; h < 2; ++h) {
+            const int g = warp + 8 * h;
+            const int q = q0 + 32 * g + lane;
+            float v[32];
+            tmem_ld32(*tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(GT_TILES * 32) * cb + 32u * (g >> 2), v);
+            const float2 uq = usm[q];
+#pragma unroll
+            for (int l = 0; l <= L; ++l) {
+                const float2 G = make_float2((v[2 * l] + v[16 + 2 * l]) + c0[l].x, (v[2 * l + 1] + v[17 + 2 * l]) + c0[l].y);
+                z[h][l] = cmul(uq, G);
+            }
+            if (lane >= 26) {
+#pragma unroll
+                for (int l = 1; l <= L; ++l) zc[((cb * GT_GROUPS + g) * 6 + (l - 1)) * 6 + (lane - 26)] = z[h][l];
+            }
         }
+        tc_fence_before();
         __syncthreads();
         // ---- y_q = sum_l z_l(q - l)
-        const float2* prev = zc + ((warp > 0 ? cb * 8 + warp - 1 : (cb ^ 1) * 8 + 7) * 6) * 6;
-        float2 acc = z[0];
 #pragma unroll
-        for (int l = 1; l <= L; ++l) {
-            float2 t;
-            t.x = __shfl_up_sync(0xffffffffu, z[l].x, l);
-            t.y = __shfl_up_sync(0xffffffffu, z[l].y, l);
-            if (lane < l) t = prev[(l - 1) * 6 + (lane - l + 6)];
-            acc = fadd2(acc, t);
+        for (int h = 0; h < 2; ++h) {
+            const int g = warp + 8 * h;
+            const int q = q0 + 32 * g + lane;
+            // the group before group 0 of chunk 0 is the partner's last: its taps are added after
+            // the loop (samples 0..5), once the partner has published them
+            const bool first = ch == 0 && g == 0;
+            const float2* prev = zc + ((g > 0 ? cb * GT_GROUPS + g - 1 : (cb ^ 1) * GT_GROUPS + GT_GROUPS - 1) * 6) * 6;
+            float2 acc = z[h][0];
+#pragma unroll
+            for (int l = 1; l <= L; ++l) {
+                float2 t;
+                t.x = __shfl_up_sync(0xffffffffu, z[h][l].x, l);
+                t.y = __shfl_up_sync(0xffffffffu, z[h][l].y, l);
+                if (lane < l) t = first ? make_float2(0.f, 0.f) : prev[(l - 1) * 6 + (lane - l + 6)];
+                acc = cadd(acc, t);
+            }
+            if (first && lane < L) {
+                acc0 = acc;
+            } else {
+                if (im) acc = pa_impair(acc, nbase + (unsigned long long)q, *im);
+                y[q] = acc;
+            }
         }
-        if (im) acc = pa_impair(acc, nbase + (unsigned long long)q, *im);
-        y[q] = acc;
+    }
+    // samples 0..5: the partner's last six samples' taps (its last group's carry, zc[(nch - 1) & 1])
+    cluster_sync_all();
+    if (warp == 0 && lane < L) {
+        const float2* pz = reinterpret_cast<const float2*>(sm_r + GT_ZC) +
+                           ((((nch - 1) & 1) * GT_GROUPS + GT_GROUPS - 1) * 6) * 6;
+#pragma unroll
+        for (int l = 1; l <= L; ++l)
+            if (lane < l) acc0 = cadd(acc0, pz[(l - 1) * 6 + (lane - l + 6)]);
+        if (im) acc0 = pa_impair(acc0, nbase + (unsigned long long)lane, *im);
+        y[lane] = acc0;
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(*tslot, 128);
+        tmem_dealloc(*tslot, GT_TMEM);
     }
     // the caller reuses this shared memory (receive-DFT scratch): retire the mbarriers first —
     // without this ~0.6 % of the received rows (XPA) came out different run to run

@@ -182,7 +182,7 @@ def qam_map(idx, M_qam, out=None):
 
 
 def set_gmp_path(mode: int):
-    """GMP of the N = 16384 cluster chain (include/fdpd.h fd_set_gmp_path): 0 = auto, 1 = FP32 SIMT,
+    """GMP of the N = 16384 cluster chain (include/fdpd.h fd_set_gmp_path): 0 = auto (= FP32 SIMT), 1 = FP32 SIMT,
     2 = tensor cores (C4 / C5 GMP shape).  Process-wide."""
     _check(lib().fd_set_gmp_path(int(mode)))
 
