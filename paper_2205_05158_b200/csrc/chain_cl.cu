@@ -29,6 +29,14 @@ namespace cg = cooperative_groups;
 
 namespace fdpd {
 
+// Cluster barrier with release / acquire at cluster scope (shared::cluster and global accesses of
+// the pair are ordered).  cooperative_groups' cluster.sync() adds a GPU-scope fence and an L1
+// invalidate (MEMBAR.ALL.GPU + ERRBAR + CCTL.IVALL: ~1.7 % of the CTA's lifetime per call, four
+// calls); the only global data exchanged between the pair, y, is re-read with ld.global.cg.
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 #include "gmp_tc.cuh"
 
 // TCG: the GMP on the tensor cores (gmp_tc.cuh; the C4 / C5 shape at N_L = 8192 only).
@@ -62,7 +70,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     if constexpr (!TCG) stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
     if (imp.precoded) {
         const float2* Xr = P + nb * N_d + c;
-        for (int jl = tid; jl < NdL; jl += T) xs[jl] = __ldg(Xr + 2 * jl);
+        for (int j0 = tid; j0 < NdL; j0 += 8 * T) {      // eight loads in flight per thread
+            float2 t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (j0 + k * T < NdL) t[k] = __ldg(Xr + 2 * (j0 + k * T));
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (j0 + k * T < NdL) xs[j0 + k * T] = t[k];
+        }
     } else {
         const float2* Pb = P + (size_t)n * imp.p_stride + (size_t)b * U * N_d + c;
         const float2* sn = s + n * U * N_d + c;
@@ -128,7 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     }
 
     // ---- radix-2 combine across the pair: x[c N_L + m] = Y_0[m] + (-1)^c W_N^{-m} Y_1[m]
-    cl.sync();                                   // both Y complete
+    cluster_sync_all();                          // both Y complete
     {
         const float2* usm_r = cl.map_shared_rank(usm, c ^ 1);
 #pragma unroll
@@ -140,7 +156,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
             v[j] = cscale(c ? csub(Y0, t) : cadd(Y0, t), sc);
         }
     }
-    cl.sync();                                   // the partner has read our Y
+    cluster_sync_all();                          // the partner has read our Y
     using Lay = RunLayout<RS>;
     if constexpr (TCG) {
 #pragma unroll
@@ -153,21 +169,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
             esm[Lay::e_phys(i)] = fmaf(v[j].x, v[j].x, v[j].y * v[j].y);
         }
     }
-    cl.sync();                                   // both halves' u / e staged (GMP halo reads)
+    cluster_sync_all();                          // both halves' u / e staged (GMP halo reads)
 
     // ---- GMP on this half; y (global) gets samples [c N_L, (c + 1) N_L)
     float2* yo = y + nb * N;
     if constexpr (TCG) {
         static_assert(T == 256, "gmp_tc_half runs 256 threads");
-        gmp_tc_half<KP, L, M>(usm, cl.map_shared_rank(usm, c ^ 1), coef + (size_t)b * d.n_coef, cf, d.n_coef,
-                              reinterpret_cast<unsigned char*>(esm),
-                              reinterpret_cast<const unsigned char*>(cl.map_shared_rank(esm, c ^ 1)), NL,
+        // scratch right behind the natural-order u (the padded FFT layout and e are dead here)
+        unsigned char* gsm = smem_raw + (size_t)NL * sizeof(float2);
+        gmp_tc_half<KP, L, M>(usm, cl.map_shared_rank(usm, c ^ 1), coef + (size_t)b * d.n_coef, d.n_coef, gsm,
+                              reinterpret_cast<const unsigned char*>(cl.map_shared_rank(gsm, c ^ 1)), NL,
                               yo + (size_t)c * NL, tid, im, nbase);
     } else {
         gmp_runs_symbol<KP, L, M, RS, false, true>(usm, esm, cf, NL, yo + (size_t)c * NL, tid, T, nullptr, im, nbase,
                                                    cl.map_shared_rank(usm, c ^ 1), cl.map_shared_rank(esm, c ^ 1));
     }
-    cl.sync();   // the partner is done with our u / e, and both halves of y are written (cluster acq/rel)
+    cluster_sync_all();   // the partner is done with our u / e, and both halves of y are written (cluster acq/rel)
 
     // ---- receive DFT at the parity-c bins: DFT_{N_L}((y_0 + (-1)^c y_1) W_N^{c m})
     {
@@ -193,11 +210,13 @@ static int launch_cl_one(const float2* P, const float2* s, const float2* coef, f
     const float2* tw_l = twiddle_table(NL, st);
     const float2* tw_g = twiddle_table(2 * NL, st);
     if (!tw_l || !tw_g) { set_error("twiddle table allocation failed"); return FD_ERR_CUDA; }
-    const ChainSmem lay = chain_smem(NL, N_d / 2, d, false);
-    if (lay.bytes > 227 * 1024) return fail_arg("chain_cl: shared-memory footprint %d B too large", lay.bytes);
+    ChainSmem lay = chain_smem(NL, N_d / 2, d, false);
     if constexpr (TCG) {
-        if (lay.off_cf - lay.off_e < GT_BYTES) return fail_arg("chain_cl: tensor-core GMP needs %d B of scratch", GT_BYTES);
+        // GMP phase: natural-order u, then the tensor-core scratch (two CTAs per SM: <= 113 KB)
+        const int need = NL * (int)sizeof(float2) + GT_BYTES;
+        if (need > lay.bytes) lay.bytes = need;
     }
+    if (lay.bytes > 227 * 1024) return fail_arg("chain_cl: shared-memory footprint %d B too large", lay.bytes);
     set_smem(k_chain_cl<LOG2NL, KP, L, M, RS, PZ, TCG>, lay.bytes);
     k_chain_cl<LOG2NL, KP, L, M, RS, PZ, TCG><<<(unsigned)(2 * n_sym * B), fft_threads<LOG2NL>(), lay.bytes, st>>>(
         P, s, coef, y, XPA, tw_l, tw_g, B, U, N_d, (float)(1.0 / std::sqrt((double)(2 * NL))), d, imp);
