@@ -290,79 +290,116 @@ __global__ void __launch_bounds__(128) k_rx_combine_blk(const float2* __restrict
 // Many users (U = 9..32): per subcarrier the channel sum is a small complex GEMM
 // yhat_j[n][u] = sum_b X_j[n][b] h_j[u][b] with a long contraction (b < B = 256..512) — the
 // register-blocked kernel above re-reads h_fd from L2 for every symbol pair (6.9 GB per 32
-// symbols at C5).  Here a CTA owns 32 subcarriers (lane = j) x NT = 8 symbols x all users
-// (warp w: users w UPT .. w UPT + UPT - 1): X_j for its 8 symbols is staged in shared memory
+// symbols at C5).  Here a CTA owns 32 subcarriers (lane = j) x NT symbols x all users
+// (warp w: users w UPT .. w UPT + UPT - 1): X_j for its NT symbols is staged in shared memory
 // in chunks of BC antennas and read by all 8 warps, and each thread's h_fd loads (coalesced
-// over j) feed 8 symbols from registers.  Same summation order over b as k_rx_combine.
-template <bool SER, bool AWGN, int UPT>
-__global__ void __launch_bounds__(256) k_rx_combine_tile(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
-                                                         float2* __restrict__ yhat, int B, int U, int N_d,
-                                                         long long n_sym, int accumulate,
-                                                         const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
-                                                         long long* counts, SliceParams sp, Impair imp) {
-    constexpr int NT = 8, BC = 16;
-    __shared__ __align__(16) float2 xs[NT][BC][32];
+// over j) feed NT symbols from registers.  Same summation order over b as k_rx_combine.
+//
+// Pipeline: both operands are staged in shared memory by 16-byte cp.async copies, CB_A antennas
+// per stage (h_fd rows [u][a] and X rows [n][a] of 32 subcarriers = 256 B each), CB_NS stages
+// deep, so ~80 KB per CTA are in flight while a stage is consumed and neither HBM nor L2 latency
+// reaches the FMAs; one CTA barrier per stage.  (The first version staged X through registers
+// between two barriers and loaded h_fd into registers right before use: 0.646 ms per 32 C5
+// symbols with the FMA pipe 43 % busy, long-scoreboard stalls on the h_fd loads.)
+//
+// Wave balance: the full tiles (NT = 8 symbols) fill whole rounds of the resident CTA slots; the
+// tiles of the last, partial round are cut into two NT = 4 halves so that round costs about half
+// a tile time (C5: 416 tiles on 296 slots = 2 rounds -> 1.5).
+constexpr int CB_A = 2;                         // antennas per stage
+constexpr int CB_NS = 5;                        // stages
+template <int UPT, int NT>
+constexpr int combine_stage_elems() { return (8 * UPT + NT) * CB_A * 32; }   // float2 per stage: h_fd then X
+template <int UPT>
+constexpr int combine_tile_smem() { return CB_NS * combine_stage_elems<UPT, 8>() * (int)sizeof(float2); }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+    // 16-byte asynchronous copy global -> shared; !ok: zero fill (src-size 0, src not read)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+
+template <bool SER, bool AWGN, int UPT, int NT>
+__device__ __forceinline__ void combine_tile_body(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
+                                                  float2* __restrict__ yhat, int B, int U, int N_d, int jt,
+                                                  long long n0, int nt, int accumulate,
+                                                  const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
+                                                  long long* counts, const SliceParams& sp, const Impair& imp,
+                                                  float2* sm) {
+    constexpr int UT = 8 * UPT;                 // users of the tile (8 warps)
+    constexpr int STAGE = combine_stage_elems<UPT, NT>();
+    constexpr int HROWS = UT * CB_A, XROWS = NT * CB_A;     // 256-byte rows per stage
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = blockIdx.y * 32 + lane;
+    const int j0 = jt * 32, j = j0 + lane;
     const bool jok = j < N_d;
-    const long long n0 = (long long)(gridDim.x - 1 - blockIdx.x) * NT;   // last-written symbols first (L2)
-    const int nt = (int)min((long long)NT, n_sym - n0);
     const int u0 = warp * UPT;
     float2 acc[NT][UPT];
 #pragma unroll
     for (int n = 0; n < NT; ++n)
 #pragma unroll
         for (int c = 0; c < UPT; ++c) acc[n][c] = make_float2(0.f, 0.f);
-    const float2* H = hfd + (jok ? j : 0);
-    for (int b0 = 0; b0 < B; b0 += BC) {
-        const int bn = min(BC, B - b0);
-        __syncthreads();
-        {
-            // all of this thread's staging loads in flight before the shared-memory stores
-            constexpr int PER = NT * BC * 32 / 256;
-            float2 t[PER];
+    const int nstages = (B + CB_A - 1) / CB_A;
+    // This thread's 16-byte pieces of a stage: piece e = tid + 256 k -> row e / 16, subcarriers
+    // pj = j0 + 2 (e % 16), + 1.  With 16 rows per k step the rows of a thread are CB_A-periodic:
+    // its antenna a = (tid / 16) % CB_A is fixed and its h_fd user (X symbol) advances by
+    // 16 / CB_A per k, so every source is one base pointer plus a constant stride, advanced by
+    // CB_A antennas per stage (no index arithmetic in the loop).
+    static_assert(16 % CB_A == 0, "antennas per stage must divide 16");
+    constexpr int RPK = 16 / CB_A;              // users / symbols per k step
+    constexpr int HK = HROWS / 16, XK = (XROWS + 15) / 16;
+    const int pj = j0 + 2 * (threadIdx.x & 15);
+    const bool pok = pj < N_d;                  // N_d is even: both subcarriers of a piece or none
+    const int r0 = threadIdx.x >> 4, pa = r0 % CB_A, pu = r0 / CB_A;
+    const float2* hsrc = hfd + ((size_t)pu * B + pa) * N_d + (pok ? pj : 0);
+    const float2* xsrc = XPA + ((size_t)(n0 + (pu < nt ? pu : 0)) * B + pa) * N_d + (pok ? pj : 0);
+    const size_t hstep = (size_t)RPK * B * N_d;               // elements between a thread's h_fd / X pieces
+    const uint32_t sm0 = smem_u32(sm) + 16u * threadIdx.x;    // piece e of stage 0 (h_fd), X pieces behind
+    int ibuf = 0, ist = 0;                                    // next stage to issue and its buffer
+    auto issue = [&]() {
+        if (ist < nstages) {
+            const bool aok = pok && ist * CB_A + pa < B;
+            const uint32_t d = sm0 + (uint32_t)ibuf * (STAGE * 8);
 #pragma unroll
-            for (int k = 0; k < PER; ++k) {
-                const int e = threadIdx.x + 256 * k;
-                const int l = e & 31, r = e >> 5, bb = r % BC, n = r / BC;
-                const int jj = blockIdx.y * 32 + l;
-                t[k] = (n < nt && bb < bn && jj < N_d) ? __ldg(XPA + ((size_t)(n0 + n) * B + b0 + bb) * N_d + jj)
-                                                      : make_float2(0.f, 0.f);
+            for (int k = 0; k < HK; ++k) {
+                const bool ok = aok && pu + RPK * k < U;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d + 4096u * k),
+                             "l"(ok ? hsrc + hstep * k : hfd), "r"(ok ? 16 : 0)
+                             : "memory");
             }
 #pragma unroll
-            for (int k = 0; k < PER; ++k) (&xs[0][0][0])[threadIdx.x + 256 * k] = t[k];
+            for (int k = 0; k < XK; ++k) {
+                if (XROWS % 16 != 0 && r0 + 16 * k >= XROWS) break;
+                const bool ok = aok && pu + RPK * k < nt;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d + HROWS * 256u + 4096u * k),
+                             "l"(ok ? xsrc + hstep * k : XPA), "r"(ok ? 16 : 0)
+                             : "memory");
+            }
+            hsrc += (size_t)CB_A * N_d;
+            xsrc += (size_t)CB_A * N_d;
         }
-        __syncthreads();
-        // h_fd for 4 antennas (4 UPT loads) in flight per step
-        int bb = 0;
-        for (; bb + 4 <= bn; bb += 4) {
-            float2 hv[4][UPT];
+        asm volatile("cp.async.commit_group;" ::: "memory");     // (empty groups keep the count uniform)
+        ++ist;
+        if (++ibuf == CB_NS) ibuf = 0;
+    };
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+    for (int st = 0; st < CB_NS - 1; ++st) issue();
+    int cbuf = 0;
+    for (int st = 0; st < nstages; ++st) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(CB_NS - 2) : "memory");
+        __syncthreads();                       // stage st visible; everyone is done with stage st - 1
+        issue();                               // stage st + CB_NS - 1 refills the buffer of stage st - 1
+        const float2* hs = sm + (size_t)cbuf * STAGE;
+        const float2* xs = hs + HROWS * 32;
+        if (++cbuf == CB_NS) cbuf = 0;
 #pragma unroll
-                for (int c = 0; c < UPT; ++c)
-                    hv[q][c] = (u0 + c < U) ? __ldg(H + ((size_t)(u0 + c) * B + b0 + bb + q) * N_d)
-                                            : make_float2(0.f, 0.f);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int n = 0; n < NT; ++n) {
-                    const float2 xv = xs[n][bb + q][lane];
-#pragma unroll
-                    for (int c = 0; c < UPT; ++c) acc[n][c] = cfma(hv[q][c], xv, acc[n][c]);
-                }
-        }
-        for (; bb < bn; ++bb) {
-            const int b = b0 + bb;
+        for (int a = 0; a < CB_A; ++a) {
             float2 hv[UPT];
 #pragma unroll
-            for (int c = 0; c < UPT; ++c)
-                hv[c] = (u0 + c < U) ? __ldg(H + ((size_t)(u0 + c) * B + b) * N_d) : make_float2(0.f, 0.f);
+            for (int c = 0; c < UPT; ++c) hv[c] = hs[((u0 + c) * CB_A + a) * 32 + lane];
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-                const float2 xv = xs[n][bb][lane];
+                const float2 xv = xs[(n * CB_A + a) * 32 + lane];
 #pragma unroll
-                for (int c = 0; c < UPT; ++c) acc[n][c] = cfma(hv[c], xv, acc[n][c]);
+                for (int c = 0; c < UPT; ++c) acc[n][c] = cfma2(hv[c], xv, acc[n][c]);
             }
         }
     }
@@ -398,6 +435,55 @@ __global__ void __launch_bounds__(256) k_rx_combine_tile(const float2* __restric
     if (SER) add_counts(counts, err, near, cnt);
 }
 
+// Tiles t = jt * ntile_n + i (symbol tiles fastest: the CTAs sharing a subcarrier tile's h_fd
+// slice, U x B x 32, run together, so h_fd comes from HBM once per step and from L2 after; the
+// last-written symbols first: their XPA rows are still in L2).  CTAs [0, n_full) take whole
+// tiles, the rest half tiles (see above).
+template <bool SER, bool AWGN, int UPT>
+__global__ void __launch_bounds__(256, 2) k_rx_combine_tile(const float2* __restrict__ XPA, const float2* __restrict__ hfd,
+                                                            float2* __restrict__ yhat, int B, int U, int N_d,
+                                                            long long n_sym, int ntile_n, int n_full, int accumulate,
+                                                            const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
+                                                            long long* counts, SliceParams sp, Impair imp) {
+    extern __shared__ __align__(16) unsigned char cb_smem[];
+    float2* xs = reinterpret_cast<float2*>(cb_smem);   // CB_NS stages of (h_fd rows, X rows)
+    const int bid = blockIdx.x;
+    const bool full = bid < n_full;
+    const int t = full ? bid : n_full + ((bid - n_full) >> 1);
+    const int half = full ? 0 : ((bid - n_full) & 1);
+    const int jt = t / ntile_n;
+    const long long n0 = (long long)(ntile_n - 1 - (t - jt * ntile_n)) * 8 + 4 * half;
+    if (full) {
+        const int nt = (int)min(8LL, n_sym - n0);
+        combine_tile_body<SER, AWGN, UPT, 8>(XPA, hfd, yhat, B, U, N_d, jt, n0, nt, accumulate, idx, dec, counts, sp,
+                                             imp, xs);
+    } else {
+        const int nt = (int)min(4LL, n_sym - n0);
+        if (nt <= 0) return;
+        combine_tile_body<SER, AWGN, UPT, 4>(XPA, hfd, yhat, B, U, N_d, jt, n0, nt, accumulate, idx, dec, counts, sp,
+                                             imp, xs);
+    }
+}
+
+// Resident CTA slots of kern on the current device, cached per kernel (the instantiations share
+// one function-pointer type, so the cache is keyed by the pointer); also raises the kernel's
+// dynamic shared-memory limit on first use.
+template <typename K>
+static int combine_slots(K kern, int smem) {
+    static const void* keys[16];
+    static int vals[16], n = 0;
+    for (int i = 0; i < n; ++i)
+        if (keys[i] == reinterpret_cast<const void*>(kern)) return vals[i];
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem);
+    const int v = std::max(1, sms * per);
+    if (n < 16) { keys[n] = reinterpret_cast<const void*>(kern); vals[n] = v; ++n; }
+    return v;
+}
+
 template <bool SER, bool AWGN>
 static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d, long long n_sym,
                            int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
@@ -409,17 +495,23 @@ static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, i
             dim3 g((N_d + 127) / 128, (unsigned)((n_sym + ns - 1) / ns));
             kern<<<g, 128, 0, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, imp);
         };
-        auto go_tile = [&](auto kern) {
-            // n-tiles fastest: the CTAs sharing a subcarrier tile's h_fd slice (U x B x 32) run
-            // together, so h_fd comes from HBM once per step (432 MB at C5) and from L2 after
-            dim3 g((unsigned)((n_sym + 7) / 8), (N_d + 31) / 32);
-            kern<<<g, 256, 0, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, imp);
+        auto go_tile = [&](auto kern, int smem) {
+            const int slots = combine_slots(kern, smem);
+            const int ntile_n = (int)((n_sym + 7) / 8), tiles = ntile_n * ((N_d + 31) / 32);
+            // whole rounds as full tiles; a last round filling under ~3/4 of the slots as half tiles
+            int n_full = tiles / slots * slots;
+            if ((tiles - n_full) * 4 > slots * 3) n_full = tiles;
+            const unsigned grid = (unsigned)(n_full + 2 * (tiles - n_full));
+            kern<<<grid, 256, smem, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, ntile_n, n_full, accumulate, idx, dec,
+                                          counts, sp, imp);
         };
         if (U <= 2) go(k_rx_combine_blk<SER, AWGN, 2, 4>, 4);
         else if (U <= 4) go(k_rx_combine_blk<SER, AWGN, 4, 4>, 4);
         else if (U <= 8) go(k_rx_combine_blk<SER, AWGN, 8, 2>, 2);
-        else if (U <= 16) go_tile(k_rx_combine_tile<SER, AWGN, 2>);
-        else if (U <= 32) go_tile(k_rx_combine_tile<SER, AWGN, 4>);
+        // (the tile kernel copies 16-byte pieces: XPA / h_fd rows start 16-byte aligned when the
+        // bases are, N_d being even)
+        else if (U <= 16 && aligned16(XPA) && aligned16(hfd)) go_tile(k_rx_combine_tile<SER, AWGN, 2>, combine_tile_smem<2>());
+        else if (U <= 32 && aligned16(XPA) && aligned16(hfd)) go_tile(k_rx_combine_tile<SER, AWGN, 4>, combine_tile_smem<4>());
         else go(k_rx_combine_blk<SER, AWGN, 8, 2>, 2);
         return;
     }
