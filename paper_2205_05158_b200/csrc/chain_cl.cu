@@ -39,6 +39,22 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 #include "gmp_tc.cuh"
 
+// Phase trace (builds with -DFD_TRACE only; tools/chain_trace.py): per CTA the SM id and
+// %globaltimer at the phase boundaries.
+#ifdef FD_TRACE
+__device__ unsigned long long g_trace[65536 * 8];
+__device__ __forceinline__ void trace_mark(int slot) {
+    if (threadIdx.x == 0 && blockIdx.x < 65536) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[(size_t)blockIdx.x * 8 + slot] = t;
+    }
+}
+#define FD_TRACE_MARK(i) trace_mark(i)
+#else
+#define FD_TRACE_MARK(i)
+#endif
+
 // TCG: the GMP on the tensor cores (gmp_tc.cuh; the C4 / C5 shape at N_L = 8192 only).
 template <int LOG2NL, int KP, int L, int M, int RS, int PZ, bool TCG = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(), fft_min_blocks<LOG2NL>())
@@ -65,6 +81,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
         ((unsigned long long)(imp.sym0 + (long long)n) * imp.B_total + imp.b0 + b) * (unsigned long long)N +
         (unsigned long long)c * NL;
 
+#ifdef FD_TRACE
+    if (tid == 0 && blockIdx.x < 65536) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace[(size_t)blockIdx.x * 8 + 7] = smid;
+    }
+#endif
+    FD_TRACE_MARK(0);
     // ---- precode (Eq. 1) of this CTA's data bins: local jl <-> global j = 2 jl + c
     float2* xs = reinterpret_cast<float2*>(esm);
     if constexpr (!TCG) stage_coefs<KP, L, M>(coef + (size_t)b * d.n_coef, cf, d, tid, T);
@@ -105,6 +129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     }
     __syncthreads();
 
+    FD_TRACE_MARK(1);
     // ---- local IDFT of the parity-c bins -> Y_c in usm (unnormalised)
     float2 v[VPT];
     const int h = NdL >> 1;
@@ -143,6 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
         fft_run<LOG2NL, +1>(usm, v, tw_l, tid);
     }
 
+    FD_TRACE_MARK(2);
     // ---- radix-2 combine across the pair: x[c N_L + m] = Y_0[m] + (-1)^c W_N^{-m} Y_1[m]
     cluster_sync_all();                          // both Y complete
     {
@@ -171,6 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     }
     cluster_sync_all();                          // both halves' u / e staged (GMP halo reads)
 
+    FD_TRACE_MARK(3);
     // ---- GMP on this half; y (global) gets samples [c N_L, (c + 1) N_L)
     float2* yo = y + nb * N;
     if constexpr (TCG) {
@@ -184,7 +211,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
         gmp_runs_symbol<KP, L, M, RS, false, true>(usm, esm, cf, NL, yo + (size_t)c * NL, tid, T, nullptr, im, nbase,
                                                    cl.map_shared_rank(usm, c ^ 1), cl.map_shared_rank(esm, c ^ 1));
     }
+    FD_TRACE_MARK(4);
     cluster_sync_all();   // the partner is done with our u / e, and both halves of y are written (cluster acq/rel)
+    FD_TRACE_MARK(5);
 
     // ---- receive DFT at the parity-c bins: DFT_{N_L}((y_0 + (-1)^c y_1) W_N^{c m})
     {
@@ -201,6 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fft_threads<LOG2NL>(
     fft_run<LOG2NL, -1>(usm, v, tw_l, tid, reinterpret_cast<float2*>(esm));       // e (esm) is dead after the GMP
     float2* xo = XPA + nb * N_d + c;
     for (int jl = tid; jl < NdL; jl += T) xo[2 * jl] = cscale(usm[pidx(data_to_bin(jl, NL, NdL))], sc);
+    FD_TRACE_MARK(6);
 }
 
 template <int LOG2NL, int KP, int L, int M, int RS, int PZ, bool TCG = false>
@@ -217,6 +247,9 @@ static int launch_cl_one(const float2* P, const float2* s, const float2* coef, f
         if (need > lay.bytes) lay.bytes = need;
     }
     if (lay.bytes > 227 * 1024) return fail_arg("chain_cl: shared-memory footprint %d B too large", lay.bytes);
+#ifdef FD_TRACE
+    if (getenv("FD_OCC1")) lay.bytes = 120 * 1024;   // experiment: one CTA per SM
+#endif
     set_smem(k_chain_cl<LOG2NL, KP, L, M, RS, PZ, TCG>, lay.bytes);
     k_chain_cl<LOG2NL, KP, L, M, RS, PZ, TCG><<<(unsigned)(2 * n_sym * B), fft_threads<LOG2NL>(), lay.bytes, st>>>(
         P, s, coef, y, XPA, tw_l, tw_g, B, U, N_d, (float)(1.0 / std::sqrt((double)(2 * NL))), d, imp);
@@ -267,6 +300,12 @@ int launch_chain_cluster(int log2n, int variant, const float2* P, const float2* 
 }
 
 }  // namespace fdpd
+
+#ifdef FD_TRACE
+extern "C" int fd_debug_trace_read(void* host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, fdpd::g_trace, bytes) == cudaSuccess ? FD_OK : FD_ERR_CUDA;
+}
+#endif
 
 extern "C" int fd_set_gmp_path(int mode) {
     FD_REQUIRE(mode >= 0 && mode <= 2, "fd_set_gmp_path: mode=%d (0 = auto, 1 = FP32 SIMT, 2 = tensor cores)", mode);
