@@ -560,7 +560,19 @@ def run_antenna(args, cfg):
     t_zf = time.perf_counter() - t0
     chain_ev = []
     ops = AntennaOps(ch, events=chain_ev)
-    step = D.AntennaShardedStep(ops, n, cfg.U, cfg.N_d, micro=micro,
+    # Exchange of the partial received signals: fused into the channel-sum kernel over peer memory
+    # (ue_combine_peer; auto: where it applies and the peer mappings validate), else NCCL
+    # reduce_scatter_tensor.
+    peer, exchange = None, "NCCL reduce_scatter_tensor"
+    if args.exchange != "nccl" and ops.peer_ok():
+        try:
+            peer = D.PeerExchange(micro, n // micro, cfg.U, cfg.N_d, dev)
+            exchange = "fused into ue_combine_peer (peer memory, CUDA IPC mappings)"
+        except Exception as e:                      # every rank fails or none: the validation is collective
+            if args.exchange == "peer":
+                raise
+            print(f"[bench] peer exchange unavailable ({e}); using NCCL", file=sys.stderr)
+    step = D.AntennaShardedStep(ops, n, cfg.U, cfg.N_d, micro=micro, peer=peer,
                                 alloc=lambda shp: torch.empty(shp, dtype=torch.complex64, device=dev))
     s = torch.from_numpy(inp["s"]).to(dev)
     idx = torch.from_numpy(inp["idx"]).to(dev)
@@ -639,8 +651,8 @@ def run_antenna(args, cfg):
         "config": dict(config_dict(cfg, ws, n), parallelism=f"antenna x{ws} (Mode A: {B_loc} antennas per GPU)",
                        precode=("tensor cores, " + math) if math != "simt" else "FP32 SIMT kernel",
                        micro_batches=micro, world_batch_symbols=ws * n,
-                       collectives="all_gather_into_tensor(s_tilde) + reduce_scatter_tensor(y_hat partials) per "
-                                   "micro-batch (NCCL, async, overlapped) + int64 counter all_reduce",
+                       collectives="all_gather_into_tensor(s_tilde) per micro-batch (NCCL, async, overlapped) + "
+                                   "int64 counter all_reduce; y_hat partials: " + exchange,
                        comm_bytes_per_rank_per_step={"all_gather_in": comm * (ws - 1) // ws,
                                                      "reduce_scatter_out": comm * (ws - 1) // ws}),
         "roofline": {"kernel": "chain_txrx_pre (IDFT+GMP+receive DFT)", "bound": "alu", "achieved": achieved,
@@ -682,6 +694,8 @@ def main():
                     help="split-path precode: FP32 SIMT, TF32 tensor cores, or FP32-accurate split-TF32 tensor cores")
     ap.add_argument("--combine", default="auto", choices=["auto", "simt", "tc"],
                     help="channel sum: auto (= the FP32 SIMT kernels), simt, or tc (tensor cores for 9 <= U <= 32)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                    help="Mode A: partial received signals through peer memory from the channel-sum kernel, or NCCL")
     ap.add_argument("--gmp", default="auto", choices=["auto", "simt", "tc"],
                     help="GMP of the N = 16384 cluster chain: auto, FP32 SIMT, or tensor cores (C4 / C5 shape)")
     ap.add_argument("--mode", default="auto", choices=["auto", "symbol", "antenna"],

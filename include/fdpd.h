@@ -299,6 +299,26 @@ int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, i
  * real GEMM with K = 2 B_loc, FP32-accurate hi/lo split on both operands, four products),
  * else SIMT.  FD_ERR_ARG for other modes. */
 int fd_set_combine_path(int mode);
+/* Mode A (antenna sharding, BASELINE configs[4]): the channel sum fused with its
+ * exchange.  Rank `rank` of `world` holds antenna rows of XPA [n_sym][B_loc][N_d] and h_fd
+ * [U][B_loc][N_d] for the WORLD batch of n_sym = world * nm symbols (symbol n belongs to rank
+ * n / nm).  Instead of a local partial y_hat that a reduce-scatter then moves, every partial
+ * sum sum_{b local} h_fd[u][b][j] XPA[n][b][j] (Eq. 5 over this rank's antennas) is
+ * stored by the kernel straight into slot `rank` of the owner's receive buffer:
+ *   peer_recv[n / nm][rank][n % nm][u][j]      (each buffer [world][nm][U][N_d] complex64)
+ * peer_recv: HOST array of `world` DEVICE pointers, peer-mapped (NVLink P2P / CUDA IPC) or, for
+ * r = rank, local; the stores overlap the kernel's math tile by tile.  9 <= U <= 32, N_d even,
+ * XPA / h_fd 16-byte aligned (FD_ERR_ARG otherwise: use ue_combine + a reduce-scatter).
+ * The caller orders "all ranks' ue_combine_peer done" before ue_reduce_ser (a stream-ordered
+ * barrier: no kernel of this library waits on another GPU). */
+int ue_combine_peer(const void* XPA, const void* h_fd, void* const* peer_recv, int world, int rank, long long n_sym,
+                    int B_loc, int U, int N_d, cudaStream_t stream);
+/* Owner side: yhat[n][u][j] = sum_{r < world} recv[r][n][u][j] in rank order (bit-reproducible),
+ * then, when tx_idx is not NULL, slicing + SER counters like ue_slice_ser (dec nullable).
+ * recv [world][n_sym][U][N_d], yhat [n_sym][U][N_d] (n_sym = this rank's symbols). */
+int ue_reduce_ser(const void* recv, int world, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                  uint16_t* dec, long long* counts, long long n_sym, int U, int N_d, float boundary_eps,
+                  cudaStream_t stream);
 /* ue_combine (accumulate = 0) fused with ue_slice_ser. */
 int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
                    uint16_t* dec, long long* counts, long long n_sym, int B_loc, int U, int N_d,

@@ -240,3 +240,14 @@ class AntennaOps:
     def slice(self, yhat, idx, counts):
         return fdpd.ue_slice_ser(yhat, self.ch.alpha, idx, self.ch.sh.M_qam, counts=counts,
                                  boundary_eps=self.ch.sh.eps)
+
+    # fused exchange (dist.PeerExchange): partial sums stored into the owners' receive buffers
+    def peer_ok(self):
+        return 9 <= self.ch.sh.U <= 32 and self.ch.sh.N_d % 2 == 0
+
+    def combine_peer(self, XPA, peer_recv, rank):
+        return fdpd.ue_combine_peer(XPA, self.ch.h_fd, peer_recv, rank)
+
+    def reduce_slice(self, recv, yhat, idx, counts):
+        return fdpd.ue_reduce_ser(recv, self.ch.alpha, idx, self.ch.sh.M_qam, yhat=yhat, counts=counts,
+                                  boundary_eps=self.ch.sh.eps)

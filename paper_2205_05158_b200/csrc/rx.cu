@@ -105,6 +105,31 @@ __global__ void k_slice(const float2* __restrict__ yhat, const uint16_t* __restr
     add_counts(counts, err, near, cnt);
 }
 
+// Mode A, owner side of the fused exchange: y_hat = sum over the source ranks' slots, in rank
+// order (deterministic), then slicing + SER like k_slice.  recv [ws][total].
+__global__ void k_reduce_slots_ser(const float2* __restrict__ recv, int ws, float2* __restrict__ yhat,
+                                   const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec, long long* counts,
+                                   long long total, SliceParams sp) {
+    int err = 0, near = 0, cnt = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        float2 z = __ldcg(recv + i);              // written by other GPUs: not through L1
+        for (int r = 1; r < ws; ++r) z = cadd(z, __ldcg(recv + (size_t)r * total + i));
+        yhat[i] = z;
+        if (idx) {
+            bool nr = false;
+            const int di = slice_axis(z.x * sp.inv_ac, sp, nr);
+            const int dq = slice_axis(z.y * sp.inv_ac, sp, nr);
+            const int dd = di + sp.m * dq;
+            if (dec) dec[i] = (uint16_t)dd;
+            err += (dd != (int)idx[i]);
+            near += nr;
+            ++cnt;
+        }
+    }
+    if (idx) add_counts(counts, err, near, cnt);
+}
+
 #include "combine_tc.cuh"
 
 // Tensor-core channel sum for 9 <= U <= 32 (combine_tc.cuh); process-wide switch
@@ -305,6 +330,16 @@ __global__ void __launch_bounds__(128) k_rx_combine_blk(const float2* __restrict
 // Wave balance: the full tiles (NT = 8 symbols) fill whole rounds of the resident CTA slots; the
 // tiles of the last, partial round are cut into two NT = 4 halves so that round costs about half
 // a tile time (C5: 416 tiles on 296 slots = 2 rounds -> 1.5).
+// Mode A exchange fused into the channel sum (ue_combine_peer): instead of a local partial
+// y_hat that a reduce-scatter then moves, symbol n of the world batch is stored straight into
+// the receive buffer of the rank that owns it (peer memory over NVLink, or this rank's own
+// buffer): slot `rank` of owner n / nm, local symbol n % nm.
+constexpr int CB_MAX_PEERS = 16;
+struct PeerOut {
+    float2* base[CB_MAX_PEERS];   // receive buffers [ws][nm][U][N_d] of every rank (peer-mapped)
+    int ws, rank, nm;             // ws = 0: plain local output
+};
+
 constexpr int CB_A = 2;                         // antennas per stage
 constexpr int CB_NS = 5;                        // stages
 template <int UPT, int NT>
@@ -324,7 +359,7 @@ __device__ __forceinline__ void combine_tile_body(const float2* __restrict__ XPA
                                                   long long n0, int nt, int accumulate,
                                                   const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
                                                   long long* counts, const SliceParams& sp, const Impair& imp,
-                                                  float2* sm) {
+                                                  float2* sm, const PeerOut& peer) {
     constexpr int UT = 8 * UPT;                 // users of the tile (8 warps)
     constexpr int STAGE = combine_stage_elems<UPT, NT>();
     constexpr int HROWS = UT * CB_A, XROWS = NT * CB_A;     // 256-byte rows per stage
@@ -414,6 +449,15 @@ __device__ __forceinline__ void combine_tile_body(const float2* __restrict__ XPA
                 if (u >= U) continue;
                 const size_t o = ((size_t)(n0 + n) * U + u) * N_d + j;
                 float2 a = acc[n][c];
+                if constexpr (!SER && !AWGN) {
+                    if (peer.ws > 0) {          // the owner's slot for this rank (Mode A, fused exchange)
+                        const long long ng = n0 + n;
+                        const int owner = (int)(ng / peer.nm);
+                        const long long nl = ng - (long long)owner * peer.nm;
+                        peer.base[owner][(((size_t)peer.rank * peer.nm + nl) * U + u) * N_d + j] = a;
+                        continue;
+                    }
+                }
                 if (accumulate) a = cadd(a, yhat[o]);
                 if constexpr (AWGN)
                     a = cadd(a, cgauss((unsigned long long)((imp.sym0 + n0 + n) * U + u) * N_d + j, STREAM_AWGN,
@@ -444,7 +488,8 @@ __global__ void __launch_bounds__(256, 2) k_rx_combine_tile(const float2* __rest
                                                             float2* __restrict__ yhat, int B, int U, int N_d,
                                                             long long n_sym, int ntile_n, int n_full, int accumulate,
                                                             const uint16_t* __restrict__ idx, uint16_t* __restrict__ dec,
-                                                            long long* counts, SliceParams sp, Impair imp) {
+                                                            long long* counts, SliceParams sp, Impair imp,
+                                                            PeerOut peer) {
     extern __shared__ __align__(16) unsigned char cb_smem[];
     float2* xs = reinterpret_cast<float2*>(cb_smem);   // CB_NS stages of (h_fd rows, X rows)
     const int bid = blockIdx.x;
@@ -456,12 +501,12 @@ __global__ void __launch_bounds__(256, 2) k_rx_combine_tile(const float2* __rest
     if (full) {
         const int nt = (int)min(8LL, n_sym - n0);
         combine_tile_body<SER, AWGN, UPT, 8>(XPA, hfd, yhat, B, U, N_d, jt, n0, nt, accumulate, idx, dec, counts, sp,
-                                             imp, xs);
+                                             imp, xs, peer);
     } else {
         const int nt = (int)min(4LL, n_sym - n0);
         if (nt <= 0) return;
         combine_tile_body<SER, AWGN, UPT, 4>(XPA, hfd, yhat, B, U, N_d, jt, n0, nt, accumulate, idx, dec, counts, sp,
-                                             imp, xs);
+                                             imp, xs, peer);
     }
 }
 
@@ -487,9 +532,10 @@ static int combine_slots(K kern, int smem) {
 template <bool SER, bool AWGN>
 static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, int B, int U, int N_d, long long n_sym,
                            int accumulate, const uint16_t* idx, uint16_t* dec, long long* counts,
-                           const SliceParams& sp, const Impair& imp, cudaStream_t st) {
+                           const SliceParams& sp, const Impair& imp, cudaStream_t st,
+                           const PeerOut& peer = PeerOut{}) {
     if (imp.h_stride == 0 && imp.alpha_dev == nullptr) {
-        if (!AWGN && launch_combine_tc(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, SER, st))
+        if (!AWGN && peer.ws == 0 && launch_combine_tc(XPA, hfd, yhat, B, U, N_d, n_sym, accumulate, idx, dec, counts, sp, SER, st))
             return;
         auto go = [&](auto kern, int ns) {
             dim3 g((N_d + 127) / 128, (unsigned)((n_sym + ns - 1) / ns));
@@ -503,7 +549,7 @@ static void launch_combine(const float2* XPA, const float2* hfd, float2* yhat, i
             if ((tiles - n_full) * 4 > slots * 3) n_full = tiles;
             const unsigned grid = (unsigned)(n_full + 2 * (tiles - n_full));
             kern<<<grid, 256, smem, st>>>(XPA, hfd, yhat, B, U, N_d, n_sym, ntile_n, n_full, accumulate, idx, dec,
-                                          counts, sp, imp);
+                                          counts, sp, imp, peer);
         };
         if (U <= 2) go(k_rx_combine_blk<SER, AWGN, 2, 4>, 4);
         else if (U <= 4) go(k_rx_combine_blk<SER, AWGN, 4, 4>, 4);
@@ -661,6 +707,48 @@ int ue_combine(const void* XPA, const void* h_fd, void* yhat, long long n_sym, i
     FD_REQUIRE(aligned8(XPA) && aligned8(h_fd) && aligned8(yhat), "ue_combine: misaligned pointer");
     launch_combine<false, false>((const float2*)XPA, (const float2*)h_fd, (float2*)yhat, B_loc, U, N_d, n_sym, accumulate, nullptr, nullptr, nullptr, SliceParams{}, Impair{}, stream);
     return check_launch("ue_combine");
+}
+
+int ue_combine_peer(const void* XPA, const void* h_fd, void* const* peer_recv, int world, int rank, long long n_sym,
+                    int B_loc, int U, int N_d, cudaStream_t stream) {
+    FD_REQUIRE(world >= 1 && world <= CB_MAX_PEERS && rank >= 0 && rank < world,
+               "ue_combine_peer: world=%d rank=%d (world <= %d)", world, rank, CB_MAX_PEERS);
+    FD_REQUIRE(n_sym >= 0 && n_sym <= 65535 && n_sym % world == 0 && B_loc >= 1 && N_d >= 2 && N_d % 2 == 0,
+               "ue_combine_peer: bad sizes (n_sym must be a multiple of world, N_d even)");
+    FD_REQUIRE(U >= 9 && U <= 32, "ue_combine_peer: U=%d (the fused exchange serves 9 <= U <= 32)", U);
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(XPA && h_fd && peer_recv, "ue_combine_peer: NULL pointer");
+    FD_REQUIRE(aligned16(XPA) && aligned16(h_fd), "ue_combine_peer: XPA / h_fd must be 16-byte aligned");
+    PeerOut peer{};
+    peer.ws = world;
+    peer.rank = rank;
+    peer.nm = (int)(n_sym / world);
+    for (int r = 0; r < world; ++r) {
+        FD_REQUIRE(peer_recv[r] && aligned8(peer_recv[r]), "ue_combine_peer: receive buffer of rank %d missing", r);
+        peer.base[r] = (float2*)peer_recv[r];
+    }
+    launch_combine<false, false>((const float2*)XPA, (const float2*)h_fd, nullptr, B_loc, U, N_d, n_sym, 0, nullptr,
+                                 nullptr, nullptr, SliceParams{}, Impair{}, stream, peer);
+    return check_launch("ue_combine_peer");
+}
+
+int ue_reduce_ser(const void* recv, int world, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,
+                  uint16_t* dec, long long* counts, long long n_sym, int U, int N_d, float boundary_eps,
+                  cudaStream_t stream) {
+    FD_REQUIRE(world >= 1 && world <= CB_MAX_PEERS && n_sym >= 0 && U >= 1 && N_d >= 1, "ue_reduce_ser: bad sizes");
+    SliceParams sp{};
+    if (tx_idx) {
+        int rc = validate_slice(M_qam, alpha, boundary_eps, sp);
+        if (rc) return rc;
+        FD_REQUIRE(counts && aligned8(counts), "ue_reduce_ser: counts missing");
+    }
+    if (n_sym == 0) return FD_OK;
+    FD_REQUIRE(recv && yhat && aligned8(recv) && aligned8(yhat), "ue_reduce_ser: NULL or misaligned pointer");
+    const long long total = n_sym * U * N_d;
+    const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148LL * 16);
+    k_reduce_slots_ser<<<blocks, 256, 0, stream>>>((const float2*)recv, world, (float2*)yhat, tx_idx, dec, counts, total,
+                                                   sp);
+    return check_launch("ue_reduce_ser");
 }
 
 int ue_combine_ser(const void* XPA, const void* h_fd, void* yhat, float alpha, const uint16_t* tx_idx, int M_qam,

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+import torch.multiprocessing  # noqa: F401  (registers the tensor reducers PeerExchange pickles with)
 
 
 def world():
@@ -116,6 +117,84 @@ def reduce_scatter_into(mine: torch.Tensor, partial: torch.Tensor, group=None, h
                                       group=group, async_op=async_op)
 
 
+def peer_slot(n: int, nm: int, rank: int):
+    """Fused Mode A exchange: where rank `rank`'s partial y_hat of world-batch symbol n goes —
+    (owner rank, slot, local symbol) = (n // nm, rank, n % nm) in the owner's receive buffer
+    [world][nm][U][N_d] (include/fdpd.h ue_combine_peer)."""
+    return n // nm, rank, n % nm
+
+
+class PeerExchange:
+    """Receive buffers of the fused Mode A exchange (ue_combine_peer / ue_reduce_ser), one per
+    micro-batch: recv[k] [world][nm][U][N_d] on this rank, and peers[k][r] = rank r's buffer
+    mapped into this process with CUDA IPC (r == rank: the local tensor), so the channel-sum
+    kernel stores its partial sums straight into their owners' memory over NVLink.  The only
+    synchronisation is a stream-ordered barrier between "all ranks stored" and the owner's
+    reduction (no kernel waits on another GPU)."""
+
+    def __init__(self, micro, nm, U, N_d, device, group=None, host_staged=False, dtype=torch.complex64):
+        ws, rank = world()
+        self.ws, self.rank, self.group, self.host_staged = ws, rank, group, host_staged
+        self.recv = [torch.zeros((ws, nm, U, N_d), dtype=dtype, device=device) for _ in range(micro)]
+        self.peers = [[t] for t in self.recv]
+        cpu = torch.device(device).type == "cpu"      # CPU tests: shared-memory tensors stand in for IPC
+        if ws > 1 and cpu:
+            for t in self.recv:
+                t.share_memory_()
+        if ws > 1:
+            # torch's multiprocessing reducers turn a tensor into an IPC handle (CUDA) or a shared-
+            # memory file name (CPU) instead of a copy; the blobs travel through the process group
+            import pickle
+            from multiprocessing.reduction import ForkingPickler
+            every = [None] * ws
+            dist.all_gather_object(every, bytes(ForkingPickler.dumps(self.recv)), group=group)
+            self.peers = [[None] * ws for _ in range(micro)]
+            for r in range(ws):
+                theirs = self.recv if r == rank else pickle.loads(every[r])   # opens rank r's allocations here
+                for k in range(micro):
+                    t = theirs[k]
+                    if not cpu and t.device != torch.device(device) and not torch.cuda.can_device_access_peer(
+                            torch.device(device).index, t.device.index):
+                        raise RuntimeError(f"no peer access from {device} to {t.device}")
+                    self.peers[k][r] = t
+            # first touch through the runtime enables peer access between the two devices
+            for row in self.peers:
+                for t in row:
+                    if t.device != torch.device(device):
+                        t[0, 0, 0, :1].to(device)
+            self._flag = torch.zeros(1, dtype=torch.int32, device=device)
+            self._validate()
+
+    def _validate(self):
+        """Every rank writes a token into its slot of every buffer; after the barrier each rank
+        must see all of them in its own buffers (a mapping that does not reach the owner's memory
+        raises here, before any result depends on it).  Leaves the buffers zeroed."""
+        for k, row in enumerate(self.peers):
+            for t in row:
+                t[self.rank, 0, 0, 0] = float(self.rank + 1 + 16 * k)
+        self.barrier()
+        for k, t in enumerate(self.recv):
+            got = t[:, 0, 0, 0].real.cpu().tolist()
+            want = [float(r + 1 + 16 * k) for r in range(self.ws)]
+            if got != want:
+                raise RuntimeError(f"peer exchange: rank {self.rank} buffer {k} holds {got}, expected {want}")
+        self.barrier()
+        for t in self.recv:
+            t.zero_()
+        self.barrier()
+
+    def barrier(self):
+        """Every rank's stores into this rank's buffers are complete (and vice versa)."""
+        if self.ws == 1:
+            return
+        if self.host_staged:
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+        else:
+            dist.all_reduce(self._flag, group=self.group)          # stream-ordered on NCCL
+
+
 class AntennaShardedStep:
     """Mode A (BASELINE configs[4] "sharded by antenna ... allreduce of per-UE
     received subcarrier signals"), one step over a batch of world x n_per_rank symbols:
@@ -127,6 +206,9 @@ class AntennaShardedStep:
       5. reduce_scatter_tensor (SUM) of the partial received signals: rank r gets the full
          y_hat of its own symbols (the sum over antennas of Eq. 5, split by symbol blocks);
       6. slicing + SER counters on the rank's symbols, int64 counters all-reduced.
+    With `peer` (a PeerExchange) steps 4-5 are one kernel: ue_combine_peer stores every partial
+    sum into slot `rank` of its owner's receive buffer over peer memory while it computes; after
+    a stream-ordered barrier the owner sums the slots in rank order and slices (ue_reduce_ser).
 
     The batch is cut into `micro` micro-batches: with NCCL the collectives of micro-batch k are
     issued asynchronously and waited on just before their consumer, so the all-gather of k
@@ -137,8 +219,9 @@ class AntennaShardedStep:
     `alloc(shape)` allocates a complex buffer on the compute device.  host_staged: gloo on CUDA
     tensors (collectives through host copies; used by the single-GPU 2-rank validation)."""
 
-    def __init__(self, ops, n_per_rank, U, N_d, alloc, micro=2, group=None, host_staged=False):
+    def __init__(self, ops, n_per_rank, U, N_d, alloc, micro=2, group=None, host_staged=False, peer=None):
         self.ops, self.group, self.host_staged = ops, group, host_staged
+        self.peer = peer              # PeerExchange: steps 4-5 fused (partial sums stored at their owners)
         ws, _ = world()
         self.ws = ws
         self.micro = micro if (micro > 1 and n_per_rank % micro == 0) else 1
@@ -166,9 +249,17 @@ class AntennaShardedStep:
             if ag[k] is not None:
                 ag[k].wait()
             self.xpa[k] = self.ops.tx(self.st_all[k], self.xpa[k])
+            if self.peer is not None:                        # partial sums straight into the owners' buffers
+                self.ops.combine_peer(self.xpa[k], self.peer.peers[k], self.peer.rank)
+                continue
             self.ops.combine(self.xpa[k], self.part[k])
             rs[k] = reduce_scatter_into(self.mine[k], self.part[k], self.group, self.host_staged, async_op=asy)
+        if self.peer is not None:
+            self.peer.barrier()
         for k in range(M):                                   # slicing on this rank's symbols
+            if self.peer is not None:                        # sum of the ranks' slots in rank order, then slicing
+                self.ops.reduce_slice(self.peer.recv[k], self.mine[k], idx[k * nm:(k + 1) * nm], counts)
+                continue
             if rs[k] is not None:
                 rs[k].wait()
             self.ops.slice(self.mine[k], idx[k * nm:(k + 1) * nm], counts)

@@ -70,6 +70,8 @@ SIGNATURES = {
     "chain_txrx": (_i, [_vp, _vp, _vp, _vp, _vp, _ip, _i, _i, _i, _ll, _i, _i, _i, _i, _vp]),
     "ue_combine": (_i, [_vp, _vp, _vp, _ll, _i, _i, _i, _i, _vp]),
     "ue_combine_ser": (_i, [_vp, _vp, _vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _i, _f, _vp]),
+    "ue_combine_peer": (_i, [_vp, _vp, C.POINTER(C.c_void_p), _i, _i, _ll, _i, _i, _i, _vp]),
+    "ue_reduce_ser": (_i, [_vp, _i, _vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
     "ue_receive_workspace_bytes": (_sz, [_ll, _i, _i]),
     "ue_receive": (_i, [_vp, _vp, _vp, _vp, _sz, _ll, _i, _i, _i, _i, _i, _vp]),
     "ue_slice_ser": (_i, [_vp, _f, _vp, _i, _vp, _vp, _ll, _i, _i, _f, _vp]),
@@ -463,6 +465,42 @@ def ue_combine(XPA, h_fd, out=None, accumulate=False):
     _check(lib().ue_combine(_ptr(XPA), _ptr(h_fd), _ptr(out), n_sym, B, U, N_d, int(bool(accumulate)),
                             _stream(XPA)))
     return out
+
+
+def ue_combine_peer(XPA, h_fd, peer_recv, rank):
+    """Mode A: the channel sum over this rank's antennas with every partial y_hat stored straight
+    into slot `rank` of its owner's receive buffer (include/fdpd.h ue_combine_peer).  XPA
+    [world * nm][B_loc][N_d]; peer_recv: list of `world` tensors [world][nm][U][N_d] complex64,
+    entry r the (peer-mapped) receive buffer of rank r."""
+    _dev(XPA, torch.complex64, "XPA")
+    _dev(h_fd, torch.complex64, "h_fd")
+    n_sym, B, N_d = XPA.shape
+    U = h_fd.shape[0]
+    ws = len(peer_recv)
+    if n_sym % ws:
+        raise ValueError(f"ue_combine_peer: {n_sym} symbols do not split over {ws} ranks")
+    for t in peer_recv:
+        _dev(t, torch.complex64, "peer_recv")
+        if tuple(t.shape) != (ws, n_sym // ws, U, N_d):
+            raise ValueError(f"ue_combine_peer: receive buffer {tuple(t.shape)} != {(ws, n_sym // ws, U, N_d)}")
+    ptrs = (C.c_void_p * ws)(*[t.data_ptr() for t in peer_recv])
+    _check(lib().ue_combine_peer(_ptr(XPA), _ptr(h_fd), ptrs, ws, int(rank), n_sym, B, U, N_d, _stream(XPA)))
+
+
+def ue_reduce_ser(recv, alpha=1.0, tx_idx=None, M_qam=4, yhat=None, counts=None, dec=None, boundary_eps=1e-4):
+    """Mode A, owner side: y_hat = sum of the `world` slots of recv [world][n][U][N_d] in rank order,
+    then slicing + SER when tx_idx is given (include/fdpd.h ue_reduce_ser).  Returns (yhat, counts, dec)."""
+    _dev(recv, torch.complex64, "recv")
+    ws, n_sym, U, N_d = recv.shape
+    if yhat is None:
+        yhat = torch.empty((n_sym, U, N_d), dtype=torch.complex64, device=recv.device)
+    if tx_idx is not None:
+        _dev(tx_idx, torch.uint16, "tx_idx")
+        if counts is None:
+            counts = torch.zeros(3, dtype=torch.int64, device=recv.device)
+    _check(lib().ue_reduce_ser(_ptr(recv), ws, _ptr(yhat), float(alpha), _ptr(tx_idx), int(M_qam), _ptr(dec),
+                               _ptr(counts), n_sym, U, N_d, float(boundary_eps), _stream(recv)))
+    return yhat, counts, dec
 
 
 def ue_combine_ser(XPA, h_fd, alpha, tx_idx, M_qam, yhat=None, counts=None, dec=None, boundary_eps=1e-4):

@@ -46,6 +46,19 @@ class OracleAntennaOps:
         _, c = O.slice_ser(yhat.numpy(), self.alpha, idx.numpy(), self.cfg.M_qam)
         counts += torch.from_numpy(c)
 
+    # fused exchange (dist.PeerExchange): what ue_combine_peer / ue_reduce_ser do, in numpy
+    def combine_peer(self, y, peers, rank):
+        from paper_2205_05158_b200 import dist as D
+        part = O.ue_receive(y, self.Hfd[:, :, self.b0:self.b0 + self.B_loc], self.cfg.N_d)
+        nm = peers[0].shape[1]
+        for n in range(part.shape[0]):
+            owner, slot, nl = D.peer_slot(n, nm, rank)
+            peers[owner][slot, nl] = torch.from_numpy(part[n])
+
+    def reduce_slice(self, recv, yhat, idx, counts):
+        yhat.copy_(recv.sum(dim=0))
+        self.slice(yhat, idx, counts)
+
 
 def _worker(rank, world, port, mode, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -54,15 +67,20 @@ def _worker(rank, world, port, mode, q):
     from paper_2205_05158_b200 import dist as D
     try:
         cfg = configs.C1
-        if mode == "A_step":
+        if mode in ("A_step", "A_step_peer"):
             per = 4
             syms = D.symbol_range(per, rank)
             inp_all = gen.make_inputs(cfg, range(per * world))
             inp = gen.make_inputs(cfg, syms)
             b0, B_loc = D.antenna_shard(cfg.B, world, rank)
             ops = OracleAntennaOps(cfg, inp_all, b0, B_loc)
+            peer = None
+            if mode == "A_step_peer":      # receive buffers in shared memory, mapped by the other rank
+                mp.set_sharing_strategy("file_system")
+                peer = D.PeerExchange(2, per // 2, cfg.U, cfg.N_d, "cpu", host_staged=True, dtype=torch.complex128)
             step = D.AntennaShardedStep(ops, per, cfg.U, cfg.N_d,
-                                        alloc=lambda sh: torch.zeros(sh, dtype=torch.complex128), micro=2)
+                                        alloc=lambda sh: torch.zeros(sh, dtype=torch.complex128), micro=2,
+                                        host_staged=peer is not None, peer=peer)
             counts = torch.zeros(3, dtype=torch.int64)
             mine = step.step(torch.from_numpy(inp["s"].astype(np.complex128)), torch.from_numpy(inp["idx"]), counts)
             q.put((rank, (np.concatenate([m.numpy() for m in mine]), counts.numpy())))
@@ -135,6 +153,32 @@ def test_antenna_sharded_step_matches_unsharded():
         want = full["yhat"][4 * r:4 * r + 4]
         assert np.max(np.abs(yhat - want)) < 1e-12 * max(1.0, np.max(np.abs(want)))
         assert np.array_equal(counts, full["counts"])
+
+
+def test_antenna_sharded_step_fused_exchange():
+    """The same step with dist.PeerExchange: each rank stores its partial received signals straight
+    into the owner's receive buffer (mapped from the other process: shared memory here, CUDA IPC /
+    NVLink peer memory on GPUs), one barrier, then the owner sums the slots in rank order."""
+    res = _run("A_step_peer")
+    cfg = configs.C1
+    full = O.run_config(cfg, gen.make_inputs(cfg, range(8)))
+    for r in (0, 1):
+        yhat, counts = res[r]
+        want = full["yhat"][4 * r:4 * r + 4]
+        assert np.max(np.abs(yhat - want)) < 1e-12 * max(1.0, np.max(np.abs(want)))
+        assert np.array_equal(counts, full["counts"])
+
+
+def test_peer_slot_covers_every_buffer_once():
+    from paper_2205_05158_b200 import dist as D
+    for ws, nm in ((1, 3), (2, 2), (8, 4)):
+        seen = set()
+        for rank in range(ws):
+            for n in range(ws * nm):
+                owner, slot, nl = D.peer_slot(n, nm, rank)
+                assert 0 <= owner < ws and slot == rank and 0 <= nl < nm
+                seen.add((owner, slot, nl))
+        assert len(seen) == ws * ws * nm
 
 
 def test_split_covers_everything():

@@ -243,11 +243,14 @@ def test_precode_tiles_ragged(F, n, B, U, Nd):
 
 
 @pytest.mark.parametrize("n,B,U,Nd", [(11, 512, 32, 3300), (9, 37, 12, 70), (17, 256, 16, 600), (3, 64, 4, 600),
-                                      (5, 40, 7, 36), (2, 24, 24, 100)])
+                                      (5, 40, 7, 36), (2, 24, 24, 100), (25, 37, 20, 3302), (41, 19, 13, 1998)])
 def test_combine_ser_ragged(F, n, B, U, Nd):
     """Channel sum + slicing (register-blocked kernel for U <= 8, staged tile kernel for
     U = 9..32) on ragged symbol / subcarrier / antenna counts against the oracle einsum and
-    slicer; decisions identical except within 1e-4 of a boundary."""
+    slicer; decisions identical except within 1e-4 of a boundary.  The last two shapes have more
+    tiles than a B200 holds CTAs (296), so whole tiles and the half tiles of the last round run in
+    one launch, with a one-symbol last tile (an empty second half), an odd antenna count (a
+    partial last stage), a subcarrier count off the 32-wide tiles and unused user lanes."""
     rng = np.random.default_rng(n * 131 + U)
     M_qam = 64
     XPA = crandn(rng, n, B, Nd, scale=0.3)
@@ -269,6 +272,68 @@ def test_combine_ser_ragged(F, n, B, U, Nd):
     err_gpu = int((dg != idx).sum())
     assert c[0] == err_gpu
     assert abs(err_gpu - int(c_o[0])) <= int(near.sum())
+
+
+@pytest.mark.parametrize("ws,nm,B,U,Nd", [(1, 5, 24, 16, 200), (3, 4, 30, 32, 132), (2, 40, 9, 12, 1300), (8, 1, 64, 32, 70)])
+def test_combine_peer_exchange(F, ws, nm, B, U, Nd):
+    """Mode A's fused exchange on one GPU: `ws` ranks run one after the other, each with its
+    antenna shard of the world batch, ue_combine_peer storing the partial sums into the owners'
+    receive buffers (all local here); every owner's ue_reduce_ser must then equal the oracle's
+    full channel sum over all antennas (Eq. 5) on its own symbols, decisions element by
+    element outside the 1e-4 band, and untouched slots stay as they were."""
+    from paper_2205_05158_b200 import dist as D
+    rng = np.random.default_rng(ws * 17 + U)
+    M_qam, alpha, n = 16, 0.9, ws * nm
+    XPA = crandn(rng, n, B, Nd, scale=0.3)
+    h = crandn(rng, U, B, Nd, scale=0.3)
+    idx = rng.integers(0, M_qam, size=(n, U, Nd)).astype(np.uint16)
+    want = np.einsum("ubj,nbj->nuj", h.astype(np.complex128), XPA.astype(np.complex128))
+    recv = [torch.full((ws, nm, U, Nd), 7.0 + 3.0j, dtype=torch.complex64, device="cuda") for _ in range(ws)]
+    for r in range(ws):
+        b0, bl = D.antenna_shard(B, ws, r)
+        F.ue_combine_peer(dev(XPA[:, b0:b0 + bl]), dev(h[:, b0:b0 + bl]), recv, r)
+    torch.cuda.synchronize()
+    for owner in range(ws):
+        got = host(recv[owner])
+        for r in range(ws):                                   # slot r holds rank r's partial of the owner's symbols
+            b0, bl = D.antenna_shard(B, ws, r)
+            part = np.einsum("ubj,nbj->nuj", h[:, b0:b0 + bl].astype(np.complex128),
+                             XPA[owner * nm:(owner + 1) * nm, b0:b0 + bl].astype(np.complex128))
+            assert rel(got[r], part) < TOL
+            assert D.peer_slot(owner * nm + nm - 1, nm, r) == (owner, r, nm - 1)
+        sl = slice(owner * nm, (owner + 1) * nm)
+        d_idx = torch.from_numpy(idx[sl].astype(np.int32)).to("cuda").to(torch.uint16)
+        dec = torch.zeros((nm, U, Nd), dtype=torch.uint16, device="cuda")
+        yhat, counts, _ = F.ue_reduce_ser(recv[owner], alpha, d_idx, M_qam, dec=dec)
+        assert rel(host(yhat), want[sl]) < TOL
+        s_slots = host(recv[owner]).astype(np.complex128).sum(axis=0)       # rank order, like the kernel (fp32 there)
+        assert rel(host(yhat), s_slots) < 1e-6
+        dec_o, c_o = O.slice_ser(want[sl], alpha, idx[sl], M_qam)
+        _, near = _near_mask(want[sl], alpha, M_qam)
+        dg = host(dec)
+        assert np.array_equal(dg[~near], dec_o[~near])
+        c = host(counts)
+        assert c[1] == nm * U * Nd and c[0] == int((dg != idx[sl]).sum())
+    y2, c2, _ = F.ue_reduce_ser(recv[0])                      # no slicing: counts untouched / absent
+    assert c2 is None and rel(host(y2), want[:nm]) < TOL
+
+
+def test_combine_unaligned_bases(F):
+    """XPA / h_fd whose bases are 8- but not 16-byte aligned (views one complex64 into a buffer):
+    the tile kernel's 16-byte copies do not apply, the register-blocked kernel takes over."""
+    rng = np.random.default_rng(77)
+    n, B, U, Nd = 9, 24, 16, 200
+    XPA = crandn(rng, n, B, Nd, scale=0.3)
+    h = crandn(rng, U, B, Nd, scale=0.3)
+    want = np.einsum("ubj,nbj->nuj", h.astype(np.complex128), XPA.astype(np.complex128))
+    bx = torch.zeros(XPA.size + 1, dtype=torch.complex64, device="cuda")
+    bh = torch.zeros(h.size + 1, dtype=torch.complex64, device="cuda")
+    bx[1:] = dev(XPA).reshape(-1)
+    bh[1:] = dev(h).reshape(-1)
+    Xv, hv = bx[1:].view(n, B, Nd), bh[1:].view(U, B, Nd)
+    assert Xv.data_ptr() % 16 == 8 and hv.data_ptr() % 16 == 8
+    assert rel(host(F.ue_combine(Xv, hv)), want) < TOL
+    assert rel(host(F.ue_combine(dev(XPA), hv)), want) < TOL
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])

@@ -43,9 +43,14 @@ def main():
     micro = 2 if per % 2 == 0 else 1
     ch = Chain(sh, inp["h_taps"], inp["coef"], inp["params"], device=dev, max_batch=ws * per // micro, b0=b0,
                B_loc=B_loc, precode_math=math)
-    step = D.AntennaShardedStep(AntennaOps(ch), per, cfg.U, cfg.N_d,
+    ops = AntennaOps(ch)
+    peer = None
+    if os.environ.get("MODEA_PEER") == "1":          # fused exchange: partial sums stored through CUDA IPC mappings
+        assert ops.peer_ok(), "fused exchange needs 9 <= U <= 32"
+        peer = D.PeerExchange(micro, per // micro, cfg.U, cfg.N_d, dev, host_staged=True)
+    step = D.AntennaShardedStep(ops, per, cfg.U, cfg.N_d,
                                 alloc=lambda shp: torch.empty(shp, dtype=torch.complex64, device=dev),
-                                micro=micro, host_staged=True)
+                                micro=micro, host_staged=True, peer=peer)
     s = torch.from_numpy(inp["s"]).to(dev)
     idx = torch.from_numpy(inp["idx"]).to(dev)
     counts = torch.zeros(3, dtype=torch.int64, device=dev)
@@ -61,7 +66,7 @@ def main():
     dist.all_reduce(cr)
     torch.cuda.synchronize()
     line = json.dumps({"rank": rank, "world": ws, "config": name, "per_rank": per, "micro": micro, "b0": b0,
-                      "B_loc": B_loc, "precode": math, "yhat_rel_l2_vs_1rank": e, "counts_modeA": counts.cpu().tolist(),
+                      "B_loc": B_loc, "precode": math, "peer": peer is not None, "yhat_rel_l2_vs_1rank": e, "counts_modeA": counts.cpu().tolist(),
                       "counts_1rank": cr.tolist()})
     out = os.environ.get("MODEA_OUT")
     if out:                              # one file per rank (the ranks' stdout interleave)
