@@ -314,7 +314,20 @@ __device__ __forceinline__ void gmp_runs_symbol(float2* __restrict__ buf, float*
         // keep the coefficient-row loads inside the loop (no hoisting into registers)
         asm volatile("" ::: "memory");
         float2 out[R];
-        gmp_run<KP, L, M, R, HALO>(buf, esw, cf, N, rho, out, buf_r, esw_r);
+        if constexpr (HALO) {
+            // Only the first and the last warp-row of runs reach into the partner's half (windows of
+            // at most 16 samples to either side): every other row takes the plain evaluation, whose
+            // window loads are shared-memory loads at fixed offsets instead of generic loads behind a
+            // pointer select per 16-byte chunk (~45 of the run's ~270 non-FFMA2 instructions).  The
+            // choice is warp-uniform, and inside [0, N) both paths load the same values.
+            const int row0 = (rho - (tid & 31)) * R;              // first sample of this warp-row
+            if (row0 < 16 || row0 + 32 * R + 16 > N)
+                gmp_run<KP, L, M, R, true>(buf, esw, cf, N, rho, out, buf_r, esw_r);
+            else
+                gmp_run<KP, L, M, R, false>(buf, esw, cf, N, rho, out);
+        } else {
+            gmp_run<KP, L, M, R, false>(buf, esw, cf, N, rho, out);
+        }
         if (im) {
 #pragma unroll
             for (int i = 0; i < R; ++i) out[i] = pa_impair(out[i], nbase + (unsigned long long)(R * rho + i), *im);
