@@ -630,7 +630,9 @@ __global__ void __launch_bounds__(256) k_conv_out_cl(const float* __restrict__ a
     const int blk = active ? (int)(gi - img * nblk) : 0, by = blk / nbx, bx = blk - by * nbx;
     const int y0 = BS * by, x0 = BS * bx;   // output pixel (y0, x0); haloed rows / cols y0 .. y0 + BS + 1
     const float4* a4 = reinterpret_cast<const float4*>(act + (size_t)img * Wp * Wp * CINP) + gq;
-    float acc[BS][BS][2] = {};
+    float2 acc[BS * BS];                  // (out 0, out 1) of pixel py * BS + px: one FFMA2 per weight pair
+#pragma unroll
+    for (int p = 0; p < BS * BS; ++p) acc[p] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int r = 0; r < BS + 2; ++r) {
         float4 nb[BS + 2];
@@ -652,39 +654,48 @@ __global__ void __launch_bounds__(256) k_conv_out_cl(const float* __restrict__ a
                     const int tap = dy * 3 + dx;
                     const float2 w0 = wsm[(0 * 9 + tap) * G + gq], w1 = wsm[(1 * 9 + tap) * G + gq];
                     const float2 w2 = wsm[(2 * 9 + tap) * G + gq], w3 = wsm[(3 * 9 + tap) * G + gq];
-                    float a0 = acc[py][px][0], a1 = acc[py][px][1];
-                    a0 = fmaf(w0.x, q.x, a0); a1 = fmaf(w0.y, q.x, a1);
-                    a0 = fmaf(w1.x, q.y, a0); a1 = fmaf(w1.y, q.y, a1);
-                    a0 = fmaf(w2.x, q.z, a0); a1 = fmaf(w2.y, q.z, a1);
-                    a0 = fmaf(w3.x, q.w, a0); a1 = fmaf(w3.y, q.w, a1);
-                    acc[py][px][0] = a0;
-                    acc[py][px][1] = a1;
+                    float2 a = acc[py * BS + px];
+                    a = cfma_real(w0, q.x, a);
+                    a = cfma_real(w1, q.y, a);
+                    a = cfma_real(w2, q.z, a);
+                    a = cfma_real(w3, q.w, a);
+                    acc[py * BS + px] = a;
                 }
         }
     }
+    // Reduce-scatter over the group's G lanes: at every level a lane hands one half of its pixels to
+    // its partner and keeps the other (G - 1 exchanges of float2 per lane pair of levels instead of
+    // a full butterfly over all 16 pixels), so each lane ends with the complete sums of 16 / G
+    // pixels and writes them itself.  The order of the additions is fixed by the lane layout.
+    int base = 0;                          // first pixel this lane still holds
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1)
+    for (int o = G / 2, cnt = BS * BS; o > 0; o >>= 1, cnt >>= 1) {
+        const bool hi = (gq & o) != 0;
 #pragma unroll
-        for (int py = 0; py < BS; ++py)
-#pragma unroll
-            for (int px = 0; px < BS; ++px) {
-                acc[py][px][0] += __shfl_xor_sync(0xffffffffu, acc[py][px][0], o);
-                acc[py][px][1] += __shfl_xor_sync(0xffffffffu, acc[py][px][1], o);
-            }
-    if (!active || gq != 0) return;
+        for (int i = 0; i < BS * BS / 2; ++i) {
+            if (i >= cnt / 2) break;
+            const float2 send = hi ? acc[i] : acc[i + cnt / 2];
+            const float2 keep = hi ? acc[i + cnt / 2] : acc[i];
+            float2 recv;
+            recv.x = __shfl_xor_sync(0xffffffffu, send.x, o);
+            recv.y = __shfl_xor_sync(0xffffffffu, send.y, o);
+            acc[i] = fadd2(keep, recv);
+        }
+        base += hi ? cnt / 2 : 0;
+    }
+    if (!active) return;
     const float b0 = bias[0], b1 = bias[1];
 #pragma unroll
-    for (int py = 0; py < BS; ++py)
-#pragma unroll
-        for (int px = 0; px < BS; ++px) {
-            const int y = y0 + py, x = x0 + px;
-            const int k = y * S + x;
-            if (y < S && x < S && k < N_d) {
-                const size_t o = (size_t)img * N_d + k;
-                const float2 z = __ldg(s_in + o);
-                s_out[o] = make_float2(z.x + (acc[py][px][0] + b0), z.y + (acc[py][px][1] + b1));
-            }
+    for (int i = 0; i < BS * BS / G; ++i) {
+        const int p = base + i, py = p / BS, px = p - py * BS;
+        const int y = y0 + py, x = x0 + px;
+        const int k = y * S + x;
+        if (y < S && x < S && k < N_d) {
+            const size_t o = (size_t)img * N_d + k;
+            const float2 z = __ldg(s_in + o);
+            s_out[o] = make_float2(z.x + (acc[i].x + b0), z.y + (acc[i].y + b1));
         }
+    }
 }
 
 // ============================================================================ host side
