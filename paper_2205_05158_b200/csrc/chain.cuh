@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), fft_min_blocks<LOG2N>())
             float2 X[16];
             dft16_sparse_in<+1, PZ>(x0, x1, x14, x15, X);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) usm[pidx(16 * j + r)] = X[r];
+            for (int r = 0; r < 16; ++r) usm[17 * j + r] = X[r];   // = pidx(16 j + r)
         }
         __syncthreads();
         if constexpr (KP > 0) {

@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
+#define FD_FFT_PLAIN_PIDX 1   // see fft.cuh: this kernel is faster with the plain padded indices
 #include "chain.cuh"
 #include "tcgen05.cuh"
 

@@ -20,6 +20,22 @@ namespace fdpd {
 
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int padded_len(int n) { return n + (n >> 4); }
+// pidx(i + c) = pidx(i) + pidx_off(c) whenever the low nibbles of i and c do not carry (c a
+// multiple of 16, or i a multiple of 16 and c < 16): written out, the padded index of a pass
+// position becomes one base per thread plus compile-time offsets — ptxas does not find this by
+// itself and spent a LOP3 + LEA.HI + LEA per shared-memory access on it (a fifth of the
+// instructions of the Ns = 16 pass).
+__host__ __device__ constexpr int pidx_off(int c) { return c + (c >> 4); }
+// FD_FFT_PLAIN_PIDX (defined by chain_cl.cu): keep pidx(position) as written.  The cluster-split
+// chain measured 1.7 % SLOWER with the base + offset form (C5 5.66 -> 5.76 ms; its FFT phases
+// run under the other CTA's GMP, and the different schedule costs more there than the integer
+// instructions saved), the single-CTA chains 1.3 - 2.8 % faster (C2 2.74 -> 2.70 ms, C3 6.65 ->
+// 6.46 ms).
+#ifdef FD_FFT_PLAIN_PIDX
+constexpr bool kPidxBase = false;
+#else
+constexpr bool kPidxBase = true;
+#endif
 
 // multiply by DIR * i
 template <int DIR>
@@ -133,12 +149,20 @@ __host__ __device__ constexpr int fft_min_blocks() { return LOG2N <= 12 ? 3 : (L
 template <int R, int VPT, int T, int N>
 __device__ __forceinline__ int pass_pos(int tid, int q, int r) { return tid + q * T + r * (N / R); }
 
+// Shared-memory slot of pass position (q, r) of thread tid; p0 = pidx(tid).
+template <int R, int VPT, int T, int N>
+__device__ __forceinline__ int pass_slot(int tid, int p0, int q, int r) {
+    if constexpr (kPidxBase && T % 16 == 0 && (N / R) % 16 == 0) return p0 + pidx_off(q * T + r * (N / R));
+    else return pidx(pass_pos<R, VPT, T, N>(tid, q, r));
+}
+
 template <int R, int VPT, int T, int N>
 __device__ __forceinline__ void pass_load_smem(const float2* sm, float2 (&v)[VPT], int tid) {
+    const int p0 = pidx(tid);
 #pragma unroll
     for (int q = 0; q < VPT / R; ++q)
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[q * R + r] = sm[pidx(pass_pos<R, VPT, T, N>(tid, q, r))];
+        for (int r = 0; r < R; ++r) v[q * R + r] = sm[pass_slot<R, VPT, T, N>(tid, p0, q, r)];
 }
 
 // Multiplies v[off + r], r = 1..R-1, by the pass twiddle W^{r step}: the power-of-two
@@ -200,8 +224,16 @@ __device__ __forceinline__ void pass_compute_store(float2* sm, float2 (&v)[VPT],
         else if (Ns > 1) pass_twiddle<R, DIR>(v, q * R, k * (N / (Ns * R)), tw);
         dftR<R, DIR>(v, q * R);
         const int d = (j - k) * R + k;
+        // Ns is a compile-time value after inlining: offsets r Ns are multiples of 16 (Ns >= 16),
+        // or d is a multiple of 16 and r < 16 (first pass, radix 16)
+        if (kPidxBase && ((Ns & 15) == 0 || (Ns == 1 && R == 16))) {
+            const int pd = pidx(d);
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[pidx(d + r * Ns)] = v[q * R + r];
+            for (int r = 0; r < R; ++r) sm[pd + pidx_off(r * Ns)] = v[q * R + r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) sm[pidx(d + r * Ns)] = v[q * R + r];
+        }
     }
 }
 
@@ -229,20 +261,21 @@ __device__ __forceinline__ void fft_run(float2* sm, float2 (&v)[(1 << LOG2N) / f
             constexpr int H = VPT / 2;
             // second half: straight from the pass buffer into the parking slots (8 in flight),
             // then the first half into registers
+            const int p0 = pidx(tid);
 #pragma unroll
             for (int c0 = H; c0 < VPT; c0 += 8) {
                 float2 t[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int x = c0 + e;
-                    t[e] = sm[pidx(pass_pos<R, VPT, T, N>(tid, x / R, x % R))];
+                    t[e] = sm[pass_slot<R, VPT, T, N>(tid, p0, x / R, x % R)];
                 }
 #pragma unroll
                 for (int e = 0; e < 8; ++e) scr[(c0 + e - H) * T + tid] = t[e];
                 asm volatile("" ::: "memory");
             }
 #pragma unroll
-            for (int x = 0; x < H; ++x) v[x] = sm[pidx(pass_pos<R, VPT, T, N>(tid, x / R, x % R))];
+            for (int x = 0; x < H; ++x) v[x] = sm[pass_slot<R, VPT, T, N>(tid, p0, x / R, x % R)];
             __syncthreads();
             pass_compute_store<R, DIR, VPT, T, N, TWOFF, 0, QN / 2>(sm, v, pass_ns<LOG2N>(P), tw, tid);
 #pragma unroll

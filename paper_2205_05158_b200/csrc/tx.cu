@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(fft_threads<LOG2N>(), ofdm_min_blocks<LOG2N>()
             dft16_sparse_in<+1, PZ>(xb[0], PZ == 2 ? xb[1] : make_float2(0.f, 0.f),
                                     PZ == 2 ? xb[NB - 2] : make_float2(0.f, 0.f), xb[NB - 1], Y);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) sm[pidx(16 * j + r)] = Y[r];
+            for (int r = 0; r < 16; ++r) sm[17 * j + r] = Y[r];   // = pidx(16 j + r)
         }
         __syncthreads();
         if constexpr (NPS > 2) fft_run<LOG2N, +1, 1, NPS - 1>(sm, v, tw, tid);
