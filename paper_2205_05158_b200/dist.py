@@ -143,45 +143,64 @@ class PeerExchange:
                 t.share_memory_()
         if ws > 1:
             # torch's multiprocessing reducers turn a tensor into an IPC handle (CUDA) or a shared-
-            # memory file name (CPU) instead of a copy; the blobs travel through the process group
+            # memory file name (CPU) instead of a copy; the blobs travel through the process group.
+            # Every failure below is agreed on by all ranks (_agree) before anyone raises, so the
+            # ranks either all use the exchange or all fall back — never a mix that would deadlock.
             import pickle
             from multiprocessing.reduction import ForkingPickler
+            self._flag = torch.zeros(1, dtype=torch.int32, device=device)
             every = [None] * ws
             dist.all_gather_object(every, bytes(ForkingPickler.dumps(self.recv)), group=group)
-            self.peers = [[None] * ws for _ in range(micro)]
-            for r in range(ws):
-                theirs = self.recv if r == rank else pickle.loads(every[r])   # opens rank r's allocations here
-                for k in range(micro):
-                    t = theirs[k]
-                    if not cpu and t.device != torch.device(device) and not torch.cuda.can_device_access_peer(
-                            torch.device(device).index, t.device.index):
-                        raise RuntimeError(f"no peer access from {device} to {t.device}")
-                    self.peers[k][r] = t
-            # first touch through the runtime enables peer access between the two devices
-            for row in self.peers:
-                for t in row:
-                    if t.device != torch.device(device):
-                        t[0, 0, 0, :1].to(device)
-            self._flag = torch.zeros(1, dtype=torch.int32, device=device)
+            err = None
+            try:
+                self.peers = [[None] * ws for _ in range(micro)]
+                for r in range(ws):
+                    theirs = self.recv if r == rank else pickle.loads(every[r])   # opens rank r's allocations here
+                    for k in range(micro):
+                        t = theirs[k]
+                        if not cpu and t.device != torch.device(device) and not torch.cuda.can_device_access_peer(
+                                torch.device(device).index, t.device.index):
+                            raise RuntimeError(f"no peer access from {device} to {t.device}")
+                        self.peers[k][r] = t
+                # first touch through the runtime enables peer access between the two devices
+                for row in self.peers:
+                    for t in row:
+                        if t.device != torch.device(device):
+                            t[0, 0, 0, :1].to(device)
+            except Exception as e:                         # noqa: BLE001 (reported after the agreement)
+                err = e
+            if not self._agree(err is None):
+                raise RuntimeError(f"peer exchange: mapping the receive buffers failed on some rank ({err})")
             self._validate()
+
+    def _agree(self, ok: bool) -> bool:
+        """True iff `ok` on every rank (all-reduce MIN over the group)."""
+        dev = "cpu" if self.host_staged else self._flag.device
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
 
     def _validate(self):
         """Every rank writes a token into its slot of every buffer; after the barrier each rank
         must see all of them in its own buffers (a mapping that does not reach the owner's memory
-        raises here, before any result depends on it).  Leaves the buffers zeroed."""
+        is caught here, before any result depends on it; all ranks raise together).  Leaves the
+        buffers zeroed."""
         for k, row in enumerate(self.peers):
             for t in row:
                 t[self.rank, 0, 0, 0] = float(self.rank + 1 + 16 * k)
         self.barrier()
+        bad = None
         for k, t in enumerate(self.recv):
             got = t[:, 0, 0, 0].real.cpu().tolist()
             want = [float(r + 1 + 16 * k) for r in range(self.ws)]
             if got != want:
-                raise RuntimeError(f"peer exchange: rank {self.rank} buffer {k} holds {got}, expected {want}")
+                bad = f"rank {self.rank} buffer {k} holds {got}, expected {want}"
         self.barrier()
         for t in self.recv:
             t.zero_()
         self.barrier()
+        if not self._agree(bad is None):
+            raise RuntimeError(f"peer exchange: stores did not reach their owners on some rank ({bad})")
 
     def barrier(self):
         """Every rank's stores into this rank's buffers are complete (and vice versa)."""
